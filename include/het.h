@@ -1,0 +1,168 @@
+/*
+ * het.h — C-ABI of the B200-native HET cached-embedding hot path.
+ *
+ * HET (Miao et al., "HET: Scaling out Huge Embedding Model Training via
+ * Cache-enabled Distributed Framework", arXiv 2112.07221, PVLDB).  Citations
+ * "P:n" are lines of /root/reference/PAPER.md (canonical copy 168-810);
+ * "Rn" are the readings of the paper listed in DESIGN.md.
+ *
+ * One handle = one worker (one GPU, one process).  The worker owns a cache
+ * embedding table in HBM and, with N workers, the 1/N hash shard
+ * of the global embedding table and its global clocks (R15:
+ * owner(k) = k mod N, local row = k div N).
+ *
+ * Pointers: every `keys`, `grads`, `out`, `rows`, `cg` argument may be a
+ * device pointer (cudaMalloc / torch CUDA tensor) or a host pointer (pinned
+ * or pageable); host buffers are staged through library-owned device
+ * buffers with cudaMemcpyAsync on `stream`.  The caller owns its buffers and
+ * keeps them alive until `stream` has completed the call.  Layouts: keys
+ * int64[n]; rows float32[n][D] row-major; clocks uint32[n].
+ *
+ * Streams: all device work is enqueued on `stream` (a cudaStream_t); calls
+ * return without host synchronisation except het_sync, het_stats, the debug
+ * exports and (N > 1) the count exchanges of the all-to-alls.
+ *
+ * Errors: argument/shape/protocol errors are returned synchronously and leave
+ * the cache untouched.  Errors detected on the device (a key outside
+ * [0, rows), cache entries exhausted) abort the rest of that call on the
+ * device, are latched ("sticky"), and are returned by the next het_sync /
+ * het_stats / het_check.
+ *
+ * Collectives: with N > 1, het_lookup, het_update, het_evict, het_sync,
+ * het_read_global and het_dense_allreduce are collective — every rank calls
+ * them in the same order with the same clock (n may differ, including 0).
+ */
+#ifndef HET_H
+#define HET_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct het_cache* het_cache_t;     /* opaque; the library owns all table/cache/hash/comm state */
+typedef struct CUstream_st* het_stream_t;  /* == cudaStream_t */
+
+typedef enum { HET_LFU = 0, HET_LRU = 1 } het_policy_t;
+
+typedef enum {
+  HET_OK = 0,
+  HET_ERR_ARG = 1,        /* bad argument or shape */
+  HET_ERR_KEY_RANGE = 2,  /* a key outside [0, rows) (sticky) */
+  HET_ERR_PROTOCOL = 3,   /* write without matching read */
+  HET_ERR_CAPACITY = 4,   /* cache entries or per-call capacity exhausted */
+  HET_ERR_OOM = 5,
+  HET_ERR_CUDA = 6,
+  HET_ERR_NCCL = 7
+} het_status_t;
+
+#define HET_S_INF 0xFFFFFFFFu  /* s = infinity: no clock checks, every hit valid (R4) */
+
+typedef struct {
+  int rank;                    /* this worker, 0 <= rank < world */
+  int world;                   /* N workers = GPUs */
+  const void* nccl_unique_id;  /* 128-byte ncclUniqueId from het_get_unique_id on rank 0 */
+} het_dist_t;
+
+typedef struct {
+  uint32_t max_keys_per_call;  /* n_max: bound on n for lookup/update/evict (sizes all scratch) */
+  uint64_t init_seed;          /* seed of the initial table W0 (R14); 0 = default 2112072210 */
+  int lfu_persist;             /* 1 (default): LFU counts persist across evictions (R7); 0: reset */
+  int debug_log;               /* reserved */
+} het_opts_t;
+
+typedef struct {
+  uint64_t lookups, keys, unique, hits, exp1, exp2, misses, evictions, dirty_pushes;
+  uint64_t bytes_clock_tx, bytes_clock_rx, bytes_emb_tx, bytes_emb_rx;  /* wire bytes (N > 1) */
+  uint64_t launches;           /* kernels launched by the library so far */
+  uint32_t resident, capacity; /* |cache| and C */
+  int sticky_error;            /* het_status_t latched on the device, 0 = none */
+} het_stats_t;
+
+/* ncclUniqueId (128 bytes) for multi-GPU bootstrap; call on rank 0, broadcast. */
+het_status_t het_get_unique_id(void* out128);
+
+/* Create one worker ("core methods of the HET client library").
+ *   rows       R, keys are int64 in [0, R) (R15); R <= 2^32
+ *   D          embedding dimension, multiple of 4
+ *   cache_frac C = floor(cache_frac * R) cache entries per worker (R10); 0 = no cache
+ *   s          staleness threshold, HET_S_INF = infinity
+ *   policy     LFU or LRU eviction
+ *   dist       NULL for a single worker, else rank/world/ncclUniqueId
+ *   opt        NULL for defaults (n_max = 65536)
+ * Allocates everything up front (no allocation on the hot path) and writes
+ * W0 (R14) with c_g = 0.  Synchronises `stream` before returning. */
+het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint32_t s,
+                              het_policy_t policy, const het_dist_t* dist, const het_opts_t* opt,
+                              het_stream_t stream, het_cache_t* out);
+
+/* Het.Read (Alg. 2) of one mini-batch: dedup,
+ * Cache.Find, CheckValid, Evict(k)+Fetch(k) of expired hits
+ * fused into one sync (R5), Fetch of misses,
+ * LFU/LRU touch, then Cache.Get: out[pos] = cached row of keys[pos]
+ * (lookup semantics P:349-355).  clock_t = the caller's iteration t,
+ * strictly increasing (LRU tick, R8).  out: float32[n][D]. */
+het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t clock_t,
+                        float* out, het_stream_t stream);
+
+/* Het.Write (Alg. 3) for the keys of the immediately preceding
+ * het_lookup (same n; the lookup's dedup is reused): per unique key
+ * acc = sum of grads[pos] in ascending position (R11), delta = -lr * acc,
+ * v += delta, pending += delta, c_c += 1; then the
+ * overflow Evict() (R9).  grads: float32[n][D]. */
+het_status_t het_update(het_cache_t h, const int64_t* keys, uint32_t n, const float* grads,
+                        float lr, het_stream_t stream);
+
+/* Het.Cache.Evict: keys != NULL evicts those keys (pushing
+ * accumulated deltas and c_c to their owner, c_g = max(c_g, c_c)); keys ==
+ * NULL runs the overflow eviction down to C entries. */
+het_status_t het_evict(het_cache_t h, const int64_t* keys, uint32_t n, het_stream_t stream);
+
+/* End-of-run flush (R16): push every dirty entry, empty the cache,
+ * synchronise `stream`, return any sticky device error. */
+het_status_t het_sync(het_cache_t h, het_stream_t stream);
+
+/* Counters since create (synchronises the device). */
+het_status_t het_stats(het_cache_t h, het_stats_t* out);
+
+/* Return the sticky device error without other side effects (synchronises). */
+het_status_t het_check(het_cache_t h);
+
+/* Read global rows W[k] and clocks c_g[k] (inspection/tests).  With N > 1
+ * only keys owned by this rank (k mod N == rank) may be passed. */
+het_status_t het_read_global(het_cache_t h, const int64_t* keys, uint32_t n, float* rows,
+                             uint32_t* cg, het_stream_t stream);
+
+/* Eq. 2 dense synchronisation: buf[0..count) <- mean over the N
+ * workers (NCCL all-reduce sum, then scale by 1/N); identity at N = 1. */
+het_status_t het_dense_allreduce(het_cache_t h, float* buf, uint64_t count, het_stream_t stream);
+
+/* Debug / parity exports of the last call (synchronise `stream`; host or
+ * device destinations).  Unique keys ascending, inverse/perm int32[n],
+ * seg_off int32[U+1], status uint8[U] (0 HIT, 1 EXP1, 2 EXP2, 3 MISS). */
+het_status_t het_debug_lookup_log(het_cache_t h, int64_t* uniq, int32_t* inverse, int32_t* perm,
+                                  int32_t* seg_off, uint8_t* status, uint32_t* U,
+                                  het_stream_t stream);
+/* Victims of the last overflow eviction, ascending key, with dirty flags. */
+het_status_t het_debug_victims(het_cache_t h, int64_t* keys, uint8_t* dirty, uint32_t cap,
+                               uint32_t* e, het_stream_t stream);
+/* Resident entries ascending by key: v/p float32[m][D], clocks, policy primary
+ * (LFU count or LRU tick).  cap bounds m; NULL arrays are skipped. */
+het_status_t het_debug_dump_cache(het_cache_t h, int64_t* keys, float* v, float* p, uint32_t* cs,
+                                  uint32_t* cc, uint32_t* prim, uint32_t cap, uint32_t* m,
+                                  het_stream_t stream);
+
+/* Per-kernel timing with CUDA events on the launching stream (bench). */
+het_status_t het_profile_enable(het_cache_t h, int on);
+/* Fills up to cap (name, total ms, launches) records; returns count in *k. */
+het_status_t het_profile_read(het_cache_t h, char (*names)[32], double* ms, uint64_t* launches,
+                              uint32_t cap, uint32_t* k);
+
+het_status_t het_cache_destroy(het_cache_t h);
+const char* het_last_error(het_cache_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HET_H */

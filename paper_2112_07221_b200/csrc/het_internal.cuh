@@ -1,0 +1,202 @@
+// Internal state and device helpers of libhet (not part of the C-ABI).
+//
+// Layout in HBM (per rank = per worker):
+//   server shard (R15 owner = k mod N, local row = k div N)
+//     W   float[rows_local][D]          global embedding rows this rank owns
+//     cg  u32[rows_local]               global Lamport clocks c_g
+//   worker cache, struct-of-arrays over Ecap = C + 2*n_max entries
+//     ekey i64[Ecap] (-1 = free)  v,p float[Ecap][D]  cs,cc u32[Ecap]
+//     eprim u32[Ecap]  (LFU count or LRU tick: the policy's primary order key)
+//     fstack i32[Ecap] + ctl.ftop       free-entry stack
+//   open-addressing hash (Cache.Find): hkey i64[S], hval i32[S],
+//     S = pow2 >= 4*Ecap, 32-slot aligned windows probed by one warp
+//   count_by_key u32[R]                 persistent LFU counts (R7)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace het {
+
+constexpr uint32_t S_INF = 0xFFFFFFFFu;
+constexpr int64_t HK_EMPTY = -1;
+constexpr int64_t HK_TOMB = -2;
+
+enum : uint8_t { ST_HIT = 0, ST_EXP1 = 1, ST_EXP2 = 2, ST_MISS = 3, ST_NEEDQ = 4 };
+
+// device counters (u64), order shared with het_stats_t
+enum {
+  C_UNIQUE = 0, C_HITS, C_EXP1, C_EXP2, C_MISSES, C_EVICTIONS, C_DIRTY_PUSHES, C_NUM
+};
+
+// small control block in device memory
+struct Ctl {
+  int32_t U;            // unique keys of the current call
+  int32_t ftop;         // free-stack top (number of free entries)
+  int32_t n_tomb;       // tombstones in the hash table
+  int32_t abort;        // current call aborted (sticky error raised)
+  int32_t err;          // sticky error code (het_status_t), 0 = none
+  int32_t rebuild;      // hash rebuild requested for this step
+  // eviction selection state (K8)
+  int64_t need;         // |cache| - C
+  uint32_t base;        // lower bound of all residents' primaries
+  uint32_t T;           // threshold primary
+  int64_t needT;        // victims still needed among prim == T
+  int32_t nvict;        // victims emitted
+  int32_t ncand;        // candidates with prim == T
+  int32_t nsub;         // sub-candidates in key bucket kb1
+  uint32_t kb1;         // key bucket (top bits) of the boundary
+  int64_t need2;        // victims still needed among sub-candidates
+  uint32_t T_last;      // previous eviction threshold (valid lower bound)
+  uint32_t min_install; // min primary among this step's installs
+  int32_t resolved;     // selection resolved (0/1)
+  int32_t pad_;
+  // multi-GPU exchange bookkeeping
+  int32_t nq;           // clock queries built this call
+  int32_t nreq;         // sync/fetch requests built this call
+  int32_t npush;        // eviction pushes built this call
+  int32_t pad2_;
+};
+
+struct Dev {
+  // config
+  int64_t R; uint32_t D; int64_t C; uint32_t s; int policy; int lfu_persist;
+  int rank, world; uint64_t seed0; int kbits;  // bits of R-1
+  // server shard
+  float* W; uint32_t* cg; int64_t rows_local;
+  // cache entries
+  int64_t Ecap; int64_t* ekey; float* v; float* p; uint32_t* cs; uint32_t* cc;
+  uint32_t* eprim; int32_t* fstack;
+  // hash
+  int64_t* hkey; int32_t* hval; int hbits; uint64_t hmask;
+  uint32_t* count_by_key;
+  Ctl* ctl; unsigned long long* cnt;
+};
+
+// Per-call scratch (sized by n_max at create)
+struct Call {
+  int n;                       // occurrences in this call
+  uint64_t t;                  // caller clock (LRU tick)
+  const int64_t* keys;         // [n] device
+  int64_t* uniq;               // [n_max]
+  int32_t* inverse;            // [n_max]
+  int32_t* perm;               // [n_max]
+  int32_t* seg_off;            // [n_max+1]
+  uint8_t* status;             // [n_max]
+  int32_t* uentry;             // [n_max] entry index per unique key
+  uint64_t* sortbuf0;          // [n_max] composite sort buffers (large path)
+  uint64_t* sortbuf1;
+  int32_t* blockbuf;           // block counts for scans
+};
+
+__device__ __forceinline__ uint64_t fmix64(uint64_t x) {
+  x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27; x *= 0x94D049BB133111EBull;
+  x ^= x >> 31; return x;
+}
+
+// R14 initial row value (the CUDA side's own copy of the counter hash)
+__device__ __forceinline__ float init_w0(uint64_t seed0, int64_t k, uint32_t d) {
+  uint64_t h = fmix64(fmix64(fmix64(seed0) ^ (uint64_t)k) ^ (uint64_t)d);
+  int32_t q = (int32_t)(h >> 40) - (1 << 23);
+  return __fmul_rn((float)q, 9.313225746154785e-10f);  // 2^-30, exact
+}
+
+__device__ __forceinline__ uint64_t hash_home(const Dev& s, int64_t key) {
+  uint64_t h = ((uint64_t)key * 0x9E3779B97F4A7C15ull) >> (64 - s.hbits);
+  return h & ~31ull;
+}
+
+__device__ __forceinline__ void raise_err(Ctl* ctl, int code) {
+  atomicCAS(&ctl->err, 0, code);
+  ctl->abort = 1;
+}
+
+// Warp-cooperative probe: all 32 lanes call with the same key; returns the
+// entry index (>= 0) or -1 when absent.  A window of 32 aligned slots is read
+// with one coalesced 256 B load; ballots find a match or an EMPTY slot.
+__device__ __forceinline__ int32_t warp_find(const Dev& s, int64_t key, int lane) {
+  uint64_t w = hash_home(s, key);
+  for (int it = 0; it < (1 << 20); ++it) {
+    uint64_t slot = (w + lane) & s.hmask;
+    int64_t hk = s.hkey[slot];
+    unsigned m = __ballot_sync(0xffffffffu, hk == key);
+    if (m) {
+      int src = __ffs(m) - 1;
+      int32_t val = s.hval[slot];
+      return __shfl_sync(0xffffffffu, val, src);
+    }
+    if (__ballot_sync(0xffffffffu, hk == HK_EMPTY)) return -1;
+    w = (w + 32) & s.hmask;
+  }
+  return -1;
+}
+
+// Warp-cooperative insert of a key known to be absent.  Claims the first
+// EMPTY or TOMB slot in probe order with atomicCAS.
+__device__ __forceinline__ void warp_insert(const Dev& s, int64_t key, int32_t entry, int lane) {
+  uint64_t w = hash_home(s, key);
+  for (;;) {
+    uint64_t slot = (w + lane) & s.hmask;
+    int64_t hk = s.hkey[slot];
+    unsigned m = __ballot_sync(0xffffffffu, hk == HK_EMPTY || hk == HK_TOMB);
+    while (m) {
+      int src = __ffs(m) - 1;
+      int ok = 0;
+      if (lane == src) {
+        unsigned long long old = atomicCAS((unsigned long long*)&s.hkey[slot],
+                                           (unsigned long long)hk, (unsigned long long)key);
+        if (old == (unsigned long long)hk) {
+          s.hval[slot] = entry;
+          if (hk == HK_TOMB) atomicSub(&s.ctl->n_tomb, 1);
+          ok = 1;
+        }
+      }
+      ok = __shfl_sync(0xffffffffu, ok, src);
+      if (ok) return;
+      m &= m - 1;
+    }
+    w = (w + 32) & s.hmask;
+  }
+}
+
+// Warp-cooperative delete: the key is present.
+__device__ __forceinline__ void warp_erase(const Dev& s, int64_t key, int lane) {
+  uint64_t w = hash_home(s, key);
+  for (;;) {
+    uint64_t slot = (w + lane) & s.hmask;
+    int64_t hk = s.hkey[slot];
+    unsigned m = __ballot_sync(0xffffffffu, hk == key);
+    if (m) {
+      if (lane == __ffs(m) - 1) {
+        s.hkey[slot] = HK_TOMB;
+        atomicAdd(&s.ctl->n_tomb, 1);
+      }
+      return;
+    }
+    if (__ballot_sync(0xffffffffu, hk == HK_EMPTY)) return;  // not found (should not happen)
+    w = (w + 32) & s.hmask;
+  }
+}
+
+// warp-aggregated counter increment
+__device__ __forceinline__ void warp_count(unsigned long long* c, bool pred) {
+  unsigned m = __ballot_sync(__activemask(), pred);
+  if (m && (threadIdx.x & 31) == (__ffs(__activemask()) - 1)) atomicAdd(c, (unsigned long long)__popc(m));
+}
+
+// ---------------------------------------------------------------- launchers
+// dedup (K1): returns number of kernel launches issued
+int launch_dedup(const Call& c, int n, int64_t R, int pbits, Ctl* ctl, cudaStream_t st);
+
+// cache kernels (k_cache.cu)
+void launch_init_shard(const Dev& s, cudaStream_t st);
+void launch_reset_cache(const Dev& s, cudaStream_t st);
+void launch_probe(const Dev& s, const Call& c, int n_max_units, cudaStream_t st);
+void launch_sync_fetch_install_local(const Dev& s, const Call& c, int n_units, cudaStream_t st);
+void launch_gather(const Dev& s, const Call& c, float* out, cudaStream_t st);
+void launch_segreduce_apply(const Dev& s, const Call& c, const float* grads, float lr, int n_units,
+                            cudaStream_t st);
+int launch_evict_overflow(const Dev& s, void* evbuf, int n_max, cudaStream_t st);
+void launch_hash_rebuild(const Dev& s, cudaStream_t st);
+
+}  // namespace het

@@ -1,0 +1,26 @@
+// Multi-GPU orchestration (one worker per GPU, hash-sharded server, NCCL
+// all-to-all exchanges over NVLink).  Internal to libhet.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "../../include/het.h"
+#include "het_internal.cuh"
+
+namespace het {
+
+struct MgpuState;
+
+het_status_t mgpu_create(MgpuState*& mg, const Dev& d, uint32_t n_max, const void* uid, cudaStream_t st);
+void mgpu_destroy(MgpuState* mg);
+het_status_t mgpu_lookup(MgpuState* mg, const Dev& d, const Call& c, void* prof, cudaStream_t st);
+het_status_t mgpu_evict_overflow(MgpuState* mg, const Dev& d, void* evbuf, void* prof, cudaStream_t st);
+het_status_t mgpu_evict_keys(MgpuState* mg, const Dev& d, const Call& c, cudaStream_t st);
+het_status_t mgpu_flush(MgpuState* mg, const Dev& d, cudaStream_t st);
+het_status_t mgpu_allreduce_sum(MgpuState* mg, float* buf, uint64_t count, cudaStream_t st);
+void mgpu_bytes(MgpuState* mg, uint64_t* ctx, uint64_t* crx, uint64_t* etx, uint64_t* erx);
+uint64_t mgpu_take_launches(MgpuState* mg);
+
+void* prof_begin(void* h, const char* name, cudaStream_t st);
+void prof_end(void* h, void* rec, cudaStream_t st);
+
+}  // namespace het

@@ -1,0 +1,241 @@
+// K1 dedup: the "unique embedding key set" of a mini-batch (Alg. 1 line 5,
+// PAPER.md:462; §4.2 "remove the duplicate keys") with the inverse
+// index and the stable grouping of positions by key (reading R2: unique keys
+// ascending, positions ascending within a key).
+//
+// Design: every occurrence becomes one 64-bit composite (key << pbits) | pos;
+// composites are distinct, so sorting them is a stable sort of (key, pos).
+//  * n <= 16384: one CTA sorts all composites in shared memory (bitonic),
+//    flags segment heads, block-scans them and writes unique/inverse/perm/
+//    seg_off in the same kernel (one launch).
+//  * larger n: CTA-tile bitonic sorts of 8192 composites, log2(n/8192) merge
+//    passes (each element finds its rank in the partner run by binary
+//    search), then a three-kernel reduce/scan/write for the outputs.
+#include "het_internal.cuh"
+
+namespace het {
+
+constexpr int DD_THREADS = 1024;
+constexpr int DD_SMALL_MAX = 16384;   // 128 KB of composites in smem
+constexpr int TILE = 8192;            // large-path CTA tile
+
+__device__ __forceinline__ void bitonic_smem(uint64_t* a, int npad) {
+  for (int k = 2; k <= npad; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (npad >> 1); i += blockDim.x) {
+        int lo = 2 * j * (i / j) + (i % j);
+        int hi = lo + j;
+        bool up = (lo & k) == 0;
+        uint64_t x = a[lo], y = a[hi];
+        if ((x > y) == up) { a[lo] = y; a[hi] = x; }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// exclusive block scan of one int per thread; returns the exclusive prefix, total in *tot
+__device__ __forceinline__ int block_excl_scan(int x, int* warp_sums, int* tot) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int v = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) warp_sums[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    int w = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) warp_sums[lane] = w;       // inclusive
+  }
+  __syncthreads();
+  int base = wid ? warp_sums[wid - 1] : 0;
+  *tot = warp_sums[nw - 1];
+  __syncthreads();
+  return base + v - x;
+}
+
+__global__ void __launch_bounds__(DD_THREADS, 1)
+k_dedup_small(const int64_t* __restrict__ keys, int n, int64_t R, int pbits, Ctl* ctl,
+              int64_t* uniq, int32_t* inverse, int32_t* perm, int32_t* seg_off) {
+  extern __shared__ uint64_t sm[];
+  __shared__ int warp_sums[32];
+  int npad = 2;
+  while (npad < n) npad <<= 1;
+  int bad = 0;
+  for (int j = threadIdx.x; j < npad; j += blockDim.x) {
+    uint64_t c = ~0ull;
+    if (j < n) {
+      int64_t k = keys[j];
+      if (k < 0 || k >= R) bad = 1;
+      c = ((uint64_t)k << pbits) | (uint64_t)j;
+    }
+    sm[j] = c;
+  }
+  if (__syncthreads_or(bad)) {
+    if (threadIdx.x == 0) { raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/); ctl->U = 0; seg_off[0] = 0; }
+    return;
+  }
+  bitonic_smem(sm, npad);
+  // each thread owns ITEMS consecutive composites
+  int items = (npad + blockDim.x - 1) / blockDim.x;
+  int j0 = threadIdx.x * items;
+  int heads = 0;
+  for (int i = 0; i < items; ++i) {
+    int j = j0 + i;
+    if (j < n && (j == 0 || (sm[j] >> pbits) != (sm[j - 1] >> pbits))) ++heads;
+  }
+  int tot;
+  int u = block_excl_scan(heads, warp_sums, &tot) - 1;
+  for (int i = 0; i < items; ++i) {
+    int j = j0 + i;
+    if (j >= n) break;
+    uint64_t c = sm[j];
+    int64_t k = (int64_t)(c >> pbits);
+    int pos = (int)(c & ((1ull << pbits) - 1));
+    if (j == 0 || k != (int64_t)(sm[j - 1] >> pbits)) {
+      ++u;
+      uniq[u] = k;
+      seg_off[u] = j;
+    }
+    perm[j] = pos;
+    inverse[pos] = u;
+  }
+  if (threadIdx.x == 0) { seg_off[tot] = n; ctl->U = tot; }
+}
+
+// ------------------------------------------------------------- large path
+__global__ void __launch_bounds__(DD_THREADS)
+k_tile_sort(const int64_t* __restrict__ keys, int n, int64_t R, int pbits, Ctl* ctl, uint64_t* out) {
+  extern __shared__ uint64_t sm[];
+  int base = blockIdx.x * TILE;
+  int len = min(TILE, n - base);
+  int bad = 0;
+  for (int j = threadIdx.x; j < TILE; j += blockDim.x) {
+    uint64_t c = ~0ull;
+    if (j < len) {
+      int64_t k = keys[base + j];
+      if (k < 0 || k >= R) bad = 1;
+      c = ((uint64_t)k << pbits) | (uint64_t)(base + j);
+    }
+    sm[j] = c;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) raise_err(ctl, 2);
+  bitonic_smem(sm, TILE);
+  for (int j = threadIdx.x; j < len; j += blockDim.x) out[base + j] = sm[j];
+}
+
+// merge sorted runs of length `width` pairwise: src -> dst
+__global__ void k_merge(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, int n, int width) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int run = i / width;
+  int a0 = (run & ~1) * width;
+  int mid = min(a0 + width, n);
+  int b1 = min(a0 + 2 * width, n);
+  uint64_t x = src[i];
+  int lo, hi;
+  if (i < mid) { lo = mid; hi = b1; }   // element of A: count B elements < x
+  else { lo = a0; hi = mid; }           // element of B: count A elements < x
+  int l = lo, h = hi;
+  while (l < h) {
+    int m = (l + h) >> 1;
+    if (src[m] < x) l = m + 1; else h = m;
+  }
+  int rank = l - lo;
+  int out = (i < mid) ? (i - a0) + rank + a0 : (i - mid) + rank + a0;
+  dst[out] = x;
+}
+
+constexpr int SCAN_BLK = 1024;
+
+__global__ void k_head_count(const uint64_t* __restrict__ c, int n, int pbits, int32_t* blockcnt) {
+  __shared__ int warp_sums[32];
+  int j = blockIdx.x * SCAN_BLK + threadIdx.x;
+  int h = (j < n && (j == 0 || (c[j] >> pbits) != (c[j - 1] >> pbits))) ? 1 : 0;
+  int tot;
+  block_excl_scan(h, warp_sums, &tot);
+  if (threadIdx.x == 0) blockcnt[blockIdx.x] = tot;
+}
+
+__global__ void k_scan_blocks(int32_t* blockcnt, int nb, Ctl* ctl) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
+    int b = b0 + threadIdx.x;
+    int x = b < nb ? blockcnt[b] : 0;
+    int tot;
+    int ex = block_excl_scan(x, warp_sums, &tot);
+    if (b < nb) blockcnt[b] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ctl->U = carry;
+}
+
+__global__ void k_head_write(const uint64_t* __restrict__ c, int n, int pbits, const int32_t* blockoff,
+                             Ctl* ctl, int64_t* uniq, int32_t* inverse, int32_t* perm, int32_t* seg_off) {
+  __shared__ int warp_sums[32];
+  int j = blockIdx.x * SCAN_BLK + threadIdx.x;
+  uint64_t x = j < n ? c[j] : 0;
+  int h = (j < n && (j == 0 || (x >> pbits) != (c[j - 1] >> pbits))) ? 1 : 0;
+  int tot;
+  int ex = block_excl_scan(h, warp_sums, &tot);
+  if (j < n) {
+    int u = blockoff[blockIdx.x] + ex + h - 1;
+    int pos = (int)(x & ((1ull << pbits) - 1));
+    if (h) { uniq[u] = (int64_t)(x >> pbits); seg_off[u] = j; }
+    perm[j] = pos;
+    inverse[pos] = u;
+  }
+  if (j == n - 1) seg_off[ctl->U] = n;
+}
+
+__global__ void k_abort_if_bad(Ctl* ctl, int32_t* seg_off) {
+  if (ctl->abort) { ctl->U = 0; seg_off[0] = 0; }
+}
+
+int launch_dedup(const Call& c, int n, int64_t R, int pbits, Ctl* ctl, cudaStream_t st) {
+  if (n <= DD_SMALL_MAX) {
+    int npad = 2;
+    while (npad < n) npad <<= 1;
+    size_t smem = (size_t)npad * 8;
+    k_dedup_small<<<1, DD_THREADS, smem, st>>>(c.keys, n, R, pbits, ctl, c.uniq, c.inverse, c.perm,
+                                               c.seg_off);
+    return 1;
+  }
+  int launches = 0;
+  int ntiles = (n + TILE - 1) / TILE;
+  k_tile_sort<<<ntiles, DD_THREADS, TILE * 8, st>>>(c.keys, n, R, pbits, ctl, c.sortbuf0);
+  ++launches;
+  uint64_t* a = c.sortbuf0;
+  uint64_t* b = c.sortbuf1;
+  for (int w = TILE; w < n; w <<= 1) {
+    k_merge<<<(n + 255) / 256, 256, 0, st>>>(a, b, n, w);
+    ++launches;
+    uint64_t* t = a; a = b; b = t;
+  }
+  int nb = (n + SCAN_BLK - 1) / SCAN_BLK;
+  k_head_count<<<nb, SCAN_BLK, 0, st>>>(a, n, pbits, c.blockbuf);
+  k_scan_blocks<<<1, 1024, 0, st>>>(c.blockbuf, nb, ctl);
+  k_head_write<<<nb, SCAN_BLK, 0, st>>>(a, n, pbits, c.blockbuf, ctl, c.uniq, c.inverse, c.perm,
+                                        c.seg_off);
+  k_abort_if_bad<<<1, 1, 0, st>>>(ctl, c.seg_off);
+  return launches + 4;
+}
+
+void dedup_set_attrs() {
+  cudaFuncSetAttribute(k_dedup_small, cudaFuncAttributeMaxDynamicSharedMemorySize, DD_SMALL_MAX * 8);
+  cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE * 8);
+}
+
+}  // namespace het

@@ -1,0 +1,300 @@
+"""Thin ctypes binding of libhet.so (include/het.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels of libhet.so.  The functions keep the C names; ``HetCache`` is a small
+convenience wrapper over torch tensors.  There is no CPU fallback: if
+libhet.so is missing this module raises on import of the library.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhet.so")
+
+HET_LFU, HET_LRU = 0, 1
+HET_S_INF = 0xFFFFFFFF
+STATUS = {0: "HET_OK", 1: "HET_ERR_ARG", 2: "HET_ERR_KEY_RANGE", 3: "HET_ERR_PROTOCOL",
+          4: "HET_ERR_CAPACITY", 5: "HET_ERR_OOM", 6: "HET_ERR_CUDA", 7: "HET_ERR_NCCL"}
+HIT, EXP1, EXP2, MISS = 0, 1, 2, 3
+
+
+class HetError(RuntimeError):
+    def __init__(self, code, msg=""):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class het_dist_t(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p)]
+
+
+class het_opts_t(ctypes.Structure):
+    _fields_ = [("max_keys_per_call", ctypes.c_uint32), ("init_seed", ctypes.c_uint64),
+                ("lfu_persist", ctypes.c_int), ("debug_log", ctypes.c_int)]
+
+
+class het_stats_t(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in
+                ["lookups", "keys", "unique", "hits", "exp1", "exp2", "misses", "evictions",
+                 "dirty_pushes", "bytes_clock_tx", "bytes_clock_rx", "bytes_emb_tx", "bytes_emb_rx",
+                 "launches"]] + [("resident", ctypes.c_uint32), ("capacity", ctypes.c_uint32),
+                                 ("sticky_error", ctypes.c_int)]
+
+    def as_dict(self):
+        return {f[0]: int(getattr(self, f[0])) for f in self._fields_}
+
+
+EXPORTS = ["het_get_unique_id", "het_cache_create", "het_lookup", "het_update", "het_evict",
+           "het_sync", "het_stats", "het_check", "het_read_global", "het_dense_allreduce",
+           "het_debug_lookup_log", "het_debug_victims", "het_debug_dump_cache",
+           "het_profile_enable", "het_profile_read", "het_cache_destroy", "het_last_error"]
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, U32, U64, I, F, D = (ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int,
+                            ctypes.c_float, ctypes.c_double)
+    sig = {
+        "het_get_unique_id": [P],
+        "het_cache_create": [U64, U32, D, U32, I, P, P, P, P],
+        "het_lookup": [P, P, U32, U64, P, P],
+        "het_update": [P, P, U32, P, F, P],
+        "het_evict": [P, P, U32, P],
+        "het_sync": [P, P],
+        "het_stats": [P, P],
+        "het_check": [P],
+        "het_read_global": [P, P, U32, P, P, P],
+        "het_dense_allreduce": [P, P, U64, P],
+        "het_debug_lookup_log": [P, P, P, P, P, P, P, P],
+        "het_debug_victims": [P, P, P, U32, P, P],
+        "het_debug_dump_cache": [P, P, P, P, P, P, P, U32, P, P],
+        "het_profile_enable": [P, I],
+        "het_profile_read": [P, P, P, P, U32, P],
+        "het_cache_destroy": [P],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.het_last_error.argtypes = [P]
+    lib.het_last_error.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _ptr(x):
+    """Device or host address of a torch tensor / numpy array / int / None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        assert x.is_contiguous()
+        return x.data_ptr()
+    raise TypeError(type(x))
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_stream().cuda_stream
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _check(h, rc, what):
+    if rc != 0:
+        msg = load().het_last_error(h).decode() if h else ""
+        raise HetError(rc, f"{what}: {msg}")
+
+
+# ----------------------------------------------------------------- C-named wrappers
+def het_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(None, load().het_get_unique_id(buf), "het_get_unique_id")
+    return buf.raw
+
+
+def het_cache_create(rows, D, cache_frac, s, policy=HET_LFU, rank=0, world=1, unique_id=None,
+                     max_keys_per_call=65536, init_seed=0, lfu_persist=1, stream=None):
+    lib = load()
+    dist = None
+    uid = None
+    if world > 1:
+        uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+        dist = het_dist_t(rank, world, ctypes.cast(uid, ctypes.c_void_p))
+    opts = het_opts_t(max_keys_per_call, init_seed, lfu_persist, 0)
+    h = ctypes.c_void_p()
+    rc = lib.het_cache_create(rows, D, cache_frac, s, policy,
+                              ctypes.byref(dist) if dist is not None else None,
+                              ctypes.byref(opts), _stream(stream), ctypes.byref(h))
+    _check(None, rc, "het_cache_create")
+    return h.value
+
+
+def het_lookup(h, keys, n, clock, out, stream=None):
+    _check(h, load().het_lookup(h, _ptr(keys), n, clock, _ptr(out), _stream(stream)), "het_lookup")
+
+
+def het_update(h, keys, n, grads, lr, stream=None):
+    _check(h, load().het_update(h, _ptr(keys), n, _ptr(grads), ctypes.c_float(lr), _stream(stream)),
+           "het_update")
+
+
+def het_evict(h, keys, n, stream=None):
+    _check(h, load().het_evict(h, _ptr(keys), n, _stream(stream)), "het_evict")
+
+
+def het_sync(h, stream=None):
+    _check(h, load().het_sync(h, _stream(stream)), "het_sync")
+
+
+def het_check(h):
+    _check(h, load().het_check(h), "het_check")
+
+
+def het_stats(h) -> dict:
+    st = het_stats_t()
+    _check(h, load().het_stats(h, ctypes.byref(st)), "het_stats")
+    return st.as_dict()
+
+
+def het_read_global(h, keys, n, rows, cg, stream=None):
+    _check(h, load().het_read_global(h, _ptr(keys), n, _ptr(rows), _ptr(cg), _stream(stream)),
+           "het_read_global")
+
+
+def het_dense_allreduce(h, buf, count, stream=None):
+    _check(h, load().het_dense_allreduce(h, _ptr(buf), count, _stream(stream)), "het_dense_allreduce")
+
+
+def het_profile_enable(h, on):
+    _check(h, load().het_profile_enable(h, 1 if on else 0), "het_profile_enable")
+
+
+def het_profile_read(h):
+    cap = 64
+    names = (ctypes.c_char * 32 * cap)()
+    ms = (ctypes.c_double * cap)()
+    cnt = (ctypes.c_uint64 * cap)()
+    k = ctypes.c_uint32()
+    _check(h, load().het_profile_read(h, names, ms, cnt, cap, ctypes.byref(k)), "het_profile_read")
+    return {bytes(names[i]).split(b"\0")[0].decode(): (float(ms[i]), int(cnt[i])) for i in range(k.value)}
+
+
+def het_cache_destroy(h):
+    if h:
+        load().het_cache_destroy(h)
+
+
+# ----------------------------------------------------------------- convenience wrapper
+class HetCache:
+    """One worker's cache (torch tensors in, torch tensors out)."""
+
+    def __init__(self, rows, D, cache_frac, s, policy=HET_LFU, rank=0, world=1, unique_id=None,
+                 max_keys_per_call=65536, init_seed=0, lfu_persist=1):
+        import torch
+        self.torch = torch
+        self.rows, self.D, self.world, self.rank = rows, D, world, rank
+        self.n_max = max_keys_per_call
+        self.h = het_cache_create(rows, D, cache_frac, s, policy, rank, world, unique_id,
+                                  max_keys_per_call, init_seed, lfu_persist)
+
+    def close(self):
+        if self.h:
+            het_cache_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def lookup(self, keys, t, out=None):
+        torch = self.torch
+        n = keys.numel()
+        if out is None:
+            out = torch.empty((n, self.D), dtype=torch.float32, device=keys.device)
+        het_lookup(self.h, keys, n, t, out)
+        return out
+
+    def update(self, keys, grads, lr):
+        het_update(self.h, keys, keys.numel(), grads, lr)
+
+    def evict(self, keys=None):
+        if keys is None:
+            het_evict(self.h, None, 0)
+        else:
+            het_evict(self.h, keys, keys.numel())
+
+    def sync(self):
+        het_sync(self.h)
+
+    def stats(self):
+        return het_stats(self.h)
+
+    def read_global(self, keys):
+        keys = np.ascontiguousarray(np.asarray(keys, np.int64))
+        rows = np.zeros((keys.size, self.D), np.float32)
+        cg = np.zeros(keys.size, np.uint32)
+        het_read_global(self.h, keys, keys.size, rows, cg)
+        return rows, cg
+
+    def lookup_log(self):
+        lib = load()
+        n = self.n_max
+        uniq = np.zeros(n, np.int64)
+        inv = np.zeros(n, np.int32)
+        perm = np.zeros(n, np.int32)
+        seg = np.zeros(n + 1, np.int32)
+        st = np.zeros(n, np.uint8)
+        U = ctypes.c_uint32()
+        _check(self.h, lib.het_debug_lookup_log(self.h, _ptr(uniq), _ptr(inv), _ptr(perm), _ptr(seg),
+                                                _ptr(st), ctypes.byref(U), _stream(None)), "lookup_log")
+        u = U.value
+        return dict(unique=uniq[:u], inverse=inv, perm=perm, seg_off=seg[:u + 1], status=st[:u])
+
+    def victims(self):
+        lib = load()
+        cap = 2 * self.n_max + 1
+        k = np.zeros(cap, np.int64)
+        d = np.zeros(cap, np.uint8)
+        e = ctypes.c_uint32()
+        _check(self.h, lib.het_debug_victims(self.h, _ptr(k), _ptr(d), cap, ctypes.byref(e),
+                                             _stream(None)), "victims")
+        return k[:e.value], d[:e.value]
+
+    def dump_cache(self, cap=1 << 20, rows=True):
+        lib = load()
+        m = ctypes.c_uint32()
+        # size query
+        rc = lib.het_debug_dump_cache(self.h, None, None, None, None, None, None, 0, ctypes.byref(m),
+                                      _stream(None))
+        mm = m.value
+        keys = np.zeros(mm, np.int64)
+        v = np.zeros((mm, self.D), np.float32) if rows else None
+        p = np.zeros((mm, self.D), np.float32) if rows else None
+        cs = np.zeros(mm, np.uint32)
+        cc = np.zeros(mm, np.uint32)
+        prim = np.zeros(mm, np.uint32)
+        _check(self.h, lib.het_debug_dump_cache(self.h, _ptr(keys), _ptr(v), _ptr(p), _ptr(cs), _ptr(cc),
+                                                _ptr(prim), mm, ctypes.byref(m), _stream(None)), "dump")
+        return dict(keys=keys, v=v, p=p, cs=cs, cc=cc, prim=prim)

@@ -1,0 +1,204 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs.  Bar (BASELINE.json north_star): unique/inverse/perm,
+hit/miss/expire decisions, victims and counters bit-exact; rows within 1e-6
+relative (fp32, per-key gradients summed in ascending batch position)."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.oracle import Oracle, capacity, S_INF, LFU, LRU  # noqa: E402
+from workload import gen  # noqa: E402
+
+LR = 0.01
+RTOL = 1e-6
+
+
+def _het():
+    from paper_2112_07221_b200 import het
+    return het
+
+
+def assert_rows(a, b):
+    np.testing.assert_allclose(a, b, rtol=RTOL, atol=1e-30)
+
+
+class Pair:
+    def __init__(self, R, D, frac, s, policy=LFU, persist=1, n_max=4096, track_div=1):
+        het = _het()
+        self.R, self.D = R, D
+        self.o = Oracle(R=R, D=D, C=capacity(frac, R), s=s, policy=policy, lfu_persist=persist,
+                        track_div=track_div)
+        self.g = het.HetCache(R, D, frac, s, policy, max_keys_per_call=n_max, lfu_persist=persist)
+        self.exact_rows = 0
+
+    def step(self, t, keys, grads, check_logs=True, check_victims=True):
+        kd = torch.from_numpy(keys).cuda()
+        out = self.g.lookup(kd, t).cpu().numpy()
+        oo = self.o.lookup(t, [keys])[0]
+        assert_rows(out, oo)
+        self.exact_rows += int((out == oo).all())
+        if check_logs:
+            gl = self.g.lookup_log()
+            ol = self.o.lookup_log(0)
+            n = keys.size
+            assert np.array_equal(gl["unique"], ol["unique"])
+            assert np.array_equal(gl["inverse"][:n], ol["inverse"])
+            assert np.array_equal(gl["perm"][:n], ol["perm"])
+            assert np.array_equal(gl["seg_off"], ol["seg_off"])
+            assert np.array_equal(gl["status"], ol["status"]), (t, np.nonzero(gl["status"] != ol["status"]))
+        if grads is not None:
+            self.g.update(kd, torch.from_numpy(grads).cuda(), LR)
+            self.o.update([grads], LR)
+            if check_victims:
+                gk, gd = self.g.victims()
+                ok, od = self.o.victims(0)
+                order = np.argsort(ok, kind="stable")
+                assert np.array_equal(gk, ok[order]), t
+                assert np.array_equal(gd, od[order]), t
+
+    def compare_stats(self):
+        gs = self.g.stats()
+        os_ = self.o.stats(0)
+        for k in ["lookups", "keys", "unique", "hits", "exp1", "exp2", "misses", "evictions", "dirty_pushes"]:
+            assert gs[k] == os_[k], (k, gs[k], os_[k])
+        assert gs["resident"] == self.o.cache_size(0)
+
+    def compare_cache(self):
+        gc = self.g.dump_cache()
+        oc = self.o.dump_cache(0)
+        assert np.array_equal(gc["keys"], oc["keys"])
+        assert np.array_equal(gc["cs"], oc["cs"])
+        assert np.array_equal(gc["cc"], oc["cc"])
+        prim = oc["count"] if self.g_policy == LFU else oc["tick"]
+        assert np.array_equal(gc["prim"], prim)
+        assert_rows(gc["v"], oc["v"])
+        assert_rows(gc["p"], oc["p"])
+
+    def finish(self):
+        self.g.sync()
+        self.o.flush()
+        keys = np.arange(self.R, dtype=np.int64)
+        gr, gcg = self.g.read_global(keys)
+        orows, ocg = self.o.read_global(keys)
+        assert np.array_equal(gcg, ocg)
+        assert_rows(gr, orows)
+
+
+def toy_keys(t, B=128, i=0):
+    return gen.criteo_keys(i, t, 1, B, gen.cards_for("toy"))[0].numpy()
+
+
+@pytest.mark.parametrize("policy,s,persist,frac", [
+    (LFU, 10, 1, 0.1),       # BASELINE configs[0]
+    (LRU, 10, 1, 0.1),
+    (LFU, 0, 1, 0.1),
+    (LFU, S_INF, 1, 0.1),
+    (LFU, 3, 0, 0.05),
+    (LRU, 100, 1, 0.3),
+    (LFU, 10, 1, 0.0),       # no cache: HET Hybrid mode (R10)
+])
+def test_toy_full_parity(policy, s, persist, frac):
+    R, D, T = 1000, 8, 200
+    p = Pair(R, D, frac, s, policy, persist)
+    p.g_policy = policy
+    for t in range(T):
+        keys = toy_keys(t)
+        grads = gen.grads(0, t, keys.size, D).numpy()
+        p.step(t, keys, grads)
+    p.compare_stats()
+    p.compare_cache()
+    p.finish()
+
+
+def test_ragged_and_degenerate_calls():
+    """n = 0, n = 1, all-duplicate batches, lookup without update, explicit Evict(k)."""
+    R, D = 500, 12
+    p = Pair(R, D, 0.02, 2, LFU)
+    p.g_policy = LFU
+    rng = np.random.default_rng(0)
+    t = 0
+    for n in [0, 1, 5, 3, 0, 64, 1]:
+        keys = rng.integers(0, R, size=n).astype(np.int64)
+        p.step(t, keys, gen.grads(0, t, n, D).numpy()); t += 1
+    keys = np.full(40, 7, np.int64)
+    p.step(t, keys, gen.grads(0, t, 40, D).numpy()); t += 1
+    keys = rng.integers(0, 20, size=30).astype(np.int64)
+    p.step(t, keys, None); t += 1                       # lookup only (no write)
+    p.step(t, keys, gen.grads(0, t, 30, D).numpy()); t += 1
+    ek = np.unique(keys)[:5]
+    p.g.evict(torch.from_numpy(ek).cuda())
+    p.o.evict_keys([ek])
+    for _ in range(20):
+        keys = rng.integers(0, R, size=rng.integers(0, 100)).astype(np.int64)
+        p.step(t, keys, gen.grads(0, t, keys.size, D).numpy()); t += 1
+    p.compare_stats()
+    p.compare_cache()
+    p.finish()
+
+
+def test_large_batch_multi_cta_dedup():
+    """n > 16384 takes the multi-CTA sort/merge dedup path."""
+    R, D = 50000, 4
+    cards = gen.scaled_cards(R)
+    p = Pair(R, D, 0.1, 5, LFU, n_max=40000)
+    p.g_policy = LFU
+    for t in range(6):
+        keys = gen.criteo_keys(0, t, 1, 1500, cards)[0].numpy()   # n = 39000
+        p.step(t, keys, gen.grads(0, t, keys.size, D).numpy())
+    p.compare_stats()
+    p.finish()
+
+
+def test_eviction_slow_paths():
+    """LRU ticks far above the initial base (slow threshold path) and a key
+    bucket with more than 16384 tied candidates (slow sub-select path)."""
+    R, D = 1 << 26, 4
+    p = Pair(R, D, 100 / R, S_INF, LRU, n_max=24000)
+    p.g_policy = LRU
+    t0 = 10 ** 6
+    keys = np.arange(0, 20000, dtype=np.int64)
+    p.step(t0, keys, gen.grads(0, 0, keys.size, D).numpy())
+    p.compare_stats()
+    p2 = Pair(R, D, 100 / R, S_INF, LFU, n_max=24000)
+    p2.g_policy = LFU
+    p2.step(1, keys, gen.grads(0, 0, keys.size, D).numpy())
+    p2.compare_stats()
+    p2.compare_cache()
+
+
+def test_errors_are_reported():
+    het = _het()
+    g = het.HetCache(100, 4, 0.1, 1, max_keys_per_call=64)
+    k = torch.tensor([1, 2, 3], dtype=torch.int64, device="cuda")
+    with pytest.raises(het.HetError) as e:
+        g.update(k, torch.zeros(3, 4, device="cuda"), LR)       # write without read
+    assert e.value.code == 3
+    bad = torch.tensor([1, 100], dtype=torch.int64, device="cuda")
+    g.lookup(bad, 0)
+    with pytest.raises(het.HetError) as e:
+        het.het_check(g.h)
+    assert e.value.code == 2
+    with pytest.raises(het.HetError):
+        g.lookup(torch.zeros(65, dtype=torch.int64, device="cuda"), 1)  # n > n_max
+
+
+def test_host_pointer_path():
+    """Host buffers are staged by the library (the e2e path of bench.py)."""
+    het = _het()
+    R, D = 1000, 8
+    o = Oracle(R=R, D=D, C=capacity(0.1, R), s=10)
+    g = het.HetCache(R, D, 0.1, 10, max_keys_per_call=4096)
+    for t in range(30):
+        keys = toy_keys(t)
+        grads = gen.grads(0, t, keys.size, D).numpy()
+        out = np.zeros((keys.size, D), np.float32)
+        het.het_lookup(g.h, keys, keys.size, t, out)
+        torch.cuda.synchronize()
+        assert_rows(out, o.lookup(t, [keys])[0])
+        het.het_update(g.h, keys, keys.size, grads, LR)
+        o.update([grads], LR)
+    g.sync()
