@@ -1,0 +1,424 @@
+"""Benchmark of the HET cached-embedding hot path on B200 (driver contract).
+
+One *step* = one pass of the whole hot path over one worker-iteration of
+synthetic input: het_lookup (dedup, probe, CheckValid, sync/fetch, gather)
++ het_update (segment-reduce, SGD apply + pending, overflow eviction) and,
+with N > 1, the dense all-reduce of the MLP gradients.
+
+N = 1 workload: BASELINE.json configs[1] "WDL on Criteo-shaped synthetic":
+26 Zipf(0.7) fields, 33,762,577 rows, D = 128, batch 128, cache 10 %,
+s = 100, LFU.  N > 1: configs[3] "DCN", the same per-GPU batch with the
+table hash-sharded over the GPUs (weak scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--sweep]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from workload import gen  # noqa: E402
+
+METRIC = "embedding rows/s (lookup+update)"
+UNIT = "rows/s"
+R_WDL = sum(gen.CRITEO_CARDS)
+CFG = dict(rows=R_WDL, D=128, batch=128, fields=26, cache_frac=0.1, s=100, policy="LFU", alpha=0.7,
+           lr=0.01, dense_params=1 << 20)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, gpu):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def max_over_ranks(x, world, device):
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world, device):
+    if world > 1:
+        torch.distributed.barrier(device_ids=[device.index])
+    torch.cuda.synchronize()
+
+
+# ----------------------------------------------------------------------------- algorithmic bytes
+def algorithmic_bytes(kernel, s, D, n_steps, resident):
+    """Algorithmic bytes per launch of one kernel:
+    the bytes the method must move, from the per-step counters s (totals over
+    n_steps): n occurrences, U unique, m misses, v expired, e evictions."""
+    row = 4 * D
+    n, U = s["keys"] / n_steps, s["unique"] / n_steps
+    m, v = s["misses"] / n_steps, (s["exp1"] + s["exp2"]) / n_steps
+    e, ed = s["evictions"] / n_steps, s["dirty_pushes"] / n_steps
+    if kernel == "dedup":
+        return 8 * n + 8 * n + 12 * U            # keys in; inverse+perm, unique+seg_off out
+    if kernel == "probe":
+        return U * (8 + 12 + 8 + 4 + 8 + 4 + 5)  # key, one slot, clocks, c_g, count r/w, prim, status+entry
+    if kernel == "sync_fetch":
+        return (m + v) * (2 * row + 8) + v * 2 * row   # W read + v write (+ p read, W write for syncs)
+    if kernel == "gather":
+        return U * row + n * row + 4 * n + 4 * U
+    if kernel == "segreduce_apply":
+        return n * row + 4 * n + U * 4 * row + 8 * U
+    if kernel == "evict":
+        return 4 * resident + e * 8 + ed * 3 * row     # one look at every resident's priority + pushes
+    return None
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_gpu(args):
+    from paper_2112_07221_b200 import het
+
+    rank, world, local = dist_env()
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=device)
+    B, D, F = CFG["batch"], CFG["D"], CFG["fields"]
+    n = B * F
+    R = CFG["rows"]
+    lr = CFG["lr"]
+    cards = gen.cards_for("criteo")
+    uid = None
+    if world > 1:
+        obj = [het.het_get_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    cache = het.HetCache(R, D, CFG["cache_frac"], CFG["s"], het.HET_LFU, rank=rank, world=world,
+                         unique_id=uid, max_keys_per_call=n)
+    C = int(math.floor(CFG["cache_frac"] * R))
+
+    # ---- fill: run the hot path until the cache holds C entries (untimed setup)
+    t = 0
+    chunk = 500
+    fill_steps = 0
+    t_fill0 = time.time()
+    while True:
+        keys_blk = gen.criteo_keys(rank, t, chunk, B, cards, CFG["alpha"], device=device)
+        for j in range(chunk):
+            k = keys_blk[j]
+            cache.lookup(k, t)
+            cache.update(k, gen.grads(rank, t, n, D, device=device), lr)
+            t += 1
+        fill_steps += chunk
+        res = cache.stats()["resident"]
+        full = 1.0 if res >= C else 0.0
+        if world > 1:
+            full = -max_over_ranks(-full, world, device)
+        if full >= 1.0 or fill_steps >= 20000:
+            break
+    fill_s = time.time() - t_fill0
+
+    # ---- inputs of the measured steps, resident in HBM before timing
+    W, K = args.warmup, args.steps
+    keys_all = gen.criteo_keys(rank, t, W + 2 * K, B, cards, CFG["alpha"], device=device)
+    grads_all = [gen.grads(rank, t + j, n, D, device=device) for j in range(W + 2 * K)]
+    dense = torch.zeros(CFG["dense_params"], dtype=torch.float32, device=device)
+    dense_src = gen.dense_grads(rank, 0, CFG["dense_params"], device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)   # > 126 MB L2
+    st = torch.cuda.current_stream()
+
+    def step(j):
+        k = keys_all[j]
+        cache.lookup(k, t + j, out=out_buf)
+        cache.update(k, grads_all[j], lr)
+        if world > 1:
+            dense.copy_(dense_src)
+            het.het_dense_allreduce(cache.h, dense, dense.numel())
+
+    out_buf = torch.empty((n, D), dtype=torch.float32, device=device)
+    for j in range(W):
+        step(j)
+    barrier(world, device)
+    s0 = cache.stats()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clk = Clocks(local)
+    barrier(world, device)
+    for j in range(K):
+        flush.fill_(j & 0xFF)
+        ev[j][0].record(st)
+        step(W + j)
+        ev[j][1].record(st)
+    barrier(world, device)
+    clocks = clk.stop()
+    s1 = cache.stats()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    ms = max_over_ranks(ms, world, device)
+    launches = s1["launches"] - s0["launches"]
+    sd = {k: s1[k] - s0[k] for k in ["keys", "unique", "hits", "exp1", "exp2", "misses", "evictions",
+                                     "dirty_pushes", "lookups"]}
+
+    # ---- per-kernel timing pass (events on the launching stream) for the roofline
+    het.het_profile_enable(cache.h, True)
+    het.het_profile_read(cache.h)
+    p0 = cache.stats()
+    for j in range(K):
+        flush.fill_(j & 0xFF)
+        step(W + K + j)
+    torch.cuda.synchronize()
+    prof = het.het_profile_read(cache.h)
+    het.het_profile_enable(cache.h, False)
+    p1 = cache.stats()
+    pd = {k: p1[k] - p0[k] for k in sd}
+    resident = p1["resident"]
+    hbm, peak_kind = peaks()
+    kern = {}
+    for name, (tot_ms, cnt) in prof.items():
+        ab = algorithmic_bytes(name, pd, D, K, resident)
+        avg = tot_ms / max(cnt, 1)
+        kern[name] = dict(ms_per_launch=avg, launches=cnt, share=None,
+                          achieved_gbs=(ab / (avg * 1e-3) / 1e9) if ab else None)
+    tot = sum(v["ms_per_launch"] * v["launches"] for v in kern.values()) or 1.0
+    for v in kern.values():
+        v["share"] = v["ms_per_launch"] * v["launches"] / tot
+    dom = max(kern, key=lambda k: kern[k]["share"]) if kern else None
+    roof = None
+    if dom:
+        a = kern[dom]["achieved_gbs"]
+        roof = {"bound": "hbm", "kernel": dom, "achieved": a, "peak": hbm, "unit": "GB/s",
+                "frac": (a / hbm) if a else None, "traffic": None, "peak_source": peak_kind}
+
+    # ---- e2e: same steps through the C-ABI with host (pinned) buffers
+    keys_h = keys_all[:W + K].cpu().pin_memory()
+    grads_h = [g.cpu().pin_memory() for g in grads_all[:W + K]]
+    out_h = torch.empty((n, D), dtype=torch.float32).pin_memory()
+    te0, te1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tb = t + W + 2 * K
+    for j in range(W):
+        het.het_lookup(cache.h, keys_h[j], n, tb + j, out_h)
+        het.het_update(cache.h, keys_h[j], n, grads_h[j], lr)
+    barrier(world, device)
+    e2e_ms = 0.0
+    for j in range(K):
+        flush.fill_(j & 0xFF)
+        te0.record(st)
+        het.het_lookup(cache.h, keys_h[W + j], n, tb + W + j, out_h)
+        het.het_update(cache.h, keys_h[W + j], n, grads_h[W + j], lr)
+        if world > 1:
+            dense.copy_(dense_src)
+            het.het_dense_allreduce(cache.h, dense, dense.numel())
+        te1.record(st)
+        te1.synchronize()
+        e2e_ms += te0.elapsed_time(te1)
+    e2e_ms = max_over_ranks(e2e_ms / K, world, device)
+
+    value = n * world / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded Zipf Criteo-shaped keys, counter-hash fp32 grads)",
+        "config": {"workload": "WDL" if world == 1 else "DCN", "rows": R, "D": D, "batch_per_gpu": B,
+                   "fields": F, "cache_frac": CFG["cache_frac"], "cache_entries_per_gpu": C,
+                   "s": CFG["s"], "policy": CFG["policy"], "zipf_alpha": CFG["alpha"],
+                   "dense_params": CFG["dense_params"] if world > 1 else 0,
+                   "parallelism": f"hash-sharded table x{world}, dp{world}",
+                   "l2": "flushed between timed steps (256 MB write outside the step events)",
+                   "fill_steps": fill_steps, "fill_s": round(fill_s, 1)},
+        "samples_per_s": B * world / (ms * 1e-3),
+        "unique_rows_per_s": sd["unique"] / K * world / (ms * 1e-3),
+        "step_counters": {k: v / K for k, v in sd.items()},
+        "gpu_launches": int(launches),
+        "launches_per_step": launches / K,
+        "roofline": roof,
+        "kernels": kern,
+        "clocks": clocks,
+        "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": n * 8 + n * D * 4, "d2h_bytes_per_step": n * D * 4},
+    }
+    if args.sweep and world == 1:
+        line["hbm_sweep"] = run_sweep(het, device)
+    cache.close()
+    if rank == 0:
+        line["cpu_baseline"] = cpu_baseline(args)
+    return line, rank, world
+
+
+def run_sweep(het, device):
+    """n-sweep at D = 128 to the bandwidth-bound regime:
+    gather and segreduce_apply %HBM at B in {1024, 8192, 32768}."""
+    res = []
+    hbm, _ = peaks()
+    cards = gen.cards_for("criteo")
+    D = CFG["D"]
+    for B in [1024, 8192, 32768]:
+        n = B * 26
+        c = het.HetCache(CFG["rows"], D, CFG["cache_frac"], CFG["s"], het.HET_LFU, max_keys_per_call=n)
+        t = 0
+        steps = max(8, 40 * 128 // B)
+        keys = gen.criteo_keys(0, 0, steps + 6, B, cards, CFG["alpha"], device=device)
+        g = gen.grads(0, 0, n, D, device=device)
+        for j in range(steps):
+            c.lookup(keys[j], t); c.update(keys[j], g, CFG["lr"]); t += 1
+        het.het_profile_enable(c.h, True)
+        het.het_profile_read(c.h)
+        s0 = c.stats()
+        for j in range(5):
+            c.lookup(keys[steps + j], t); c.update(keys[steps + j], g, CFG["lr"]); t += 1
+        torch.cuda.synchronize()
+        prof = het.het_profile_read(c.h)
+        s1 = c.stats()
+        sd = {k: s1[k] - s0[k] for k in ["keys", "unique", "misses", "exp1", "exp2", "evictions", "dirty_pushes"]}
+        ent = {"batch": B, "n": n}
+        for kname in ["gather", "segreduce_apply", "dedup", "probe", "sync_fetch", "evict"]:
+            if kname in prof:
+                tot, cnt = prof[kname]
+                ab = algorithmic_bytes(kname, sd, D, 5, s1["resident"])
+                avg = tot / cnt
+                ent[kname] = {"ms": avg, "GBs": ab / (avg * 1e-3) / 1e9, "frac": ab / (avg * 1e-3) / 1e9 / hbm}
+        res.append(ent)
+        c.close()
+    return res
+
+
+# ----------------------------------------------------------------------------- oracle legs
+def oracle_sample(steps, warmup):
+    """The CPU oracle (as it stands) on the WDL workload from a cold cache:
+    `warmup` untimed + `steps` timed iterations, full D=128 rows, 1 thread."""
+    from oracle.oracle import Oracle, capacity
+    B, D, F = CFG["batch"], CFG["D"], CFG["fields"]
+    n = B * F
+    R = CFG["rows"]
+    o = Oracle(R=R, D=D, C=capacity(CFG["cache_frac"], R), s=CFG["s"])
+    cards = gen.cards_for("criteo")
+    keys = gen.criteo_keys(0, 0, warmup + steps, B, cards, CFG["alpha"]).numpy()
+    grads = [gen.grads(0, j, n, D).numpy() for j in range(warmup + steps)]
+    for j in range(warmup):
+        o.lookup(j, [keys[j]])
+        o.update([grads[j]], CFG["lr"])
+    t0 = time.perf_counter()
+    for j in range(warmup, warmup + steps):
+        o.lookup(j, [keys[j]])
+        o.update([grads[j]], CFG["lr"])
+    dt = time.perf_counter() - t0
+    return n * steps / dt, dt
+
+
+def cpu_baseline(args, steps=300):
+    v, dt = oracle_sample(steps, 5)
+    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"WDL config, iterations 5..{5 + steps} from a cold cache (full D=128 rows), "
+                      f"single-threaded C++ oracle, {dt:.1f} s; host: {os.cpu_count()} cores, "
+                      f"{_cpu_model()}"}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    v, dt = oracle_sample(args.steps, args.warmup)
+    n = CFG["batch"] * CFG["fields"]
+    ms = dt / args.steps * 1e3
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "WDL" if world == 1 else "DCN", "rows": CFG["rows"], "D": CFG["D"],
+                       "batch_per_gpu": CFG["batch"], "cache_frac": CFG["cache_frac"], "s": CFG["s"],
+                       "policy": CFG["policy"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"first {args.warmup}+{args.steps} WDL iterations from a cold cache, "
+                                       f"single-threaded C++ oracle of the paper's protocol; "
+                                       f"{os.cpu_count()} host cores, {_cpu_model()}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sweep", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        line = run_reference(args)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    line, rank, world = run_gpu(args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,8 +20,7 @@ void dedup_set_attrs();
 void cache_set_attrs();
 size_t evbuf_struct_size();
 void evbuf_init(void* evbuf, uint32_t* hist, uint32_t* khist, int32_t* victims, int32_t* cand,
-                int32_t* sub, int32_t* flags, int64_t* vkeys, uint8_t* vdirty);
-int launch_evict_select(const Dev& s, void* evbuf, cudaStream_t st);
+                int32_t* sub, int32_t* flags, int64_t* vkeys, uint8_t* vdirty, int64_t* vsel);
 }  // namespace het
 
 using namespace het;
@@ -43,6 +43,7 @@ struct het_cache {
   int32_t* victims = nullptr;
   int64_t* victim_keys = nullptr;
   uint8_t* victim_dirty = nullptr;
+  int64_t* victim_sel = nullptr;
   // staging for host pointers (allocated on first use)
   int64_t* stage_keys = nullptr;
   float* stage_rows = nullptr;
@@ -147,28 +148,37 @@ __global__ void k_read_global(Dev s, const int64_t* keys, int n, float* rows, ui
 
 // explicit Evict(key) at N = 1: push if dirty, delete, free
 __global__ void k_evict_keys_local(Dev s, Call c) {
+  __shared__ int dpop[LFU_CB_MAX];
+  dpop_init(dpop);
+  __syncthreads();
   Ctl* ctl = s.ctl;
   int lane = threadIdx.x & 31;
   int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (ctl->abort || u >= ctl->U) return;
-  int64_t key = c.uniq[u];
-  int32_t e = warp_find(s, key, lane);
-  if (e < 0) return;
-  uint32_t ecs = s.cs[e], ecc = s.cc[e];
-  bool dirty = ecc > ecs;
-  if (dirty) {
-    float* Wr = s.W + key * s.D;
-    const float* pr = s.p + (int64_t)e * s.D;
-    for (uint32_t d = lane; d < s.D; d += 32) Wr[d] = __fadd_rn(Wr[d], pr[d]);
-    if (lane == 0) { uint32_t g = s.cg[key]; s.cg[key] = g > ecc ? g : ecc; }
+  if (!ctl->abort && u < ctl->U) {
+    int64_t key = c.uniq[u];
+    int32_t e = warp_find(s, key, lane);
+    if (e >= 0) {
+      uint32_t ecs = s.cs[e], ecc = s.cc[e];
+      bool dirty = ecc > ecs;
+      if (dirty) {
+        float* Wr = s.W + key * s.D;
+        const float* pr = s.p + (int64_t)e * s.D;
+        for (uint32_t d = lane; d < s.D; d += 32) Wr[d] = __fadd_rn(Wr[d], pr[d]);
+        if (lane == 0) { uint32_t g = s.cg[key]; s.cg[key] = g > ecc ? g : ecc; }
+      }
+      warp_erase(s, key, lane);
+      if (lane == 0) {
+        if (s.policy == 0) lfu_move(s, key, s.eprim[e], EP_FREE, dpop);
+        s.eprim[e] = EP_FREE;
+        s.ekey[e] = -1;
+        s.fstack[atomicAdd(&ctl->ftop, 1)] = e;
+        atomicAdd(&s.cnt[C_EVICTIONS], 1ull);
+        if (dirty) atomicAdd(&s.cnt[C_DIRTY_PUSHES], 1ull);
+      }
+    }
   }
-  warp_erase(s, key, lane);
-  if (lane == 0) {
-    s.ekey[e] = -1;
-    s.fstack[atomicAdd(&ctl->ftop, 1)] = e;
-    atomicAdd(&s.cnt[C_EVICTIONS], 1ull);
-    if (dirty) atomicAdd(&s.cnt[C_DIRTY_PUSHES], 1ull);
-  }
+  __syncthreads();
+  dpop_flush(s, dpop);
 }
 
 // het_sync at N = 1: every dirty entry pushes (distinct keys: order-free)
@@ -281,6 +291,19 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   A(d.hkey, (size_t)S);
   A(d.hval, (size_t)S);
   A(d.count_by_key, d.lfu_persist ? rows : 1);
+  d.bm_words = ((int64_t)rows + 31) / 32;
+  d.nbk = ((int64_t)rows + (1 << LFU_BLK_SHIFT) - 1) >> LFU_BLK_SHIFT;
+  d.lfu_cb = 0;
+  if (policy == HET_LFU) {  // count bitmaps, bounded to ~1 GB
+    int cb = LFU_CB_MAX;
+    while (cb > 2 && (double)cb * d.bm_words * 4 > 1.0e9) cb >>= 1;
+    d.lfu_cb = cb;
+    if (const char* env = std::getenv("HET_LFU_CB"))  // test knob: shrink the bitmap window
+      d.lfu_cb = std::max(0, std::min(atoi(env), d.lfu_cb));
+  }
+  A(d.bm, d.lfu_cb ? (size_t)d.lfu_cb * d.bm_words : 1);
+  A(d.bcnt, d.lfu_cb ? (size_t)d.lfu_cb * d.nbk : 1);
+  A(d.pop, LFU_CB_MAX);
   A(d.ctl, 1);
   A(d.cnt, C_NUM);
   {
@@ -302,11 +325,13 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
     A(h->victims, 2 * (size_t)nm + 1);
     A(h->victim_keys, 2 * (size_t)nm + 1);
     A(h->victim_dirty, 2 * (size_t)nm + 1);
+    A(h->victim_sel, 2 * (size_t)nm + 1);
     A(cand, d.Ecap);
     A(sub, d.Ecap);
     A(flags, 4);
     h->evbuf_host = std::malloc(evbuf_struct_size());
-    evbuf_init(h->evbuf_host, hist, khist, h->victims, cand, sub, flags, h->victim_keys, h->victim_dirty);
+    evbuf_init(h->evbuf_host, hist, khist, h->victims, cand, sub, flags, h->victim_keys, h->victim_dirty,
+               h->victim_sel);
     cudaMemsetAsync(hist, 0, 2048 * 4, stream);
     cudaMemsetAsync(khist, 0, 2048 * 4, stream);
     cudaMemsetAsync(flags, 0, 16, stream);
@@ -319,8 +344,12 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   if (d.lfu_persist) cudaMemsetAsync(d.count_by_key, 0, rows * 4, stream);
   cudaMemsetAsync(d.cs, 0, d.Ecap * 4, stream);
   cudaMemsetAsync(d.cc, 0, d.Ecap * 4, stream);
-  cudaMemsetAsync(d.eprim, 0, d.Ecap * 4, stream);
   launch_init_shard(d, stream);
+  if (d.lfu_cb) {
+    cudaMemsetAsync(d.bm, 0, (size_t)d.lfu_cb * d.bm_words * 4, stream);
+    cudaMemsetAsync(d.bcnt, 0, (size_t)d.lfu_cb * d.nbk * 4, stream);
+  }
+  cudaMemsetAsync(d.pop, 0, LFU_CB_MAX * 4, stream);
   launch_reset_cache(d, stream);
   if (world > 1) {
     rc = mgpu_create(h->mg, d, h->n_max, dist->nccl_unique_id, stream);
@@ -406,7 +435,8 @@ static het_status_t evict_overflow(het_cache* h, cudaStream_t st) {
   Dev& d = h->d;
   if (d.world == 1) {
     Prof p(h, "evict", st);
-    h->launches += launch_evict_overflow(d, h->evbuf_host, h->n_max, st);
+    h->launches += launch_evict_select(d, h->evbuf_host, st);
+    h->launches += launch_evict_apply_local(d, h->evbuf_host, st);
   } else {
     het_status_t rc = mgpu_evict_overflow(h->mg, d, h->evbuf_host, h->prof ? (void*)h : nullptr, st);
     if (rc) return rc;
@@ -498,6 +528,11 @@ het_status_t het_sync(het_cache_t h, het_stream_t stream_) {
   }
   launch_reset_cache(d, st);
   h->launches += 1;
+  if (d.lfu_cb) {
+    cudaMemsetAsync(d.bm, 0, (size_t)d.lfu_cb * d.bm_words * 4, st);
+    cudaMemsetAsync(d.bcnt, 0, (size_t)d.lfu_cb * d.nbk * 4, st);
+  }
+  cudaMemsetAsync(d.pop, 0, LFU_CB_MAX * 4, st);
   h->have_lookup = false;
   h->overflow_bound = 0;
   CUDA_TRY(h, cudaGetLastError());

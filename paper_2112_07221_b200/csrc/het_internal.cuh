@@ -20,6 +20,9 @@ namespace het {
 constexpr uint32_t S_INF = 0xFFFFFFFFu;
 constexpr int64_t HK_EMPTY = -1;
 constexpr int64_t HK_TOMB = -2;
+constexpr uint32_t EP_FREE = 0xFFFFFFFFu;  // eprim of a free entry
+constexpr int LFU_CB_MAX = 16;             // LFU count values kept in key bitmaps
+constexpr int LFU_BLK_SHIFT = 12;          // 4096 keys per bitmap block counter
 
 enum : uint8_t { ST_HIT = 0, ST_EXP1 = 1, ST_EXP2 = 2, ST_MISS = 3, ST_NEEDQ = 4 };
 
@@ -49,7 +52,9 @@ struct Ctl {
   uint32_t T_last;      // previous eviction threshold (valid lower bound)
   uint32_t min_install; // min primary among this step's installs
   int32_t resolved;     // selection resolved (0/1)
-  int32_t pad_;
+  int32_t generic;      // run the generic (scan) selection this step
+  int32_t vmode;        // victims list holds 0 = entry indices, 1 = keys
+  int32_t pad3_;
   // multi-GPU exchange bookkeeping
   int32_t nq;           // clock queries built this call
   int32_t nreq;         // sync/fetch requests built this call
@@ -70,6 +75,10 @@ struct Dev {
   int64_t* hkey; int32_t* hval; int hbits; uint64_t hmask;
   uint32_t* count_by_key;
   Ctl* ctl; unsigned long long* cnt;
+  // LFU count bitmaps (P:632 LFU): bit (c, key) set iff
+  // key is resident with count c < lfu_cb; bcnt = set bits per 4096-key block
+  int lfu_cb; int64_t bm_words; int64_t nbk;
+  uint32_t* bm; uint32_t* bcnt; int32_t* pop;
 };
 
 // Per-call scratch (sized by n_max at create)
@@ -178,6 +187,32 @@ __device__ __forceinline__ void warp_erase(const Dev& s, int64_t key, int lane) 
   }
 }
 
+// move a key between LFU count bitmaps (oldc/newc = EP_FREE for none);
+// dpop: block-local population deltas flushed by the caller
+__device__ __forceinline__ void lfu_move(const Dev& s, int64_t key, uint32_t oldc, uint32_t newc, int* dpop) {
+  if (s.lfu_cb == 0 || oldc == newc) return;
+  int64_t w = key >> 5;
+  uint32_t bit = 1u << (key & 31);
+  int64_t blk = key >> LFU_BLK_SHIFT;
+  if (oldc < (uint32_t)s.lfu_cb) {
+    atomicAnd(&s.bm[(int64_t)oldc * s.bm_words + w], ~bit);
+    atomicSub(&s.bcnt[(int64_t)oldc * s.nbk + blk], 1u);
+    atomicSub(&dpop[oldc], 1);
+  }
+  if (newc < (uint32_t)s.lfu_cb) {
+    atomicOr(&s.bm[(int64_t)newc * s.bm_words + w], bit);
+    atomicAdd(&s.bcnt[(int64_t)newc * s.nbk + blk], 1u);
+    atomicAdd(&dpop[newc], 1);
+  }
+}
+
+__device__ __forceinline__ void dpop_init(int* dpop) {
+  if (threadIdx.x < LFU_CB_MAX) dpop[threadIdx.x] = 0;
+}
+__device__ __forceinline__ void dpop_flush(const Dev& s, int* dpop) {
+  if (s.lfu_cb && threadIdx.x < s.lfu_cb && dpop[threadIdx.x]) atomicAdd(&s.pop[threadIdx.x], dpop[threadIdx.x]);
+}
+
 // warp-aggregated counter increment
 __device__ __forceinline__ void warp_count(unsigned long long* c, bool pred) {
   unsigned m = __ballot_sync(__activemask(), pred);
@@ -196,7 +231,8 @@ void launch_sync_fetch_install_local(const Dev& s, const Call& c, int n_units, c
 void launch_gather(const Dev& s, const Call& c, float* out, cudaStream_t st);
 void launch_segreduce_apply(const Dev& s, const Call& c, const float* grads, float lr, int n_units,
                             cudaStream_t st);
-int launch_evict_overflow(const Dev& s, void* evbuf, int n_max, cudaStream_t st);
+int launch_evict_select(const Dev& s, void* evbuf, cudaStream_t st);
+int launch_evict_apply_local(const Dev& s, void* evbuf, cudaStream_t st);
 void launch_hash_rebuild(const Dev& s, cudaStream_t st);
 
 }  // namespace het

@@ -61,53 +61,114 @@ __device__ __forceinline__ int block_excl_scan(int x, int* warp_sums, int* tot) 
   return base + v - x;
 }
 
+// Single-CTA dedup.  E composites per thread held in registers (thread t owns
+// elements [t*E, t*E+E) of the power-of-two padded array).  Bitonic stages
+// with partner distance j < E run inside a thread, E <= j < 32E through warp
+// shuffles, j >= 32E through shared memory; only the last kind needs a
+// __syncthreads (15 of the 78 stages at n = 4096).
+template <int E>
 __global__ void __launch_bounds__(DD_THREADS, 1)
-k_dedup_small(const int64_t* __restrict__ keys, int n, int64_t R, int pbits, Ctl* ctl,
+k_dedup_small(const int64_t* __restrict__ keys, int n, int npad, int64_t R, int pbits, Ctl* ctl,
               int64_t* uniq, int32_t* inverse, int32_t* perm, int32_t* seg_off) {
   extern __shared__ uint64_t sm[];
   __shared__ int warp_sums[32];
-  int npad = 2;
-  while (npad < n) npad <<= 1;
+  __shared__ uint64_t warp_last[32];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  uint64_t r[E];
   int bad = 0;
-  for (int j = threadIdx.x; j < npad; j += blockDim.x) {
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    int j = tid * E + q;
     uint64_t c = ~0ull;
     if (j < n) {
       int64_t k = keys[j];
       if (k < 0 || k >= R) bad = 1;
       c = ((uint64_t)k << pbits) | (uint64_t)j;
     }
-    sm[j] = c;
+    r[q] = c;
   }
   if (__syncthreads_or(bad)) {
-    if (threadIdx.x == 0) { raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/); ctl->U = 0; seg_off[0] = 0; }
+    if (tid == 0) { raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/); ctl->U = 0; seg_off[0] = 0; }
     return;
   }
-  bitonic_smem(sm, npad);
-  // each thread owns ITEMS consecutive composites
-  int items = (npad + blockDim.x - 1) / blockDim.x;
-  int j0 = threadIdx.x * items;
+  for (int k = 2; k <= npad; k <<= 1) {
+    int j = k >> 1;
+    if (j >= 32 * E) {
+#pragma unroll
+      for (int q = 0; q < E; ++q) sm[tid * E + q] = r[q];
+      __syncthreads();
+      for (; j >= 32 * E; j >>= 1) {
+        for (int i = tid; i < (npad >> 1); i += blockDim.x) {
+          int lo = 2 * j * (i / j) + (i % j);
+          int hi = lo + j;
+          bool up = (lo & k) == 0;
+          uint64_t x = sm[lo], y = sm[hi];
+          if ((x > y) == up) { sm[lo] = y; sm[hi] = x; }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int q = 0; q < E; ++q) r[q] = sm[tid * E + q];
+      __syncthreads();
+    }
+    for (; j >= E; j >>= 1) {          // partner in lane ^ (j / E), same register
+      int lm = j / E;
+      bool lower = (tid & lm) == 0;
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        uint64_t x = r[q];
+        uint64_t y = __shfl_xor_sync(0xffffffffu, x, lm);
+        bool up = (((tid * E + q) & k) == 0);
+        bool keep_min = (lower == up);
+        r[q] = keep_min ? (x < y ? x : y) : (x < y ? y : x);
+      }
+    }
+#pragma unroll
+    for (int jj = E / 2; jj > 0; jj >>= 1) {  // inside the thread
+      if (jj > (k >> 1)) continue;
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        if ((q & jj) == 0) {
+          bool up = (((tid * E + q) & k) == 0);
+          uint64_t x = r[q], y = r[q + jj];
+          if ((x > y) == up) { r[q] = y; r[q + jj] = x; }
+        }
+      }
+    }
+  }
+  // segment heads: compare with the previous element (previous thread's last)
+  uint64_t prev = __shfl_up_sync(0xffffffffu, r[E - 1], 1);
+  if (lane == 31) warp_last[tid >> 5] = r[E - 1];
+  __syncthreads();
+  if (lane == 0) prev = (tid >> 5) ? warp_last[(tid >> 5) - 1] : ~0ull;
   int heads = 0;
-  for (int i = 0; i < items; ++i) {
-    int j = j0 + i;
-    if (j < n && (j == 0 || (sm[j] >> pbits) != (sm[j - 1] >> pbits))) ++heads;
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    int j = tid * E + q;
+    uint64_t p = q ? r[q - 1] : prev;
+    if (j < n && (j == 0 || (r[q] >> pbits) != (p >> pbits))) ++heads;
   }
   int tot;
   int u = block_excl_scan(heads, warp_sums, &tot) - 1;
-  for (int i = 0; i < items; ++i) {
-    int j = j0 + i;
-    if (j >= n) break;
-    uint64_t c = sm[j];
-    int64_t k = (int64_t)(c >> pbits);
-    int pos = (int)(c & ((1ull << pbits) - 1));
-    if (j == 0 || k != (int64_t)(sm[j - 1] >> pbits)) {
-      ++u;
-      uniq[u] = k;
-      seg_off[u] = j;
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    int j = tid * E + q;
+    if (j < n) {
+      uint64_t c = r[q];
+      uint64_t p = q ? r[q - 1] : prev;
+      int64_t k = (int64_t)(c >> pbits);
+      int pos = (int)(c & ((1ull << pbits) - 1));
+      if (j == 0 || (c >> pbits) != (p >> pbits)) {
+        ++u;
+        uniq[u] = k;
+        seg_off[u] = j;
+      }
+      perm[j] = pos;
+      inverse[pos] = u;
     }
-    perm[j] = pos;
-    inverse[pos] = u;
   }
-  if (threadIdx.x == 0) { seg_off[tot] = n; ctl->U = tot; }
+  if (tid == 0) { seg_off[tot] = n; ctl->U = tot; }
 }
 
 // ------------------------------------------------------------- large path
@@ -206,11 +267,17 @@ __global__ void k_abort_if_bad(Ctl* ctl, int32_t* seg_off) {
 
 int launch_dedup(const Call& c, int n, int64_t R, int pbits, Ctl* ctl, cudaStream_t st) {
   if (n <= DD_SMALL_MAX) {
-    int npad = 2;
+    int npad = 32;
     while (npad < n) npad <<= 1;
+    int E = npad <= DD_THREADS ? 1 : npad / DD_THREADS;
+    int threads = npad / E;
     size_t smem = (size_t)npad * 8;
-    k_dedup_small<<<1, DD_THREADS, smem, st>>>(c.keys, n, R, pbits, ctl, c.uniq, c.inverse, c.perm,
-                                               c.seg_off);
+    switch (E) {
+#define DD_CASE(EE) case EE: k_dedup_small<EE><<<1, threads, smem, st>>>(c.keys, n, npad, R, pbits, ctl, \
+        c.uniq, c.inverse, c.perm, c.seg_off); break;
+      DD_CASE(1) DD_CASE(2) DD_CASE(4) DD_CASE(8) DD_CASE(16)
+#undef DD_CASE
+    }
     return 1;
   }
   int launches = 0;
@@ -234,7 +301,11 @@ int launch_dedup(const Call& c, int n, int64_t R, int pbits, Ctl* ctl, cudaStrea
 }
 
 void dedup_set_attrs() {
-  cudaFuncSetAttribute(k_dedup_small, cudaFuncAttributeMaxDynamicSharedMemorySize, DD_SMALL_MAX * 8);
+  cudaFuncSetAttribute(k_dedup_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, DD_SMALL_MAX * 8);
+  cudaFuncSetAttribute(k_dedup_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, DD_SMALL_MAX * 8);
+  cudaFuncSetAttribute(k_dedup_small<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, DD_SMALL_MAX * 8);
+  cudaFuncSetAttribute(k_dedup_small<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, DD_SMALL_MAX * 8);
+  cudaFuncSetAttribute(k_dedup_small<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, DD_SMALL_MAX * 8);
   cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, TILE * 8);
 }
 

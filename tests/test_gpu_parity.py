@@ -114,6 +114,22 @@ def test_toy_full_parity(policy, s, persist, frac):
     p.finish()
 
 
+@pytest.mark.parametrize("cb", ["0", "2"])
+def test_lfu_generic_fallback(cb, monkeypatch):
+    """LFU with the count bitmaps disabled (0) or tiny (2): the exact generic
+    selection runs instead of / after the bitmap path."""
+    monkeypatch.setenv("HET_LFU_CB", cb)
+    R, D = 1000, 8
+    p = Pair(R, D, 0.1, 10, LFU, 1)
+    p.g_policy = LFU
+    for t in range(120):
+        keys = toy_keys(t)
+        p.step(t, keys, gen.grads(0, t, keys.size, D).numpy())
+    p.compare_stats()
+    p.compare_cache()
+    p.finish()
+
+
 def test_ragged_and_degenerate_calls():
     """n = 0, n = 1, all-duplicate batches, lookup without update, explicit Evict(k)."""
     R, D = 500, 12
