@@ -58,6 +58,9 @@ typedef enum {
 } het_status_t;
 
 #define HET_S_INF 0xFFFFFFFFu  /* s = infinity: no clock checks, every hit valid (R4) */
+/* clock_t value asking the library for its own device-side iteration counter
+ * (0, 1, 2, ... per lookup): lets a captured CUDA graph of a step be replayed. */
+#define HET_CLOCK_AUTO 0xFFFFFFFFFFFFFFFFull
 
 typedef struct {
   int rank;                    /* this worker, 0 <= rank < world */
@@ -102,7 +105,8 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
  * fused into one sync (R5), Fetch of misses,
  * LFU/LRU touch, then Cache.Get: out[pos] = cached row of keys[pos]
  * (lookup semantics P:349-355).  clock_t = the caller's iteration t,
- * strictly increasing (LRU tick, R8).  out: float32[n][D]. */
+ * strictly increasing (LRU tick, R8), or HET_CLOCK_AUTO.  out: float32[n][D].
+ * Capturable into a CUDA graph (device pointers, HET_CLOCK_AUTO, N = 1). */
 het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t clock_t,
                         float* out, het_stream_t stream);
 

@@ -396,7 +396,8 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
   c.t = clock_t;
   c.keys = keys;
   Dev& d = h->d;
-  cudaMemsetAsync(&d.ctl->abort, 0, 4, st);
+  launch_begin(d, clock_t, (int)n, st);
+  h->launches += 1;
   {
     Prof p(h, "dedup", st);
     h->launches += launch_dedup(c, (int)n, d.R, h->pbits, d.ctl, st);
@@ -426,8 +427,6 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
   h->have_lookup = true;
   h->last_n = n;
   h->overflow_bound += n;
-  h->lookups += 1;
-  h->keys += n;
   return HET_OK;
 }
 
@@ -443,9 +442,11 @@ static het_status_t evict_overflow(het_cache* h, cudaStream_t st) {
     h->launches += mgpu_take_launches(h->mg);
   }
   h->overflow_bound = 0;
-  if ((++h->updates & 63) == 0) {
-    launch_hash_rebuild(d, st);
-    h->launches += 3;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  if (cap == cudaStreamCaptureStatusActive || (++h->updates & 63) == 0) {
+    launch_hash_rebuild(d, st);  // a captured graph re-checks every step
+    h->launches += 2;
   }
   return HET_OK;
 }
@@ -552,8 +553,8 @@ het_status_t het_stats(het_cache_t h, het_stats_t* out) {
   CUDA_TRY(h, cudaMemcpy(cnt, h->d.cnt, sizeof(cnt), cudaMemcpyDeviceToHost));
   CUDA_TRY(h, cudaMemcpy(&ctl, h->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
   std::memset(out, 0, sizeof(*out));
-  out->lookups = h->lookups;
-  out->keys = h->keys;
+  out->lookups = cnt[C_LOOKUPS];
+  out->keys = cnt[C_KEYS];
   out->unique = cnt[C_UNIQUE];
   out->hits = cnt[C_HITS];
   out->exp1 = cnt[C_EXP1];

@@ -28,8 +28,9 @@ enum : uint8_t { ST_HIT = 0, ST_EXP1 = 1, ST_EXP2 = 2, ST_MISS = 3, ST_NEEDQ = 4
 
 // device counters (u64), order shared with het_stats_t
 enum {
-  C_UNIQUE = 0, C_HITS, C_EXP1, C_EXP2, C_MISSES, C_EVICTIONS, C_DIRTY_PUSHES, C_NUM
+  C_UNIQUE = 0, C_HITS, C_EXP1, C_EXP2, C_MISSES, C_EVICTIONS, C_DIRTY_PUSHES, C_LOOKUPS, C_KEYS, C_NUM
 };
+constexpr uint64_t CLOCK_AUTO = ~0ull;   // HET_CLOCK_AUTO: device-side iteration counter
 
 // small control block in device memory
 struct Ctl {
@@ -55,6 +56,8 @@ struct Ctl {
   int32_t generic;      // run the generic (scan) selection this step
   int32_t vmode;        // victims list holds 0 = entry indices, 1 = keys
   int32_t pad3_;
+  uint64_t t_cur;       // clock of the current call (LRU tick)
+  uint64_t t_auto;      // next automatic clock (HET_CLOCK_AUTO)
   // multi-GPU exchange bookkeeping
   int32_t nq;           // clock queries built this call
   int32_t nreq;         // sync/fetch requests built this call
@@ -140,6 +143,25 @@ __device__ __forceinline__ int32_t warp_find(const Dev& s, int64_t key, int lane
   return -1;
 }
 
+// As warp_find, also returning the slot (for an erase without a second probe).
+__device__ __forceinline__ int32_t warp_find_slot(const Dev& s, int64_t key, int lane, uint64_t* slot_out) {
+  uint64_t w = hash_home(s, key);
+  for (int it = 0; it < (1 << 20); ++it) {
+    uint64_t slot = (w + lane) & s.hmask;
+    int64_t hk = s.hkey[slot];
+    unsigned m = __ballot_sync(0xffffffffu, hk == key);
+    if (m) {
+      int src = __ffs(m) - 1;
+      int32_t val = s.hval[slot];
+      *slot_out = __shfl_sync(0xffffffffu, slot, src);
+      return __shfl_sync(0xffffffffu, val, src);
+    }
+    if (__ballot_sync(0xffffffffu, hk == HK_EMPTY)) return -1;
+    w = (w + 32) & s.hmask;
+  }
+  return -1;
+}
+
 // Warp-cooperative insert of a key known to be absent.  Claims the first
 // EMPTY or TOMB slot in probe order with atomicCAS.
 __device__ __forceinline__ void warp_insert(const Dev& s, int64_t key, int32_t entry, int lane) {
@@ -147,22 +169,27 @@ __device__ __forceinline__ void warp_insert(const Dev& s, int64_t key, int32_t e
   for (;;) {
     uint64_t slot = (w + lane) & s.hmask;
     int64_t hk = s.hkey[slot];
-    unsigned m = __ballot_sync(0xffffffffu, hk == HK_EMPTY || hk == HK_TOMB);
-    while (m) {
-      int src = __ffs(m) - 1;
-      int ok = 0;
-      if (lane == src) {
-        unsigned long long old = atomicCAS((unsigned long long*)&s.hkey[slot],
-                                           (unsigned long long)hk, (unsigned long long)key);
-        if (old == (unsigned long long)hk) {
-          s.hval[slot] = entry;
-          if (hk == HK_TOMB) atomicSub(&s.ctl->n_tomb, 1);
-          ok = 1;
+    // prefer tombstones, so EMPTY slots (which end probes) are used up slowly
+    unsigned mt = __ballot_sync(0xffffffffu, hk == HK_TOMB);
+    unsigned me = __ballot_sync(0xffffffffu, hk == HK_EMPTY);
+    for (int pass = 0; pass < 2; ++pass) {
+      unsigned m = pass == 0 ? mt : me;
+      while (m) {
+        int src = __ffs(m) - 1;
+        int ok = 0;
+        if (lane == src) {
+          unsigned long long old = atomicCAS((unsigned long long*)&s.hkey[slot],
+                                             (unsigned long long)hk, (unsigned long long)key);
+          if (old == (unsigned long long)hk) {
+            s.hval[slot] = entry;
+            if (hk == HK_TOMB) atomicSub(&s.ctl->n_tomb, 1);
+            ok = 1;
+          }
         }
+        ok = __shfl_sync(0xffffffffu, ok, src);
+        if (ok) return;
+        m &= m - 1;
       }
-      ok = __shfl_sync(0xffffffffu, ok, src);
-      if (ok) return;
-      m &= m - 1;
     }
     w = (w + 32) & s.hmask;
   }
@@ -213,6 +240,35 @@ __device__ __forceinline__ void dpop_flush(const Dev& s, int* dpop) {
   if (s.lfu_cb && threadIdx.x < s.lfu_cb && dpop[threadIdx.x]) atomicAdd(&s.pop[threadIdx.x], dpop[threadIdx.x]);
 }
 
+// ---------------------------------------------------------------- TMA bulk copy + mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// one bulk (non-tensor) TMA copy global -> shared, completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
 // warp-aggregated counter increment
 __device__ __forceinline__ void warp_count(unsigned long long* c, bool pred) {
   unsigned m = __ballot_sync(__activemask(), pred);
@@ -220,6 +276,7 @@ __device__ __forceinline__ void warp_count(unsigned long long* c, bool pred) {
 }
 
 // ---------------------------------------------------------------- launchers
+void launch_begin(const Dev& s, uint64_t t, int n, cudaStream_t st);
 // dedup (K1): returns number of kernel launches issued
 int launch_dedup(const Call& c, int n, int64_t R, int pbits, Ctl* ctl, cudaStream_t st);
 

@@ -11,6 +11,8 @@
 //                         position), d = -lr*acc, v += d, p += d, c_c += 1
 //                         (R11, R13, R17)
 //   (K8/K9 eviction lives in k_evict.cu)
+#include <algorithm>
+
 #include "het_internal.cuh"
 
 namespace het {
@@ -52,6 +54,20 @@ __global__ void k_reset_cache(Dev s) {
   }
 }
 
+// first kernel of every lookup: reset the per-call abort flag, fix the
+// clock t of this call (the caller's, or the device counter for
+// HET_CLOCK_AUTO so captured CUDA graphs advance it on replay), count it.
+__global__ void k_begin(Dev s, uint64_t t, int n) {
+  Ctl* ctl = s.ctl;
+  ctl->abort = 0;
+  if (t == CLOCK_AUTO) { t = ctl->t_auto; ctl->t_auto = t + 1; }
+  ctl->t_cur = t;
+  s.cnt[C_LOOKUPS] += 1;
+  s.cnt[C_KEYS] += (unsigned long long)n;
+}
+
+void launch_begin(const Dev& s, uint64_t t, int n, cudaStream_t st) { k_begin<<<1, 1, 0, st>>>(s, t, n); }
+
 void launch_init_shard(const Dev& s, cudaStream_t st) {
   k_init_shard<<<148 * 8, 256, 0, st>>>(s);
 }
@@ -75,11 +91,15 @@ k_probe(Dev s, Call c) {
   int U = ctl->U;
   if (!ctl->abort && u < U) {
     int64_t key = c.uniq[u];
+    // issue the count and (N = 1) global-clock loads alongside the hash probe
+    uint32_t cnt = 0, gpre = 0;
+    if (lane == 0 && s.lfu_persist) cnt = s.count_by_key[key];
+    if (lane == 1 && s.world == 1 && s.s != S_INF) gpre = s.cg[key];
     int32_t e = warp_find(s, key, lane);
+    gpre = __shfl_sync(0xffffffffu, gpre, 1);
     if (lane == 0) {
       uint8_t st;
-      uint32_t cnt = 0;
-      if (s.lfu_persist) { cnt = s.count_by_key[key] + 1; s.count_by_key[key] = cnt; }
+      if (s.lfu_persist) { cnt += 1; s.count_by_key[key] = cnt; }
       if (e < 0) {
         st = ST_MISS;
       } else {
@@ -87,7 +107,7 @@ k_probe(Dev s, Call c) {
         if (s.s == S_INF) st = ST_HIT;                      // R4: no clock check
         else if (ecc - ecs > s.s) st = ST_EXP1;             // cond (1) fails
         else if (s.world == 1) {                            // cond (2), c_g read now (R1, R3)
-          uint32_t g = s.cg[key];
+          uint32_t g = gpre;
           st = (g <= ecc || g - ecc <= s.s) ? ST_HIT : ST_EXP2;
         } else st = ST_NEEDQ;                               // ask the owner (C1)
         // L6: LFU count +1 / LRU tick = t for resident entries
@@ -97,7 +117,7 @@ k_probe(Dev s, Call c) {
           s.eprim[e] = newc;
           lfu_move(s, key, oldc, newc, dpop);
         } else {
-          s.eprim[e] = (uint32_t)c.t;
+          s.eprim[e] = (uint32_t)ctl->t_cur;
         }
       }
       c.status[u] = st;
@@ -166,7 +186,7 @@ __device__ __forceinline__ void sync_fetch_local_body(Dev& s, Call& c, int* dpop
     g = s.cg[row];
     if (lane == 0) {
       s.ekey[e] = key;
-      uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)c.t;
+      uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
       s.eprim[e] = prim;
       if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
       atomicMin(&ctl->min_install, prim);
@@ -224,57 +244,134 @@ void launch_gather(const Dev& s, const Call& c, float* out, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ K7 segment-reduce + apply
-__global__ void __launch_bounds__(TPB)
-k_segreduce_apply(Dev s, Call c, const float* __restrict__ G, float lr) {
+// Heavy keys (many occurrences in the batch, e.g. the top id of a 3-value
+// Criteo field appears ~60 times in 128 samples) would serialise one row load
+// per occurrence.  Their gradient rows are staged into shared memory with TMA
+// bulk copies (cp.async.bulk, one 4D-byte row per lane, all in flight on one
+// mbarrier), then summed in ascending position from shared memory.
+constexpr int SR_WARPS = 4;
+
+__global__ void __launch_bounds__(SR_WARPS * 32)
+k_segreduce_apply(Dev s, Call c, const float* __restrict__ G, float lr, int stage_rows) {
+  extern __shared__ float4 stg[];                 // [SR_WARPS][stage_rows + 1][D4]
+  __shared__ uint64_t bars[SR_WARPS];
   Ctl* ctl = s.ctl;
-  int lane = threadIdx.x & 31;
-  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int u = blockIdx.x * SR_WARPS + wid;
   if (ctl->abort || u >= ctl->U) return;
-  int32_t e = c.uentry[u];
-  int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
-  bool dirty = s.cc[e] > s.cs[e];
+  // independent loads first: segment bounds, entry, clocks, positions
+  const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
+  const int32_t e = c.uentry[u];
+  const uint32_t ecc = s.cc[e], ecs = s.cs[e];
+  const int cnt = j1 - j0;
+  const int pos_lane = lane < cnt ? __ldg(&c.perm[j0 + lane]) : 0;
+  const bool dirty = ecc > ecs;
   const int D4 = s.D >> 2;
   const float nlr = -lr;
   float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
   float4* pr = reinterpret_cast<float4*>(s.p + (int64_t)e * s.D);
   const float4* G4 = reinterpret_cast<const float4*>(G);
-  for (int d = lane; d < D4; d += 32) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);       // U1: +0.0f, ascending position
-    for (int j = j0; j < j1; ++j) {
-      int pos = __ldg(&c.perm[j]);
-      acc = f4add(acc, __ldcs(G4 + (int64_t)pos * D4 + d));
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (stage_rows > 0 && cnt > 4) {
+    // ---- staged path
+    float4* mystg = stg + (size_t)wid * (stage_rows + 1) * D4;
+    float4* accrow = mystg + (size_t)stage_rows * D4;
+    uint64_t* bar = &bars[wid];
+    if (lane == 0) { mbar_init(bar, 1); fence_mbar_init(); }
+    __syncwarp();
+    uint32_t phase = 0;
+    const uint32_t rowbytes = s.D * 4;
+    for (int kb = 0; kb < cnt; kb += stage_rows) {
+      const int m = min(stage_rows, cnt - kb);
+      const int src = kb == 0 ? pos_lane : (kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0);
+      __syncwarp();
+      fence_proxy_async();
+      if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)m * rowbytes);
+      __syncwarp();
+      if (lane < m) bulk_g2s(mystg + (size_t)lane * D4, G4 + (int64_t)src * D4, rowbytes, bar);
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      for (int d = lane; d < D4; d += 32) {
+        float4 a = kb ? accrow[d] : zero;
+        for (int k = 0; k < m; ++k) a = f4add(a, mystg[(size_t)k * D4 + d]);
+        accrow[d] = a;
+      }
     }
-    float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
-                            __fmul_rn(nlr, acc.w));  // U2: delta = (-lr) * acc
-    vr[d] = f4add(vr[d], dl);
-    pr[d] = dirty ? f4add(pr[d], dl) : f4add(make_float4(0.f, 0.f, 0.f, 0.f), dl);
+    __syncwarp();
+    for (int d = lane; d < D4; d += 32) {
+      float4 acc = accrow[d];
+      float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
+                              __fmul_rn(nlr, acc.w));
+      vr[d] = f4add(vr[d], dl);
+      pr[d] = f4add(dirty ? pr[d] : zero, dl);
+    }
+  } else {
+    // ---- register path: up to 4 independent row loads in flight
+    for (int d = lane; d - lane < D4; d += 32) {
+      const bool act = d < D4;
+      float4 vv = act ? vr[d] : zero;
+      float4 pp = (act && dirty) ? pr[d] : zero;
+      float4 acc = zero;                              // U1: +0.0f, ascending position
+      for (int kb = 0; kb < cnt; kb += 32) {
+        const int src = kb == 0 ? pos_lane : (kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0);
+        const int m = min(32, cnt - kb);
+        int k = 0;
+        for (; k + 4 <= m; k += 4) {
+          int p0 = __shfl_sync(0xffffffffu, src, k), p1 = __shfl_sync(0xffffffffu, src, k + 1);
+          int p2 = __shfl_sync(0xffffffffu, src, k + 2), p3 = __shfl_sync(0xffffffffu, src, k + 3);
+          if (act) {
+            float4 g0 = __ldcs(G4 + (int64_t)p0 * D4 + d), g1 = __ldcs(G4 + (int64_t)p1 * D4 + d);
+            float4 g2 = __ldcs(G4 + (int64_t)p2 * D4 + d), g3 = __ldcs(G4 + (int64_t)p3 * D4 + d);
+            acc = f4add(acc, g0); acc = f4add(acc, g1); acc = f4add(acc, g2); acc = f4add(acc, g3);
+          }
+        }
+        for (; k < m; ++k) {
+          int p0 = __shfl_sync(0xffffffffu, src, k);
+          if (act) acc = f4add(acc, __ldcs(G4 + (int64_t)p0 * D4 + d));
+        }
+      }
+      if (act) {
+        float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
+                                __fmul_rn(nlr, acc.w));  // U2: delta = (-lr) * acc
+        vr[d] = f4add(vv, dl);
+        pr[d] = f4add(pp, dl);                           // clean: fl(+0 + delta) (R13)
+      }
+    }
   }
-  __syncwarp();
-  if (lane == 0) s.cc[e] = s.cc[e] + 1;  // Cache.Clock
+  if (lane == 0) s.cc[e] = ecc + 1;  // Cache.Clock
 }
 
 void launch_segreduce_apply(const Dev& s, const Call& c, const float* grads, float lr, int n_units,
                             cudaStream_t st) {
-  int blocks = (n_units + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
+  int blocks = (n_units + SR_WARPS - 1) / SR_WARPS;
   if (blocks < 1) blocks = 1;
-  k_segreduce_apply<<<blocks, TPB, 0, st>>>(s, c, grads, lr);
+  const int rowbytes = (int)s.D * 4;
+  int stage_rows = std::min(32, 12288 / rowbytes);   // <= 48 KB of staging per block
+  if (stage_rows < 4) stage_rows = 0;                  // wide rows: column parallelism suffices
+  size_t smem = stage_rows ? (size_t)SR_WARPS * (stage_rows + 1) * rowbytes : 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_segreduce_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
+  }
+  k_segreduce_apply<<<blocks, SR_WARPS * 32, smem, st>>>(s, c, grads, lr, stage_rows);
 }
 
 // ------------------------------------------------------------------ hash rebuild
-__global__ void k_rebuild_decide(Dev s) {
-  Ctl* ctl = s.ctl;
-  int64_t S = (int64_t)s.hmask + 1;
-  ctl->rebuild = (int64_t)ctl->n_tomb > S / 8 ? 1 : 0;
-  if (ctl->rebuild) ctl->n_tomb = 0;
-}
+// Hash maintenance: when tombstones exceed S/8 the table is rebuilt from the
+// resident entries.  Every block of k_rebuild_clear takes the same decision
+// from n_tomb (unchanged during the kernel); k_rebuild_insert reads it back.
 __global__ void k_rebuild_clear(Dev s) {
-  if (!s.ctl->rebuild) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= (int64_t)s.hmask;
-       i += (int64_t)gridDim.x * blockDim.x)
+  const int64_t S = (int64_t)s.hmask + 1;
+  const bool go = (int64_t)s.ctl->n_tomb > S / 8;
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->rebuild = go ? 1 : 0;
+  if (!go) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x)
     s.hkey[i] = HK_EMPTY;
 }
 __global__ void k_rebuild_insert(Dev s) {
   if (!s.ctl->rebuild) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->n_tomb = 0;
   int lane = threadIdx.x & 31;
   int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nw = (gridDim.x * blockDim.x) >> 5;
@@ -292,7 +389,6 @@ __global__ void k_rebuild_insert(Dev s) {
 }
 
 void launch_hash_rebuild(const Dev& s, cudaStream_t st) {
-  k_rebuild_decide<<<1, 1, 0, st>>>(s);
   k_rebuild_clear<<<148 * 4, 256, 0, st>>>(s);
   k_rebuild_insert<<<148 * 4, 256, 0, st>>>(s);
 }

@@ -466,22 +466,26 @@ k_ev_apply_local(Dev s, EvBuf b) {
     for (int i = w; i < nv; i += nw) {
       int32_t e;
       int64_t key;
-      if (bykey) { key = b.vsel[i]; e = warp_find(s, key, lane); }
-      else { e = b.victims[i]; key = s.ekey[e]; }
-      uint32_t ecs = s.cs[e], ecc = s.cc[e];
-      bool dirty = ecc > ecs;
-      if (dirty) {  // Evict push to the (local) server: W += p, c_g = max(c_g, c_c)
-        float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
-        const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
-        for (int d = lane; d < D4; d += 32) Wr[d] = f4add_(Wr[d], pr[d]);
-        if (lane == 0) { uint32_t g = s.cg[key]; s.cg[key] = g > ecc ? g : ecc; }
+      uint64_t slot = 0;
+      if (bykey) { key = b.vsel[i]; e = warp_find_slot(s, key, lane, &slot); }
+      else { e = b.victims[i]; key = s.ekey[e]; e = warp_find_slot(s, key, lane, &slot); }
+      const uint32_t ecs = s.cs[e], ecc = s.cc[e], prim = s.eprim[e];
+      // row loads issued before the dirty test (victims are almost always dirty)
+      float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
+      const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
+      const bool dirty = ecc > ecs;
+      for (int d = lane; d < D4; d += 32) {
+        float4 wv = Wr[d], pv = pr[d];
+        if (dirty) Wr[d] = f4add_(wv, pv);     // Evict push: W += p
       }
-      warp_erase(s, key, lane);
       if (lane == 0) {
+        if (dirty) { uint32_t g = s.cg[key]; s.cg[key] = g > ecc ? g : ecc; }
+        s.hkey[slot] = HK_TOMB;
+        atomicAdd(&ctl->n_tomb, 1);
         b.vkeys[i] = key;
         b.vdirty[i] = dirty ? 1 : 0;
         if (dirty) atomicAdd(&s_dirty, 1u);
-        if (s.policy == 0) lfu_move(s, key, s.eprim[e], EP_FREE, dpop);
+        if (s.policy == 0) lfu_move(s, key, prim, EP_FREE, dpop);
         s.eprim[e] = EP_FREE;
         s.ekey[e] = -1;
         s.fstack[atomicAdd(&ctl->ftop, 1)] = e;

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libhet.so")
 
 HET_LFU, HET_LRU = 0, 1
 HET_S_INF = 0xFFFFFFFF
+HET_CLOCK_AUTO = 0xFFFFFFFFFFFFFFFF
 STATUS = {0: "HET_OK", 1: "HET_ERR_ARG", 2: "HET_ERR_KEY_RANGE", 3: "HET_ERR_PROTOCOL",
           4: "HET_ERR_CAPACITY", 5: "HET_ERR_OOM", 6: "HET_ERR_CUDA", 7: "HET_ERR_NCCL"}
 HIT, EXP1, EXP2, MISS = 0, 1, 2, 3
@@ -238,6 +239,18 @@ class HetCache:
 
     def update(self, keys, grads, lr):
         het_update(self.h, keys, keys.numel(), grads, lr)
+
+    def capture_step(self, keys, grads, out, lr):
+        """Capture one lookup (HET_CLOCK_AUTO) + update on static device
+        buffers into a CUDA graph; replay() runs the whole step.  Run at least
+        one uncaptured step first (lazy one-time attribute setup)."""
+        torch = self.torch
+        n = keys.numel()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="relaxed"):
+            het_lookup(self.h, keys, n, HET_CLOCK_AUTO, out)
+            het_update(self.h, keys, n, grads, lr)
+        return g
 
     def evict(self, keys=None):
         if keys is None:

@@ -218,3 +218,44 @@ def test_host_pointer_path():
         het.het_update(g.h, keys, keys.size, grads, LR)
         o.update([grads], LR)
     g.sync()
+
+
+@pytest.mark.parametrize("policy", [LFU, LRU])
+def test_cuda_graph_replay_parity(policy):
+    """A step captured into a CUDA graph (HET_CLOCK_AUTO: t = 0, 1, 2, ...)
+    replays with the same results as the oracle."""
+    het = _het()
+    R, D = 1000, 8
+    o = Oracle(R=R, D=D, C=capacity(0.1, R), s=10, policy=policy)
+    g = het.HetCache(R, D, 0.1, 10, policy, max_keys_per_call=4096)
+    n = 128 * 26
+    kbuf = torch.empty(n, dtype=torch.int64, device="cuda")
+    gbuf = torch.empty((n, D), dtype=torch.float32, device="cuda")
+    out = torch.empty((n, D), dtype=torch.float32, device="cuda")
+    t = 0
+    for _ in range(5):                                   # eager steps
+        keys = toy_keys(t)
+        grads = gen.grads(0, t, n, D).numpy()
+        kbuf.copy_(torch.from_numpy(keys)); gbuf.copy_(torch.from_numpy(grads))
+        g.lookup(kbuf, het.HET_CLOCK_AUTO, out=out)
+        g.update(kbuf, gbuf, LR)
+        assert_rows(out.cpu().numpy(), o.lookup(t, [keys])[0])
+        o.update([grads], LR)
+        t += 1
+    graph = g.capture_step(kbuf, gbuf, out, LR)
+    for _ in range(40):                                  # replays
+        keys = toy_keys(t)
+        grads = gen.grads(0, t, n, D).numpy()
+        kbuf.copy_(torch.from_numpy(keys)); gbuf.copy_(torch.from_numpy(grads))
+        graph.replay()
+        torch.cuda.synchronize()
+        assert_rows(out.cpu().numpy(), o.lookup(t, [keys])[0])
+        o.update([grads], LR)
+        gk, _ = g.victims()
+        assert np.array_equal(gk, np.sort(o.victims(0)[0]))
+        t += 1
+    p = Pair.__new__(Pair)
+    p.g, p.o, p.R, p.D, p.g_policy = g, o, R, D, policy
+    p.compare_stats()
+    p.compare_cache()
+    p.finish()
