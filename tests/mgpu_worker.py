@@ -1,0 +1,77 @@
+"""One rank of the multi-GPU parity run (launched by tests/test_gpu_multi.py).
+
+Every rank runs the same N-worker lock-step oracle and checks its own worker
+against it: gathered rows (1e-6 rel), unique keys and statuses (bit-exact),
+victims (bit-exact), counters, and at the end the rows/clocks of the global
+table shard it owns.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle.oracle import Oracle, capacity  # noqa: E402
+from workload import gen  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    policy, s, frac, T = int(sys.argv[1]), int(sys.argv[2]), float(sys.argv[3]), int(sys.argv[4])
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo")
+    from paper_2112_07221_b200 import het
+    obj = [het.het_get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    R, D, lr = 1000, 8, 0.01
+    cards = gen.cards_for("toy")
+    g = het.HetCache(R, D, frac, s, policy, rank=rank, world=world, unique_id=obj[0], max_keys_per_call=4096)
+    o = Oracle(R=R, D=D, C=capacity(frac, R), s=s, policy=policy, N=world)
+    for t in range(T):
+        keys = [gen.criteo_keys(i, t, 1, 128, cards)[0].numpy() for i in range(world)]
+        if t % 7 == 3:                        # ragged: some workers send fewer keys
+            keys = [k[: 100 * (i + 1)] for i, k in enumerate(keys)]
+        grads = [gen.grads(i, t, k.size, D).numpy() for i, k in enumerate(keys)]
+        kd = torch.from_numpy(keys[rank]).cuda()
+        out = g.lookup(kd, t).cpu().numpy()
+        oo = o.lookup(t, keys)
+        np.testing.assert_allclose(out, oo[rank], rtol=1e-6, atol=1e-30)
+        gl, ol = g.lookup_log(), o.lookup_log(rank)
+        assert np.array_equal(gl["unique"], ol["unique"]), t
+        assert np.array_equal(gl["status"], ol["status"]), (t, np.nonzero(gl["status"] != ol["status"]))
+        g.update(kd, torch.from_numpy(grads[rank]).cuda(), lr)
+        o.update(grads, lr)
+        gk, gdirty = g.victims()
+        ok, od = o.victims(rank)
+        order = np.argsort(ok, kind="stable")
+        assert np.array_equal(gk, ok[order]), t
+        assert np.array_equal(gdirty, od[order]), t
+    gs, os_ = g.stats(), o.stats(rank)
+    for k in ["lookups", "keys", "unique", "hits", "exp1", "exp2", "misses", "evictions", "dirty_pushes"]:
+        assert gs[k] == os_[k], (k, gs[k], os_[k])
+    assert gs["bytes_emb_tx"] > 0
+    g.sync()
+    o.flush()
+    owned = np.arange(rank, R, world, dtype=np.int64)
+    gr, gcg = g.read_global(owned)
+    orows, ocg = o.read_global(owned)
+    assert np.array_equal(gcg, ocg)
+    np.testing.assert_allclose(gr, orows, rtol=1e-6, atol=1e-30)
+    # dense all-reduce (Eq. 2): mean over workers
+    x = torch.full((1000,), float(rank + 1), device="cuda")
+    het.het_dense_allreduce(g.h, x, x.numel())
+    torch.cuda.synchronize()
+    assert torch.allclose(x, torch.full_like(x, (world + 1) / 2.0))
+    g.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"MGPU_OK world={world} policy={policy} s={s} frac={frac} exp2={os_['exp2']} "
+              f"evictions={os_['evictions']}", flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,28 @@
+"""Multi-GPU parity: N worker processes (one per GPU) over NCCL against the
+N-worker CPU oracle.  Skipped when fewer than 2 GPUs are visible."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def ngpu():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.skipif(ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("policy,s,frac", [(0, 10, 0.1), (1, 3, 0.05), (0, 0, 0.1), (0, 0xFFFFFFFF, 0.2)])
+def test_multi_gpu_parity(policy, s, frac):
+    n = min(ngpu(), 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + policy * 7 + (s % 97)}",
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), str(policy), str(s), str(frac), "60"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert "MGPU_OK" in r.stdout
