@@ -206,10 +206,12 @@ def run_gpu(args):
     t_load = time.time()
     for j in range(W):
         step(j)
-    while time.time() - t_load < 1.0:       # >= 1 s of load before the timed region (clock samples)
+    while True:                             # >= 1 s of load before the timed region (clock samples)
+        torch.cuda.synchronize()
+        if max_over_ranks(time.time() - t_load, world, device) >= 1.0:   # same decision on every rank
+            break
         for j in range(W):
             step(j)
-        torch.cuda.synchronize()
     graph = None
     graph_launches = None
     if use_graph:
