@@ -128,9 +128,14 @@ def algorithmic_bytes(kernel, s, D, n_steps, resident):
         return U * row + n * row + 4 * n + 4 * U
     if kernel == "segreduce_apply":
         return n * row + 4 * n + U * 4 * row + 8 * U
+    if kernel == "evict_select":
+        # LFU bitmap path: the threshold count's block counters + bitmap words, victim keys out
+        return 4 * ((R_WDL + 4095) // 4096) + 16 * e
+    if kernel == "evict_apply":
+        # per victim: key, hash slot, entry metadata; dirty: p read, W read+write, c_g
+        return e * (8 + 12 + 16) + ed * (3 * row + 8)
     if kernel == "evict":
-        # victims: key + slot + entry metadata, p read, W read+write (dirty), c_g; bitmap block counters
-        return e * (8 + 12 + 16) + ed * (3 * row + 8) + 4 * ((R_WDL + 4095) // 4096)
+        return 4 * ((R_WDL + 4095) // 4096) + 16 * e + e * (8 + 12 + 16) + ed * (3 * row + 8)
     return None
 
 
@@ -226,6 +231,7 @@ def run_gpu(args):
     s0 = cache.stats()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     barrier(world, device)
+    torch.cuda.cudart().cudaProfilerStart()      # `ncu --profile-from-start off` sees the timed steps only
     for j in range(K):
         flush.fill_(j & 0xFF)
         if use_graph:
@@ -238,6 +244,7 @@ def run_gpu(args):
             step(W + j)
             ev[j][1].record(st)
     barrier(world, device)
+    torch.cuda.cudart().cudaProfilerStop()
     clocks = clk.stop()
     s1 = cache.stats()
     ms = sum(a.elapsed_time(b) for a, b in ev) / K
@@ -333,7 +340,7 @@ def run_gpu(args):
         "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": n * 8 + n * D * 4, "d2h_bytes_per_step": n * D * 4},
     }
-    if args.sweep and world == 1:
+    if not args.no_sweep and world == 1:
         line["hbm_sweep"] = run_sweep(het, device)
     cache.close()
     if rank == 0:
@@ -367,7 +374,7 @@ def run_sweep(het, device):
         s1 = c.stats()
         sd = {k: s1[k] - s0[k] for k in ["keys", "unique", "misses", "exp1", "exp2", "evictions", "dirty_pushes"]}
         ent = {"batch": B, "n": n}
-        for kname in ["gather", "segreduce_apply", "dedup", "probe", "sync_fetch", "evict"]:
+        for kname in ["gather", "segreduce_apply", "dedup", "probe", "sync_fetch", "evict_apply"]:
             if kname in prof:
                 tot, cnt = prof[kname]
                 ab = algorithmic_bytes(kname, sd, D, 5, s1["resident"])
@@ -445,7 +452,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the D=128 n-sweep (HBM regime)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

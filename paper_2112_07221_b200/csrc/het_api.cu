@@ -433,8 +433,11 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
 static het_status_t evict_overflow(het_cache* h, cudaStream_t st) {
   Dev& d = h->d;
   if (d.world == 1) {
-    Prof p(h, "evict", st);
-    h->launches += launch_evict_select(d, h->evbuf_host, st);
+    {
+      Prof p(h, "evict_select", st);
+      h->launches += launch_evict_select(d, h->evbuf_host, st);
+    }
+    Prof p(h, "evict_apply", st);
     h->launches += launch_evict_apply_local(d, h->evbuf_host, st);
   } else {
     het_status_t rc = mgpu_evict_overflow(h->mg, d, h->evbuf_host, h->prof ? (void*)h : nullptr, st);

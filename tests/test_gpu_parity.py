@@ -259,3 +259,72 @@ def test_cuda_graph_replay_parity(policy):
     p.compare_stats()
     p.compare_cache()
     p.finish()
+
+
+def test_wdl_full_size_graph_replay():
+    """BASELINE configs[1] at full size (33,762,577 rows, D=128, cache 10 %,
+    s=100, LFU, batch 128) in bench.py's launch configuration (CUDA-graph
+    replay, HET_CLOCK_AUTO), from a cold cache through the first ~200
+    eviction steps: statuses, victims, counters bit-exact every step; rows of
+    a tracked 1/256 sample of keys (the oracle keeps rows only for them)."""
+    het = _het()
+    cards = gen.cards_for("criteo")
+    R, D, B, frac, s = sum(cards), 128, 128, 0.1, 100
+    n = B * 26
+    C = capacity(frac, R)
+    track = 256
+    o = Oracle(R=R, D=D, C=C, s=s, track_div=track)
+    g = het.HetCache(R, D, frac, s, LFU, max_keys_per_call=n)
+    kbuf = torch.empty(n, dtype=torch.int64, device="cuda")
+    gbuf = torch.empty((n, D), dtype=torch.float32, device="cuda")
+    out = torch.empty((n, D), dtype=torch.float32, device="cuda")
+    T = 6450
+    chunk = 250
+    graph = None
+    evict_steps = 0
+    for t0 in range(0, T, chunk):
+        keys_blk = gen.criteo_keys(0, t0, chunk, B, cards).numpy()
+        for j in range(chunk):
+            t = t0 + j
+            keys = keys_blk[j]
+            grads = gen.grads(0, t, n, D)
+            kbuf.copy_(torch.from_numpy(keys)); gbuf.copy_(grads)
+            if graph is None:
+                g.lookup(kbuf, het.HET_CLOCK_AUTO, out=out)
+                g.update(kbuf, gbuf, LR)
+                graph = g.capture_step(kbuf, gbuf, out, LR)
+                # the eager step above already consumed t; the oracle follows
+            else:
+                graph.replay()
+            oo = o.lookup(t, [keys])[0]
+            o.update([grads.numpy()], LR)
+            gl = g.lookup_log()
+            ol = o.lookup_log(0)
+            assert np.array_equal(gl["unique"], ol["unique"]), t
+            assert np.array_equal(gl["status"], ol["status"]), t
+            gk, gd = g.victims()
+            ok, od = o.victims(0)
+            order = np.argsort(ok, kind="stable")
+            assert np.array_equal(gk, ok[order]) and np.array_equal(gd, od[order]), t
+            evict_steps += ok.size > 0
+            if j % 25 == 0:
+                sel = _tracked_mask(keys, track)
+                if sel.any():
+                    np.testing.assert_allclose(out.cpu().numpy()[sel], oo[sel], rtol=RTOL, atol=1e-30)
+    assert evict_steps > 100
+    gs, os_ = g.stats(), o.stats(0)
+    for k in ["lookups", "keys", "unique", "hits", "exp1", "exp2", "misses", "evictions", "dirty_pushes"]:
+        assert gs[k] == os_[k], (k, gs[k], os_[k])
+
+
+def _tracked_mask(keys, track):
+    # the oracle's tracking rule: fmix(key ^ 0x7472616B) % track == 0
+    M = (1 << 64) - 1
+    out = np.zeros(len(keys), bool)
+    for i, k in enumerate(keys.tolist()):
+        x = (k ^ 0x7472616B) & M
+        x ^= x >> 30; x = (x * 0xBF58476D1CE4E5B9) & M
+        x ^= x >> 27; x = (x * 0x94D049BB133111EB) & M
+        x ^= x >> 31
+        out[i] = x % track == 0
+    return out
