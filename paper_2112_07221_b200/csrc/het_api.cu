@@ -50,6 +50,7 @@ struct het_cache {
   float* stage_out = nullptr;
   // protocol state
   bool have_lookup = false;
+  bool fused = false;          // the last lookup ran the fused single-GPU kernels
   uint32_t last_n = 0;
   int64_t overflow_bound = 0;  // worst-case residents above C since the last eviction
   uint64_t lookups = 0, keys = 0, updates = 0, launches = 0;
@@ -287,6 +288,7 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   A(d.cs, d.Ecap);
   A(d.cc, d.Ecap);
   A(d.eprim, d.Ecap);
+  A(d.estep, d.Ecap);
   A(d.fstack, d.Ecap);
   A(d.hkey, (size_t)S);
   A(d.hval, (size_t)S);
@@ -341,6 +343,7 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   cache_set_attrs();
   cudaMemsetAsync(d.ctl, 0, sizeof(Ctl), stream);
   cudaMemsetAsync(d.cnt, 0, C_NUM * 8, stream);
+  cudaMemsetAsync(d.estep, 0, d.Ecap * 4, stream);
   if (d.lfu_persist) cudaMemsetAsync(d.count_by_key, 0, rows * 4, stream);
   cudaMemsetAsync(d.cs, 0, d.Ecap * 4, stream);
   cudaMemsetAsync(d.cc, 0, d.Ecap * 4, stream);
@@ -396,31 +399,41 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
   c.t = clock_t;
   c.keys = keys;
   Dev& d = h->d;
-  launch_begin(d, clock_t, (int)n, st);
-  h->launches += 1;
-  {
-    Prof p(h, "dedup", st);
-    h->launches += launch_dedup(c, (int)n, d.R, h->pbits, d.ctl, st);
-  }
-  if (d.world == 1) {
+  h->fused = fused_ok(d, (int)n) && !getenv("HET_NO_FUSED");
+  if (h->fused) {
     {
-      Prof p(h, "probe", st);
-      launch_probe(d, c, (int)n, st);
+      Prof p(h, "dedup", st);
+      h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st);
     }
-    {
-      Prof p(h, "sync_fetch", st);
-      launch_sync_fetch_install_local(d, c, (int)n, st);
-    }
-    h->launches += 2;
+    Prof p(h, "lookup_fused", st);
+    h->launches += launch_lookup_fused(d, c, dout, st);
   } else {
-    rc = mgpu_lookup(h->mg, d, c, h->prof ? (void*)h : nullptr, st);
-    if (rc) return fail(h, rc, "multi-GPU lookup failed");
-    h->launches += mgpu_take_launches(h->mg);
-  }
-  {
-    Prof p(h, "gather", st);
-    launch_gather(d, c, dout, st);
+    launch_begin(d, clock_t, (int)n, st);
     h->launches += 1;
+    {
+      Prof p(h, "dedup", st);
+      h->launches += launch_dedup(c, (int)n, d.R, h->pbits, d.ctl, st);
+    }
+    if (d.world == 1) {
+      {
+        Prof p(h, "probe", st);
+        launch_probe(d, c, (int)n, st);
+      }
+      {
+        Prof p(h, "sync_fetch", st);
+        launch_sync_fetch_install_local(d, c, (int)n, st);
+      }
+      h->launches += 2;
+    } else {
+      rc = mgpu_lookup(h->mg, d, c, h->prof ? (void*)h : nullptr, st);
+      if (rc) return fail(h, rc, "multi-GPU lookup failed");
+      h->launches += mgpu_take_launches(h->mg);
+    }
+    {
+      Prof p(h, "gather", st);
+      launch_gather(d, c, dout, st);
+      h->launches += 1;
+    }
   }
   if (out_host) CUDA_TRY(h, cudaMemcpyAsync(out, dout, (size_t)n * h->D * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaGetLastError());
@@ -467,13 +480,19 @@ het_status_t het_update(het_cache_t h, const int64_t* keys, uint32_t n, const fl
     grads = h->stage_rows;
   }
   Dev& d = h->d;
-  {
-    Prof p(h, "segreduce_apply", st);
-    launch_segreduce_apply(d, h->call, grads, lr, (int)n, st);
-    h->launches += 1;
+  if (h->fused) {
+    Prof p(h, "update_fused", st);
+    h->launches += launch_update_fused(d, h->call, grads, lr, h->evbuf_host, st);
+    h->overflow_bound = 0;
+  } else {
+    {
+      Prof p(h, "segreduce_apply", st);
+      launch_segreduce_apply(d, h->call, grads, lr, (int)n, st);
+      h->launches += 1;
+    }
+    het_status_t rc = evict_overflow(h, st);
+    if (rc) return fail(h, rc, "evict failed");
   }
-  het_status_t rc = evict_overflow(h, st);
-  if (rc) return fail(h, rc, "evict failed");
   CUDA_TRY(h, cudaGetLastError());
   h->have_lookup = false;
   return HET_OK;

@@ -56,6 +56,15 @@ struct Ctl {
   int32_t generic;      // run the generic (scan) selection this step
   int32_t vmode;        // victims list holds 0 = entry indices, 1 = keys
   int32_t pad3_;
+  int32_t dd_done;      // blocks finished in the fused dedup (last-block pattern)
+  int32_t lk_done;      // blocks finished in the fused lookup
+  int32_t emode;        // eviction this step: 0 none, 1 LFU bitmap threshold, 2 generic
+  int32_t rebuild_req;  // hash rebuild requested for the next update
+  uint32_t lk_seq;      // lookup sequence number
+  int32_t nsel;         // victim keys extracted by the fused update
+  int32_t pad5_;
+  uint32_t lowmask;     // bit c set: some resident has LFU count c < T (snapshot for enumeration)
+  int64_t Kstar;        // LFU bitmap path: largest victim key among count == T
   uint64_t t_cur;       // clock of the current call (LRU tick)
   uint64_t t_auto;      // next automatic clock (HET_CLOCK_AUTO)
   // multi-GPU exchange bookkeeping
@@ -74,6 +83,7 @@ struct Dev {
   // cache entries
   int64_t Ecap; int64_t* ekey; float* v; float* p; uint32_t* cs; uint32_t* cc;
   uint32_t* eprim; int32_t* fstack;
+  uint32_t* estep;   // lookup sequence number that last touched the entry
   // hash
   int64_t* hkey; int32_t* hval; int hbits; uint64_t hmask;
   uint32_t* count_by_key;
@@ -291,5 +301,10 @@ void launch_segreduce_apply(const Dev& s, const Call& c, const float* grads, flo
 int launch_evict_select(const Dev& s, void* evbuf, cudaStream_t st);
 int launch_evict_apply_local(const Dev& s, void* evbuf, cudaStream_t st);
 void launch_hash_rebuild(const Dev& s, cudaStream_t st);
+// fused single-GPU step (k_fused.cu)
+bool fused_ok(const Dev& s, int n);
+int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st);
+int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st);
+int launch_update_fused(const Dev& s, const Call& c, const float* grads, float lr, void* evbuf, cudaStream_t st);
 
 }  // namespace het

@@ -1,0 +1,671 @@
+// Fused single-GPU step (N = 1, n <= 8192): three kernels per iteration.
+//
+//  k_dd_fused      rank-count stable sort of the (key, position) composites
+//                  (K1); the last block to finish (atomic counter, no waiting)
+//                  flags segment heads, block-scans them, writes
+//                  unique/inverse/perm/seg_off and does the per-call begin
+//                  (abort reset, clock, counters).
+//  k_lookup_fused  warp per unique key: Cache.Find, CheckValid cond (1)+(2),
+//                  LFU/LRU touch, fused Evict(k)+Fetch(k) / miss install, and
+//                  Cache.Get scattered to every occurrence of the key (K2,
+//                  K4/K5, K6).  The last
+//                  block derives this step's eviction threshold: with LFU
+//                  count bitmaps the victims are exactly {count < T} plus the
+//                  keys <= K* among count T (R9).
+//  k_update_fused  cooperative: warp per unique key does the ordered segment
+//                  reduce + SGD + pending + clock (K7/K8)
+//                  while other warps extract the victim keys from the count
+//                  bitmaps (4096-key blocks); after one grid sync every victim
+//                  is evicted by its own warp (Evict push W += p, c_g = max,
+//                  delete, free; K9).  LRU / LFU fallback: generic
+//                  selection then apply.  Hash rebuild, when requested.
+#include <cooperative_groups.h>
+
+#include "evict_dev.cuh"
+
+namespace het {
+
+constexpr int DDF_THREADS = 512;
+constexpr int DDF_WARPS = DDF_THREADS / 32;
+constexpr int DDF_ITEMS = 16;   // FUSED_MAX / DDF_THREADS
+constexpr int LK_WARPS = 8;
+constexpr int UPD_THREADS = 256;
+constexpr int UPD_WARPS = UPD_THREADS / 32;
+
+__device__ __forceinline__ int block_scan_int(int x, int* warp_sums, int* tot) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int v = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) warp_sums[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    int w = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) warp_sums[lane] = w;
+  }
+  __syncthreads();
+  int base = wid ? warp_sums[wid - 1] : 0;
+  *tot = warp_sums[nw - 1];
+  __syncthreads();
+  return base + v - x;
+}
+
+// ------------------------------------------------------------------ K_dd
+__global__ void __launch_bounds__(DDF_THREADS)
+k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, uint64_t t, int lookup) {
+  extern __shared__ uint64_t comp[];
+  __shared__ int part[DDF_WARPS][32];
+  __shared__ int warp_sums[32];
+  __shared__ int s_last;
+  Ctl* ctl = s.ctl;
+  int bad = 0;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    int64_t k = keys[q];
+    if (k < 0 || k >= s.R) bad = 1;
+    comp[q] = ((uint64_t)k << pbits) | (uint64_t)q;
+  }
+  bad = __syncthreads_or(bad);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p = blockIdx.x * 32 + lane;
+  if (!bad) {
+    const uint64_t mine = p < n ? comp[p] : ~0ull;
+    const int per = (n + DDF_WARPS - 1) / DDF_WARPS;
+    const int q0 = wid * per, q1 = min(n, q0 + per);
+    int cnt = 0;
+#pragma unroll 8
+    for (int q = q0; q < q1; ++q) cnt += comp[q] < mine;
+    part[wid][lane] = cnt;
+    __syncthreads();
+    if (wid == 0 && p < n) {
+      int r = 0;
+#pragma unroll
+      for (int w = 0; w < DDF_WARPS; ++w) r += part[w][lane];
+      c.sortbuf0[r] = mine;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&ctl->dd_done, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // ---- last block: per-call begin + head flags / scan / outputs
+  if (threadIdx.x == 0) {
+    ctl->dd_done = 0;
+    if (lookup) {
+      if (t == CLOCK_AUTO) { t = ctl->t_auto; ctl->t_auto = t + 1; }
+      ctl->t_cur = t;
+      ctl->lk_seq = ctl->lk_seq + 1;
+      s.cnt[C_LOOKUPS] += 1;
+      s.cnt[C_KEYS] += (unsigned long long)n;
+    }
+    ctl->abort = 0;
+    if (bad) { raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/); ctl->U = 0; c.seg_off[0] = 0; }
+  }
+  if (bad) return;
+  // each thread owns DDF_ITEMS consecutive sorted composites, loaded at once
+  const uint64_t* sorted = c.sortbuf0;
+  const int j0 = threadIdx.x * DDF_ITEMS;
+  uint64_t x[DDF_ITEMS + 1];
+#pragma unroll
+  for (int i = 0; i <= DDF_ITEMS; ++i) {
+    const int j = j0 + i - 1;                  // x[0] = previous element
+    x[i] = (j >= 0 && j < n) ? __ldcg(&sorted[j]) : ~0ull;
+  }
+  int heads = 0;
+#pragma unroll
+  for (int i = 1; i <= DDF_ITEMS; ++i) {
+    const int j = j0 + i - 1;
+    if (j < n && (j == 0 || (x[i] >> pbits) != (x[i - 1] >> pbits))) ++heads;
+  }
+  int tot;
+  int u = block_scan_int(heads, warp_sums, &tot) - 1;
+#pragma unroll
+  for (int i = 1; i <= DDF_ITEMS; ++i) {
+    const int j = j0 + i - 1;
+    if (j < n) {
+      const int pos = (int)(x[i] & ((1ull << pbits) - 1));
+      if (j == 0 || (x[i] >> pbits) != (x[i - 1] >> pbits)) {
+        ++u;
+        c.uniq[u] = (int64_t)(x[i] >> pbits);
+        c.seg_off[u] = j;
+      }
+      c.perm[j] = pos;
+      c.inverse[pos] = u;
+    }
+  }
+  if (threadIdx.x == 0) { c.seg_off[tot] = n; ctl->U = tot; }
+}
+
+// ------------------------------------------------------------------ K_look
+// LFU threshold (T, K*) for this step, one CTA (the last block of k_lookup_fused):
+// T = the smallest count whose cumulative population reaches `need`, K* = the
+// needT-th smallest key of count T.  Loads are issued in parallel: the 16
+// populations by 16 lanes, the block counters of bitmap T in chunks of
+// blockDim (coalesced, block-wide prefix), stopping at the chunk holding K*.
+__device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_sums, int64_t need) {
+  Ctl* ctl = s.ctl;
+  __shared__ int s_T;
+  __shared__ long long s_needT;
+  __shared__ long long s_blk, s_before;
+  __shared__ int s_done;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    long long pc = lane < s.lfu_cb ? (long long)__ldcg(&s.pop[lane]) : 0;
+    long long incl = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const long long excl = incl - pc;
+    const unsigned hit = __ballot_sync(0xffffffffu, lane < s.lfu_cb && excl < need && incl >= need);
+    const unsigned nonempty = __ballot_sync(0xffffffffu, pc > 0);
+    if (lane == 0) {
+      ctl->emode = 2;                       // until K* is found below
+      s_T = hit ? __ffs(hit) - 1 : -1;
+    }
+    if (hit && lane == __ffs(hit) - 1) {
+      s_needT = need - excl;
+      ctl->lowmask = nonempty & ((1u << lane) - 1u);
+    }
+  }
+  __syncthreads();
+  if (s_T < 0) return;
+  const int T = s_T;
+  const int64_t needT = s_needT;
+  const uint32_t* bc = s.bcnt + (int64_t)T * s.nbk;
+  const uint32_t* bm = s.bm + (int64_t)T * s.bm_words;
+  if (threadIdx.x == 0) { s_done = 0; s_blk = -1; }
+  __syncthreads();
+  long long carry = 0;
+  for (int64_t base = 0; base < s.nbk && !s_done; base += blockDim.x) {
+    const int64_t k = base + threadIdx.x;
+    const long long x = k < s.nbk ? (long long)__ldcg(&bc[k]) : 0;
+    long long tot;
+    const long long ex = carry + block_excl_scan64(x, warp_sums, &tot);
+    if (x > 0 && ex < needT && ex + x >= needT) { s_blk = k; s_before = ex; s_done = 1; }
+    carry += tot;
+    __syncthreads();
+  }
+  if (s_blk < 0) return;
+  if (threadIdx.x < 32) {
+    const int64_t blk = s_blk;
+    const int64_t want = needT - s_before;      // 1-based rank inside the block
+    uint32_t w[4];
+    int cl = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + q;
+      w[q] = wi < s.bm_words ? __ldcg(&bm[wi]) : 0u;
+      cl += __popc(w[q]);
+    }
+    int incl = cl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int excl = incl - cl;
+    if (excl < want && incl >= want) {
+      int r = (int)(want - excl);               // r-th set bit among this lane's 4 words
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int pc = __popc(w[q]);
+        if (r <= pc) {
+          uint32_t bits = w[q];
+          for (int kk = 1; kk < r; ++kk) bits &= bits - 1;
+          int64_t key = (((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + q) << 5) + (__ffs(bits) - 1);
+          ctl->Kstar = key;
+          ctl->T = (uint32_t)T;
+          ctl->needT = needT;
+          ctl->emode = 1;
+          break;
+        }
+        r -= pc;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(LK_WARPS * 32)
+k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
+  __shared__ unsigned bc[4];
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ int s_last;
+  __shared__ int warp_sums_i[32];
+  __shared__ long long warp_sums[32];
+  if (threadIdx.x < 4) bc[threadIdx.x] = 0;
+  dpop_init(dpop);
+  __syncthreads();
+  Ctl* ctl = s.ctl;
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x * LK_WARPS + (threadIdx.x >> 5);
+  const int U = ctl->U;
+  const int D4 = s.D >> 2;
+  if (!ctl->abort && u < U) {
+    const int64_t key = c.uniq[u];
+    const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
+    const int cnt = j1 - j0;
+    const int pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
+    uint32_t cntk = 0, gpre = 0;
+    if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
+    if (lane == 1 && s.s != S_INF) gpre = s.cg[key];
+    int32_t e = warp_find(s, key, lane);
+    gpre = __shfl_sync(0xffffffffu, gpre, 1);
+    uint8_t st = ST_MISS;
+    uint32_t ecs = 0, ecc = 0;
+    if (e >= 0) { ecs = s.cs[e]; ecc = s.cc[e]; }
+    if (lane == 0) {
+      if (s.lfu_persist) { cntk += 1; s.count_by_key[key] = cntk; }
+      if (e >= 0) {
+        if (s.s == S_INF) st = ST_HIT;                       // R4
+        else if (ecc - ecs > s.s) st = ST_EXP1;              // cond (1)
+        else st = (gpre <= ecc || gpre - ecc <= s.s) ? ST_HIT : ST_EXP2;   // cond (2)
+        if (s.policy == 0) {                                 // L6
+          uint32_t oldc = s.eprim[e];
+          uint32_t newc = s.lfu_persist ? cntk : oldc + 1;
+          s.eprim[e] = newc;
+          lfu_move(s, key, oldc, newc, dpop);
+        } else {
+          s.eprim[e] = (uint32_t)ctl->t_cur;
+        }
+      }
+      c.status[u] = st;
+      atomicAdd(&bc[st == ST_HIT ? 0 : st == ST_EXP1 ? 1 : st == ST_EXP2 ? 2 : 3], 1u);
+    }
+    st = __shfl_sync(0xffffffffu, st, 0);
+    float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
+    if (st != ST_HIT) {
+      uint32_t g = gpre;
+      if (s.s == S_INF || st == ST_MISS) g = s.cg[key];
+      if (st != ST_MISS) {
+        if (ecc > ecs) {  // dirty sync push (L4): W += p, c_g = max
+          const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
+          for (int d = lane; d < D4; d += 32) Wr[d] = f4add_(Wr[d], pr[d]);
+          g = g > ecc ? g : ecc;
+          if (lane == 0) s.cg[key] = g;
+        }
+      } else {          // miss: free entry + hash insert
+        int32_t idx = 0;
+        if (lane == 0) idx = atomicSub(&ctl->ftop, 1) - 1;
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx < 0) {
+          if (lane == 0) raise_err(ctl, 4 /*HET_ERR_CAPACITY*/);
+          e = -1;
+        } else {
+          e = s.fstack[idx];
+          warp_insert(s, key, e, lane);
+          if (lane == 0) {
+            s.ekey[e] = key;
+            uint32_t prim = s.policy == 0 ? (s.lfu_persist ? cntk : 1u) : (uint32_t)ctl->t_cur;
+            s.eprim[e] = prim;
+            if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
+            atomicMin(&ctl->min_install, prim);
+          }
+        }
+      }
+      if (e >= 0) {     // L5: v = W, c_s = c_c = c_g
+        float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
+        for (int d = lane; d < D4; d += 32) vr[d] = Wr[d];
+        if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
+      }
+    }
+    if (e >= 0) {
+      if (lane == 0) c.uentry[u] = e;
+      // L7 Get, scattered to the occurrences of the key (128-bit stores)
+      const float4* vr = reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D);
+      float4* o4 = reinterpret_cast<float4*>(out);
+      for (int d = lane; d - lane < D4; d += 32) {
+        float4 val = d < D4 ? vr[d] : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int kb = 0; kb < cnt; kb += 32) {
+          const int src = kb == 0 ? pos_lane : (kb + lane < cnt ? c.perm[j0 + kb + lane] : 0);
+          const int m = min(32, cnt - kb);
+          for (int k = 0; k < m; ++k) {
+            int pos = __shfl_sync(0xffffffffu, src, k);
+            if (d < D4) __stcs(o4 + (int64_t)pos * D4 + d, val);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  dpop_flush(s, dpop);
+  if (threadIdx.x == 0) {
+    if (bc[0]) atomicAdd(&s.cnt[C_HITS], (unsigned long long)bc[0]);
+    if (bc[1]) atomicAdd(&s.cnt[C_EXP1], (unsigned long long)bc[1]);
+    if (bc[2]) atomicAdd(&s.cnt[C_EXP2], (unsigned long long)bc[2]);
+    if (bc[3]) atomicAdd(&s.cnt[C_MISSES], (unsigned long long)bc[3]);
+    if (blockIdx.x == 0 && !ctl->abort) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+  }
+  // ---- last block: this step's eviction plan (needs every install and count)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&ctl->lk_done, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t res = s.Ecap - (int64_t)__ldcg(&ctl->ftop);
+  const int64_t need = res - s.C;
+  if (threadIdx.x == 0) {
+    ctl->lk_done = 0;
+    ctl->nvict = 0; ctl->ncand = 0; ctl->nsub = 0; ctl->vmode = 0; ctl->nsel = 0;
+    const bool none = __ldcg(&ctl->abort) || need <= 0;
+    ctl->need = none ? 0 : need;
+    ctl->emode = none ? 0 : ((s.policy == 0 && s.lfu_cb && need < res) ? 1 : 2);
+    ctl->generic = ctl->emode == 2;
+    const int64_t S = (int64_t)s.hmask + 1;
+    ctl->rebuild_req = (int64_t)__ldcg(&ctl->n_tomb) > S / 8;
+  }
+  __syncthreads();
+  if (ctl->emode == 1) lfu_threshold(s, warp_sums_i, warp_sums, need);
+  __syncthreads();
+  if (threadIdx.x == 0) ctl->generic = ctl->emode == 2;
+}
+
+// ------------------------------------------------------------------ K_upd
+// Evict push of one resident entry at N = 1 (warp-cooperative) + delete + free
+__device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_t e, int64_t key, uint64_t slot,
+                                            int lane, int* dpop, unsigned* s_dirty, unsigned* s_ev) {
+  Ctl* ctl = s.ctl;
+  const uint32_t ecs = s.cs[e], ecc = s.cc[e], prim = s.eprim[e];
+  const bool dirty = ecc > ecs;
+  const int D4 = s.D >> 2;
+  if (dirty) {
+    float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
+    const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
+    for (int d = lane; d < D4; d += 32) Wr[d] = f4add_(Wr[d], pr[d]);
+  }
+  if (lane == 0) {
+    if (dirty) { uint32_t g = s.cg[key]; s.cg[key] = g > ecc ? g : ecc; }
+    s.hkey[slot] = HK_TOMB;
+    atomicAdd(&ctl->n_tomb, 1);
+    int vi = atomicAdd(&ctl->nvict, 1);
+    b.vkeys[vi] = key;
+    b.vdirty[vi] = dirty ? 1 : 0;
+    if (s.policy == 0) lfu_move(s, key, prim, EP_FREE, dpop);
+    s.eprim[e] = EP_FREE;
+    s.ekey[e] = -1;
+    s.fstack[atomicAdd(&ctl->ftop, 1)] = e;
+    atomicAdd(s_ev, 1u);
+    if (dirty) atomicAdd(s_dirty, 1u);
+  }
+}
+
+__device__ __forceinline__ void segreduce_key(const Dev& s, const Call& c, const float4* __restrict__ G4, float lr,
+                                              int u, int lane, float4* mystg, uint64_t* bar, uint32_t& phase,
+                                              int stage_rows) {
+  const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
+  const int32_t e = c.uentry[u];
+  const uint32_t ecc = s.cc[e], ecs = s.cs[e];
+  const int cnt = j1 - j0;
+  const int pos_lane = lane < cnt ? __ldg(&c.perm[j0 + lane]) : 0;
+  const bool dirty = ecc > ecs;
+  const int D4 = s.D >> 2;
+  const float nlr = -lr;
+  float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
+  float4* pr = reinterpret_cast<float4*>(s.p + (int64_t)e * s.D);
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (stage_rows > 0 && cnt > 4) {
+    float4* accrow = mystg + (size_t)stage_rows * D4;
+    const uint32_t rowbytes = s.D * 4;
+    for (int kb = 0; kb < cnt; kb += stage_rows) {
+      const int m = min(stage_rows, cnt - kb);
+      const int src = kb == 0 ? pos_lane : (kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0);
+      __syncwarp();
+      fence_proxy_async();
+      if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)m * rowbytes);
+      __syncwarp();
+      if (lane < m) bulk_g2s(mystg + (size_t)lane * D4, G4 + (int64_t)src * D4, rowbytes, bar);
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      for (int d = lane; d < D4; d += 32) {
+        float4 a = kb ? accrow[d] : zero;
+        for (int k = 0; k < m; ++k) a = f4add_(a, mystg[(size_t)k * D4 + d]);
+        accrow[d] = a;
+      }
+    }
+    __syncwarp();
+    for (int d = lane; d < D4; d += 32) {
+      float4 acc = accrow[d];
+      float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
+                              __fmul_rn(nlr, acc.w));
+      vr[d] = f4add_(vr[d], dl);
+      pr[d] = f4add_(dirty ? pr[d] : zero, dl);
+    }
+  } else {
+    for (int d = lane; d - lane < D4; d += 32) {
+      const bool act = d < D4;
+      float4 vv = act ? vr[d] : zero;
+      float4 pp = (act && dirty) ? pr[d] : zero;
+      float4 acc = zero;
+      for (int kb = 0; kb < cnt; kb += 32) {
+        const int src = kb == 0 ? pos_lane : (kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0);
+        const int m = min(32, cnt - kb);
+        int k = 0;
+        for (; k + 4 <= m; k += 4) {
+          int p0 = __shfl_sync(0xffffffffu, src, k), p1 = __shfl_sync(0xffffffffu, src, k + 1);
+          int p2 = __shfl_sync(0xffffffffu, src, k + 2), p3 = __shfl_sync(0xffffffffu, src, k + 3);
+          if (act) {
+            float4 g0 = __ldcs(G4 + (int64_t)p0 * D4 + d), g1 = __ldcs(G4 + (int64_t)p1 * D4 + d);
+            float4 g2 = __ldcs(G4 + (int64_t)p2 * D4 + d), g3 = __ldcs(G4 + (int64_t)p3 * D4 + d);
+            acc = f4add_(acc, g0); acc = f4add_(acc, g1); acc = f4add_(acc, g2); acc = f4add_(acc, g3);
+          }
+        }
+        for (; k < m; ++k) {
+          int p0 = __shfl_sync(0xffffffffu, src, k);
+          if (act) acc = f4add_(acc, __ldcs(G4 + (int64_t)p0 * D4 + d));
+        }
+      }
+      if (act) {
+        float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
+                                __fmul_rn(nlr, acc.w));
+        vr[d] = f4add_(vv, dl);
+        pr[d] = f4add_(pp, dl);
+      }
+    }
+  }
+  if (lane == 0) s.cc[e] = ecc + 1;
+}
+
+__global__ void __launch_bounds__(UPD_THREADS)
+k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, int stage_rows) {
+  extern __shared__ float4 dyn[];
+  __shared__ uint32_t h[NBIN];
+  __shared__ uint64_t bars[UPD_WARPS];
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ unsigned s_dirty, s_ev;
+  cg::grid_group grid = cg::this_grid();
+  Ctl* ctl = s.ctl;
+  dpop_init(dpop);
+  if (threadIdx.x == 0) { s_dirty = 0; s_ev = 0; }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { mbar_init(&bars[wid], 1); fence_mbar_init(); }
+  __syncthreads();
+  const bool abort = ctl->abort;
+  const int U = abort ? 0 : ctl->U;
+  const int emode = abort ? 0 : ctl->emode;
+  const bool rebuild = ctl->rebuild_req;
+  const uint32_t T = ctl->T;
+  const int64_t Kstar = ctl->Kstar;
+  const uint32_t lowmask = ctl->lowmask;
+  const int gw = blockIdx.x * UPD_WARPS + wid;
+  const int nw = gridDim.x * UPD_WARPS;
+  const int D4 = s.D >> 2;
+  float4* mystg = dyn + (size_t)wid * (stage_rows + 1) * D4;
+  uint32_t phase = 0;
+  const float4* G4 = reinterpret_cast<const float4*>(G);
+  // ---- phase 1a: ordered segment reduce + SGD + pending + clock, warp per unique key
+  for (int u = gw; u < U; u += nw) segreduce_key(s, c, G4, lr, u, lane, mystg, &bars[wid], phase, stage_rows);
+  // ---- phase 1b (LFU bitmap path): extract the victim keys -- every key of the
+  // counts < T in lowmask and the keys <= K* of count T -- into b.vsel, one
+  // 4096-key bitmap block per warp task, one atomic per warp
+  if (emode == 1) {
+    const int64_t kblk = Kstar >> LFU_BLK_SHIFT;
+    int64_t ntask = 0;
+    for (uint32_t cc = 0; cc < T; ++cc) ntask += ((lowmask >> cc) & 1) ? s.nbk : 0;
+    ntask += kblk + 1;
+    for (int64_t task = gw; task < ntask; task += nw) {
+      int64_t tsk = task;
+      uint32_t cc = 0;
+      for (; cc < T; ++cc) {
+        if (!((lowmask >> cc) & 1)) continue;
+        if (tsk < s.nbk) break;
+        tsk -= s.nbk;
+      }
+      const int64_t blk = tsk;
+      if (__ldcg(&s.bcnt[(int64_t)cc * s.nbk + blk]) == 0) continue;
+      const uint32_t* bm = s.bm + (int64_t)cc * s.bm_words;
+      uint32_t w[4];
+      int cl = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + q;
+        uint32_t bits = wi < s.bm_words ? __ldcg(&bm[wi]) : 0u;
+        if (cc == T) {   // keep keys <= K*
+          const int64_t k0 = wi << 5;
+          if (k0 > Kstar) bits = 0;
+          else if (k0 + 31 > Kstar) bits &= (Kstar - k0 == 31) ? 0xffffffffu : ((1u << (Kstar - k0 + 1)) - 1u);
+        }
+        w[q] = bits;
+        cl += __popc(bits);
+      }
+      int incl = cl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (total == 0) continue;
+      int base = 0;
+      if (lane == 31) base = atomicAdd(&ctl->nsel, total);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      int pos = base + incl - cl;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t bits = w[q];
+        const int64_t kb = ((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + q) << 5;
+        while (bits) {
+          b.vsel[pos++] = kb + (__ffs(bits) - 1);
+          bits &= bits - 1;
+        }
+      }
+    }
+  }
+  // ---- phase 2 (LFU bitmap path): every update is done; evict, warp per victim
+  if (emode == 1) {
+    grid.sync();
+    const int nsel = ctl->nsel;
+    for (int i = gw; i < nsel; i += nw) {
+      const int64_t key = b.vsel[i];
+      uint64_t slot = 0;
+      const int32_t e = warp_find_slot(s, key, lane, &slot);
+      if (e >= 0) evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev);
+    }
+  }
+  // ---- generic selection (LRU, LFU fallback, evict-all) after all updates
+  if (emode == 2) {
+    grid.sync();
+    generic_select(s, b, reinterpret_cast<uint64_t*>(dyn), h, grid);
+    grid.sync();
+    const int nv = ctl->nvict;
+    // nvict is reused as the export cursor by evict_entry: reset once, grid-wide
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->nvict = 0;
+    grid.sync();
+    for (int i = gw; i < nv; i += nw) {
+      const int32_t e0 = b.victims[i];
+      const int64_t key = s.ekey[e0];
+      uint64_t slot = 0;
+      int32_t e = warp_find_slot(s, key, lane, &slot);
+      evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev);
+    }
+  }
+  __syncthreads();
+  dpop_flush(s, dpop);
+  if (threadIdx.x == 0) {
+    if (s_ev) atomicAdd(&s.cnt[C_EVICTIONS], (unsigned long long)s_ev);
+    if (s_dirty) atomicAdd(&s.cnt[C_DIRTY_PUSHES], (unsigned long long)s_dirty);
+  }
+  // ---- hash maintenance (rare): rebuild from the resident entries
+  if (rebuild) {
+    grid.sync();
+    const int64_t S = (int64_t)s.hmask + 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x)
+      s.hkey[i] = HK_EMPTY;
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->n_tomb = 0; ctl->rebuild_req = 0; }
+    for (int64_t e0 = (int64_t)gw * 32; e0 < s.Ecap; e0 += (int64_t)nw * 32) {
+      int64_t e = e0 + lane;
+      int64_t key = e < s.Ecap ? s.ekey[e] : -1;
+      unsigned m = __ballot_sync(0xffffffffu, key >= 0);
+      while (m) {
+        int src = __ffs(m) - 1;
+        int64_t k = __shfl_sync(0xffffffffu, key, src);
+        warp_insert(s, k, (int32_t)(e0 + src), lane);
+        m &= m - 1;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+constexpr int FUSED_MAX = 8192;
+
+bool fused_ok(const Dev& s, int n) { return s.world == 1 && n <= FUSED_MAX; }
+
+int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, FUSED_MAX * 8);
+    attr = true;
+  }
+  int blocks = std::max(1, (n + 31) / 32);
+  k_dd_fused<<<blocks, DDF_THREADS, (size_t)std::max(n, 1) * 8, st>>>(c.keys, n, pbits, s, c, t, lookup);
+  return 1;
+}
+
+int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st) {
+  int blocks = std::max(1, (c.n + LK_WARPS - 1) / LK_WARPS);
+  k_lookup_fused<<<blocks, LK_WARPS * 32, 0, st>>>(s, c, out);
+  return 1;
+}
+
+int launch_update_fused(const Dev& s, const Call& c, const float* grads, float lr, void* evbuf, cudaStream_t st) {
+  static int coop_blocks = 0;
+  static size_t smem = 0;
+  static int stage_rows = 0;
+  static uint32_t forD = 0;
+  if (!coop_blocks || forD != s.D) {
+    const int rowbytes = (int)s.D * 4;
+    stage_rows = std::min(32, 12288 / rowbytes);
+    if (stage_rows < 4) stage_rows = 0;
+    size_t stg = stage_rows ? (size_t)UPD_WARPS * (stage_rows + 1) * rowbytes : 0;
+    smem = std::max(stg, (size_t)SUBMAX * 8);
+    cudaFuncSetAttribute(k_update_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev, sms, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_update_fused, UPD_THREADS, smem);
+    coop_blocks = sms * std::max(per, 1);
+    forD = s.D;
+  }
+  EvBuf& b = *reinterpret_cast<EvBuf*>(evbuf);
+  Dev sd = s;
+  Call cd = c;
+  int sr = stage_rows;
+  void* args[] = {(void*)&sd, (void*)&cd, (void*)&grads, (void*)&lr, (void*)&b, (void*)&sr};
+  cudaLaunchCooperativeKernel((void*)k_update_fused, dim3(coop_blocks), dim3(UPD_THREADS), args, smem, st);
+  return 1;
+}
+
+}  // namespace het

@@ -101,7 +101,12 @@ def toy_keys(t, B=128, i=0):
     (LRU, 100, 1, 0.3),
     (LFU, 10, 1, 0.0),       # no cache: HET Hybrid mode (R10)
 ])
-def test_toy_full_parity(policy, s, persist, frac):
+@pytest.mark.parametrize("fused", [True, False])
+def test_toy_full_parity(policy, s, persist, frac, fused, monkeypatch):
+    """fused: the 3-kernel single-GPU step; unfused: the per-phase kernels
+    (the multi-GPU / large-batch path)."""
+    if not fused:
+        monkeypatch.setenv("HET_NO_FUSED", "1")
     R, D, T = 1000, 8, 200
     p = Pair(R, D, frac, s, policy, persist)
     p.g_policy = policy
@@ -115,10 +120,13 @@ def test_toy_full_parity(policy, s, persist, frac):
 
 
 @pytest.mark.parametrize("cb", ["0", "2"])
-def test_lfu_generic_fallback(cb, monkeypatch):
+@pytest.mark.parametrize("fused", [True, False])
+def test_lfu_generic_fallback(cb, fused, monkeypatch):
     """LFU with the count bitmaps disabled (0) or tiny (2): the exact generic
     selection runs instead of / after the bitmap path."""
     monkeypatch.setenv("HET_LFU_CB", cb)
+    if not fused:
+        monkeypatch.setenv("HET_NO_FUSED", "1")
     R, D = 1000, 8
     p = Pair(R, D, 0.1, 10, LFU, 1)
     p.g_policy = LFU
