@@ -188,25 +188,22 @@ def run_gpu(args):
     W, K = args.warmup, args.steps
     keys_all = gen.criteo_keys(rank, t, W + 2 * K, B, cards, CFG["alpha"], device=device)
     grads_all = [gen.grads(rank, t + j, n, D, device=device) for j in range(W + 2 * K)]
-    dense = torch.zeros(CFG["dense_params"], dtype=torch.float32, device=device)
-    dense_src = gen.dense_grads(rank, 0, CFG["dense_params"], device=device)
+    dense = gen.dense_grads(rank, 0, CFG["dense_params"], device=device)   # the step's dense gradients
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)   # > 126 MB L2
     st = torch.cuda.current_stream()
 
+    side = torch.cuda.Stream() if world > 1 else None
+
     def step(j):
-        k = keys_all[j]
-        cache.lookup(k, AUTO, out=out_buf)
-        cache.update(k, grads_all[j], lr)
-        if world > 1:
-            dense.copy_(dense_src)
-            het.het_dense_allreduce(cache.h, dense, dense.numel())
+        # dense all-reduce overlapped on a side stream (N > 1)
+        cache.step(keys_all[j], grads_all[j], out_buf, lr, dense if world > 1 else None, side)
 
     out_buf = torch.empty((n, D), dtype=torch.float32, device=device)
     # static input buffers of the captured step (the data loader / dense
     # backward write here; filled before each timed step, outside the events)
     kbuf = torch.empty_like(keys_all[0])
     gbuf = torch.empty_like(grads_all[0])
-    use_graph = world == 1
+    use_graph = world == 1 or os.environ.get("HET_P2P", "1") != "0"   # the P2P exchange has no host sync
     clk = Clocks(local)
     t_load = time.time()
     for j in range(W):
@@ -223,7 +220,7 @@ def run_gpu(args):
         kbuf.copy_(keys_all[0]); gbuf.copy_(grads_all[0])
         step(0)
         l0 = cache.stats()["launches"]
-        graph = cache.capture_step(kbuf, gbuf, out_buf, lr)
+        graph = cache.capture_step(kbuf, gbuf, out_buf, lr, dense if world > 1 else None)
         graph_launches = cache.stats()["launches"] - l0
         for j in range(3):
             kbuf.copy_(keys_all[j]); gbuf.copy_(grads_all[j]); graph.replay()
@@ -308,8 +305,10 @@ def run_gpu(args):
         het.het_lookup(cache.h, keys_h[W + j], n, AUTO, out_h)
         het.het_update(cache.h, keys_h[W + j], n, grads_h[W + j], lr)
         if world > 1:
-            dense.copy_(dense_src)
-            het.het_dense_allreduce(cache.h, dense, dense.numel())
+            side.wait_stream(st)
+            with torch.cuda.stream(side):
+                het.het_dense_allreduce(cache.h, dense, dense.numel(), stream=side)
+            st.wait_stream(side)
         te1.record(st)
         te1.synchronize()
         e2e_ms += te0.elapsed_time(te1)
@@ -340,8 +339,11 @@ def run_gpu(args):
         "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": n * 8 + n * D * 4, "d2h_bytes_per_step": n * D * 4},
     }
+    del graph
+    torch.cuda.synchronize()
     if not args.no_sweep and world == 1:
         line["hbm_sweep"] = run_sweep(het, device)
+    barrier(world, device)
     cache.close()
     if rank == 0:
         line["cpu_baseline"] = cpu_baseline(args)

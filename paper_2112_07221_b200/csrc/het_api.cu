@@ -545,7 +545,8 @@ het_status_t het_sync(het_cache_t h, het_stream_t stream_) {
     k_flush_local<<<148 * 4, 256, 0, st>>>(d);
     h->launches += 1;
   } else {
-    het_status_t rc = mgpu_flush(h->mg, d, st);
+    het_status_t rc = mgpu_drain(h->mg, d, h->call, st);
+    if (rc == HET_OK) rc = mgpu_flush(h->mg, d, st);
     if (rc) return fail(h, rc, "multi-GPU flush failed");
     h->launches += mgpu_take_launches(h->mg);
   }
@@ -585,6 +586,10 @@ het_status_t het_stats(het_cache_t h, het_stats_t* out) {
   out->evictions = cnt[C_EVICTIONS];
   out->dirty_pushes = cnt[C_DIRTY_PUSHES];
   if (h->mg) mgpu_bytes(h->mg, &out->bytes_clock_tx, &out->bytes_clock_rx, &out->bytes_emb_tx, &out->bytes_emb_rx);
+  out->bytes_clock_tx += cnt[C_BCLK_TX];   // device-counted (peer-memory exchange)
+  out->bytes_clock_rx += cnt[C_BCLK_RX];
+  out->bytes_emb_tx += cnt[C_BEMB_TX];
+  out->bytes_emb_rx += cnt[C_BEMB_RX];
   out->launches = h->launches;
   out->resident = (uint32_t)(h->d.Ecap - ctl.ftop);
   out->capacity = (uint32_t)h->C;

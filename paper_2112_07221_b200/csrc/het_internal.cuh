@@ -28,7 +28,8 @@ enum : uint8_t { ST_HIT = 0, ST_EXP1 = 1, ST_EXP2 = 2, ST_MISS = 3, ST_NEEDQ = 4
 
 // device counters (u64), order shared with het_stats_t
 enum {
-  C_UNIQUE = 0, C_HITS, C_EXP1, C_EXP2, C_MISSES, C_EVICTIONS, C_DIRTY_PUSHES, C_LOOKUPS, C_KEYS, C_NUM
+  C_UNIQUE = 0, C_HITS, C_EXP1, C_EXP2, C_MISSES, C_EVICTIONS, C_DIRTY_PUSHES, C_LOOKUPS, C_KEYS,
+  C_BCLK_TX, C_BCLK_RX, C_BEMB_TX, C_BEMB_RX, C_NUM
 };
 constexpr uint64_t CLOCK_AUTO = ~0ull;   // HET_CLOCK_AUTO: device-side iteration counter
 

@@ -25,10 +25,12 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "het_mgpu.h"
+#include "het_p2p.h"
 
 namespace het {
 
@@ -77,6 +79,7 @@ struct MgpuState {
   uint64_t launches = 0;
   uint64_t bytes_clock_tx = 0, bytes_clock_rx = 0, bytes_emb_tx = 0, bytes_emb_rx = 0;
   std::vector<void*> allocs;
+  P2PState* p2p = nullptr;     // device-initiated exchange (default); nullptr = NCCL v1
 };
 
 template <typename T>
@@ -490,7 +493,7 @@ het_status_t mgpu_create(MgpuState*& mg, const Dev& d, uint32_t n_max, const voi
   m->N = d.world;
   m->rank = d.rank;
   m->D = d.D;
-  m->CAPS = 2 * (int64_t)n_max;
+  m->CAPS = 3 * (int64_t)n_max;
   m->REC = 4 + d.D;
   ncclUniqueId id;
   std::memcpy(&id, uid, sizeof(id));
@@ -514,12 +517,20 @@ het_status_t mgpu_create(MgpuState*& mg, const Dev& d, uint32_t n_max, const voi
   m->opbits = std::max(1, bits_for((uint64_t)NC - 1));
   cudaMemsetAsync(m->octl, 0, sizeof(Ctl), st);
   cudaMemsetAsync(m->scnt, 0, sizeof(int32_t) * 2 * m->N, st);
+  const char* env = std::getenv("HET_P2P");
+  if (!(env && env[0] == '0')) {
+    het_status_t rc = p2p_create(m->p2p, d, n_max, m->comm, st);
+    if (rc != HET_OK) return rc;
+  }
   return HET_OK;
 }
 
 void mgpu_destroy(MgpuState* m) {
   if (!m) return;
-  if (m->comm) ncclCommDestroy(m->comm);
+  p2p_destroy(m->p2p);
+  // abort rather than destroy: teardown is not collective, and a CUDA graph
+  // that captured NCCL work of this communicator may still be alive
+  if (m->comm) ncclCommAbort(m->comm);
   for (void* q : m->allocs) cudaFree(q);
   if (m->h_scnt) cudaFreeHost(m->h_scnt);
   if (m->h_rcnt) cudaFreeHost(m->h_rcnt);
@@ -536,6 +547,12 @@ het_status_t mgpu_lookup(MgpuState* m, const Dev& d, const Call& c, void* prof, 
     m->launches += 1;
   }
   const int N = m->N;
+  if (m->p2p) {
+    void* pr = prof_begin(prof, "exchange", st);
+    m->launches += p2p_round(m->p2p, d, c, 0, st);
+    prof_end(prof, pr, st);
+    return HET_OK;
+  }
   if (d.s != S_INF) {
     void* pr = prof_begin(prof, "clock_check", st);
     cudaMemsetAsync(m->scnt, 0, sizeof(int32_t) * 2 * N, st);
@@ -608,6 +625,11 @@ struct EvBufView {  // leading fields of EvBuf (k_evict.cu)
 het_status_t mgpu_evict_overflow(MgpuState* m, const Dev& d, void* evbuf, void* prof, cudaStream_t st) {
   void* pr = prof_begin(prof, "evict", st);
   m->launches += launch_evict_select(d, evbuf, st);
+  if (m->p2p) {
+    m->launches += p2p_pushes(m->p2p, d, evbuf, st);
+    prof_end(prof, pr, st);
+    return HET_OK;
+  }
   const EvBufView& b = *reinterpret_cast<const EvBufView*>(evbuf);
   cudaMemsetAsync(m->scnt, 0, sizeof(int32_t) * 2 * m->N, st);
   Call dummy{};
@@ -619,6 +641,7 @@ het_status_t mgpu_evict_overflow(MgpuState* m, const Dev& d, void* evbuf, void* 
 }
 
 het_status_t mgpu_evict_keys(MgpuState* m, const Dev& d, const Call& c, cudaStream_t st) {
+  if (m->p2p) m->launches += p2p_round(m->p2p, d, c, 1, st);   // deliver pending pushes first
   cudaMemsetAsync(m->scnt, 0, sizeof(int32_t) * 2 * m->N, st);
   k_build_pushes<<<grid_for(std::max(c.n, 1), 8), MG_TPB, 0, st>>>(d, c, *m, nullptr, nullptr, nullptr, nullptr, 1,
                                                                      0, 0);
@@ -672,6 +695,11 @@ __global__ void k_flush_build(Dev s, MgpuState m_, int64_t k0, int64_t k1) {
       for (int d = lane; d < D4; d += 32) dst[d] = pr[d];
     }
   }
+}
+
+het_status_t mgpu_drain(MgpuState* m, const Dev& d, const Call& c, cudaStream_t st) {
+  if (m->p2p) m->launches += p2p_round(m->p2p, d, c, 1, st);
+  return HET_OK;
 }
 
 het_status_t mgpu_flush(MgpuState* m, const Dev& d, cudaStream_t st) {

@@ -16,6 +16,8 @@ het_status_t mgpu_lookup(MgpuState* mg, const Dev& d, const Call& c, void* prof,
 het_status_t mgpu_evict_overflow(MgpuState* mg, const Dev& d, void* evbuf, void* prof, cudaStream_t st);
 het_status_t mgpu_evict_keys(MgpuState* mg, const Dev& d, const Call& c, cudaStream_t st);
 het_status_t mgpu_flush(MgpuState* mg, const Dev& d, cudaStream_t st);
+// deliver the eviction pushes still waiting for the next exchange round
+het_status_t mgpu_drain(MgpuState* mg, const Dev& d, const Call& c, cudaStream_t st);
 het_status_t mgpu_allreduce_sum(MgpuState* mg, float* buf, uint64_t count, cudaStream_t st);
 void mgpu_bytes(MgpuState* mg, uint64_t* ctx, uint64_t* crx, uint64_t* etx, uint64_t* erx);
 uint64_t mgpu_take_launches(MgpuState* mg);

@@ -1,0 +1,573 @@
+// Multi-GPU exchange v2: device-initiated, over NVLink peer memory.
+//
+// Every rank exports one "inbox" allocation (CUDA IPC, mapped by every peer):
+//   reqflag[N]    per source: {epoch, total records, pushes among them}
+//   respflag[N]   per owner:  {epoch}
+//   req[N][CAPS]  request records written by source s into region s
+//   rows[N][CAPS][D]  rows of dirty records (same index as the record)
+//   resp[N][CAPS][4 + D]  responses written by owner o into region o
+// One lookup is one round: requesters write their records (the eviction
+// pushes of their previous update first, then this lookup's requests)
+// straight into the owners' inboxes with 128-bit peer stores and publish the
+// round's epoch; owners link the records of each row (lock-free lists), apply
+// them per row in source-rank order -- eviction pushes (U4 of t-1), clock
+// checks against c_g after those pushes (L3), sync pushes (L4,
+// P:442-443), then answer every request with (c_g, row) (L5) -- and
+// write the responses straight into the requesters' inboxes.  No host
+// synchronisation; the step is CUDA-graph capturable.
+//
+// A hit passing condition (1) sends its pending row speculatively (dirty
+// entries); the owner applies it only if condition (2) fails (EXP2), which
+// folds the clock check (C1) into the same round as the fetches (C2), and
+// carrying the pushes of update t in round t+1 is the fusion of C3(t) with
+// C1(t+1) that SURVEY §8(e) notes has identical semantics (U4(t) precedes
+// L3(t+1) at every owner).
+//
+// Waits spin on flags in local memory written by peers (one process per GPU,
+// so the waited-for kernel always runs on another GPU); every wait has a
+// wall-clock timeout that raises a sticky error instead of hanging.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "het_internal.cuh"
+#include "het_p2p.h"
+
+namespace het {
+
+enum : uint32_t { K_PUSH = 0, K_NEEDQ = 1, K_EXP1 = 2, K_MISS = 3, K_DIRTY = 4 };
+constexpr unsigned long long WAIT_NS = 20ull * 1000 * 1000 * 1000;  // 20 s
+
+struct alignas(16) Flag {
+  unsigned long long epoch;
+  uint32_t total;
+  uint32_t pushes;
+};
+struct alignas(16) Rec {
+  int64_t key;
+  uint32_t cc;
+  uint32_t kind;
+};
+
+// POD view passed to kernels
+struct P2P {
+  int N, rank;
+  int64_t CAPS, REC;
+  uint32_t D;
+  char* const* peer;            // [N] base of every rank's inbox (own included)
+  size_t off_reqflag, off_respflag, off_req, off_rows, off_resp;
+  int32_t* lcnt;                // [N] this round's requests per owner
+  int32_t* c3cnt;               // [N] pending eviction pushes per owner
+  int32_t* ridx;                // [N][CAPS] unique index of each request
+  int32_t* head;                // [rows_local] list head per local row (-1)
+  int32_t* next;                // [N*CAPS]
+  int32_t* leaders;             // [N*CAPS]
+  int32_t* nlead;
+  int32_t* done;                // [4] last-block counters
+  unsigned long long* epoch;    // completed rounds
+  int32_t* qtot;                // [N] received totals (owner, this round)
+  int32_t* qpush;               // [N] received pushes (owner, this round)
+};
+
+__device__ __forceinline__ Flag* reqflag(const P2P& m, int r) { return (Flag*)(m.peer[r] + m.off_reqflag); }
+__device__ __forceinline__ Flag* respflag(const P2P& m, int r) { return (Flag*)(m.peer[r] + m.off_respflag); }
+__device__ __forceinline__ Rec* reqrec(const P2P& m, int r, int src) {
+  return (Rec*)(m.peer[r] + m.off_req) + (int64_t)src * m.CAPS;
+}
+__device__ __forceinline__ float* reqrow(const P2P& m, int r, int src, int64_t j) {
+  return (float*)(m.peer[r] + m.off_rows) + ((int64_t)src * m.CAPS + j) * m.D;
+}
+__device__ __forceinline__ float* resprec(const P2P& m, int r, int owner, int64_t j) {
+  return (float*)(m.peer[r] + m.off_resp) + ((int64_t)owner * m.CAPS + j) * m.REC;
+}
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// wait until flags[0..N) carry `epoch`; false on timeout (sticky error raised)
+__device__ bool wait_flags(Flag* flags, int N, unsigned long long epoch, Ctl* ctl) {
+  unsigned long long t0 = gtime();
+  for (int r = 0; r < N; ++r) {
+    while (ld_acquire(&flags[r].epoch) < epoch) {
+      if (gtime() - t0 > WAIT_NS) {
+        raise_err(ctl, 7 /*HET_ERR_NCCL: peer exchange timeout*/);
+        return false;
+      }
+      __nanosleep(64);
+    }
+  }
+  return true;
+}
+
+__device__ __forceinline__ float4 f4add_p(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+
+// block-aggregated wire-byte counters (clock tx/rx, embedding tx/rx)
+struct Bytes {
+  unsigned long long v[4];
+};
+__device__ __forceinline__ void bytes_init(unsigned long long* b) {
+  if (threadIdx.x < 4) b[threadIdx.x] = 0;
+}
+__device__ __forceinline__ void bytes_flush(const Dev& s, unsigned long long* b) {
+  if (threadIdx.x < 4 && b[threadIdx.x]) atomicAdd(&s.cnt[C_BCLK_TX + threadIdx.x], b[threadIdx.x]);
+}
+
+__device__ __forceinline__ bool last_block(int32_t* counter) {
+  __shared__ int s_last;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (s_last) __threadfence_system();
+  return s_last;
+}
+
+// ---------------------------------------------------------------- requester: build + publish
+__global__ void k_p2p_build(Dev s, Call c, P2P m, int drain) {
+  __shared__ unsigned long long sb[4];
+  bytes_init(sb);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long ep = *m.epoch + 1;
+  const int U = (drain || s.ctl->abort) ? 0 : s.ctl->U;
+  const int D4 = s.D >> 2;
+  for (int u = gw; u < U; u += nw) {
+    const uint8_t st = c.status[u];
+    if (st == ST_HIT) continue;
+    const int64_t key = c.uniq[u];
+    const int o = (int)(key % m.N);
+    const int32_t e = st == ST_MISS ? -1 : c.uentry[u];
+    uint32_t ecc = 0;
+    bool dirty = false;
+    if (e >= 0) { ecc = s.cc[e]; dirty = ecc > s.cs[e]; }
+    const uint32_t kind = (st == ST_NEEDQ ? K_NEEDQ : st == ST_EXP1 ? K_EXP1 : K_MISS) | (dirty ? K_DIRTY : 0);
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(&m.lcnt[o], 1);
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    const int64_t j = m.c3cnt[o] + slot;
+    if (lane == 0) {
+      Rec r;
+      r.key = key; r.cc = ecc; r.kind = kind;
+      reqrec(m, o, m.rank)[j] = r;
+      m.ridx[(int64_t)o * m.CAPS + slot] = u;
+      if (st == ST_NEEDQ) atomicAdd(&sb[0], 16ull);
+      else atomicAdd(&sb[2], 16ull);
+      if (dirty) atomicAdd(&sb[2], 4ull * s.D);
+    }
+    if (dirty) {
+      const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
+      float4* dst = reinterpret_cast<float4*>(reqrow(m, o, m.rank, j));
+      for (int d = lane; d < D4; d += 32) dst[d] = pr[d];
+    }
+  }
+  __syncthreads();
+  bytes_flush(s, sb);
+  if (!last_block(&m.done[0])) return;
+  if (threadIdx.x < m.N) {
+    const int o = threadIdx.x;
+    Flag* f = &reqflag(m, o)[m.rank];
+    f->total = (uint32_t)(m.c3cnt[o] + m.lcnt[o]);
+    f->pushes = (uint32_t)m.c3cnt[o];
+    __threadfence_system();
+    st_release(&f->epoch, ep);
+    m.c3cnt[o] = 0;
+  }
+  if (threadIdx.x == 0) m.done[0] = 0;
+}
+
+// ---------------------------------------------------------------- owner: wait + link
+__global__ void k_p2p_link(Dev s, P2P m) {
+  __shared__ int s_ok;
+  __shared__ int32_t tot[64];
+  const unsigned long long ep = *m.epoch + 1;
+  Flag* flags = reqflag(m, m.rank);
+  if (threadIdx.x == 0) s_ok = wait_flags(flags, m.N, ep, s.ctl);
+  __syncthreads();
+  if (!s_ok) return;
+  if (threadIdx.x < m.N) {
+    tot[threadIdx.x] = (int32_t)flags[threadIdx.x].total;
+    if (blockIdx.x == 0) { m.qtot[threadIdx.x] = (int32_t)flags[threadIdx.x].total; m.qpush[threadIdx.x] = (int32_t)flags[threadIdx.x].pushes; }
+  }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int src = 0; src < m.N; ++src) {
+    const Rec* rr = reqrec(m, m.rank, src);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot[src]; j += stride) {
+      const int64_t row = rr[j].key / m.N;
+      const int32_t id = (int32_t)(src * m.CAPS + j);
+      const int32_t old = atomicExch(&m.head[row], id);
+      m.next[id] = old;
+      if (old < 0) m.leaders[atomicAdd(m.nlead, 1)] = id;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- owner: apply + respond
+__global__ void k_p2p_process(Dev s, P2P m) {
+  __shared__ unsigned long long sb[4];
+  bytes_init(sb);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long ep = *m.epoch + 1;
+  const int nl = s.ctl->abort ? 0 : *m.nlead;
+  const int D4 = s.D >> 2;
+  for (int li = gw; li < nl; li += nw) {
+    const Rec* base = reqrec(m, m.rank, 0);
+    const int64_t row = base[m.leaders[li]].key / m.N;
+    // the row's records (<= 2 per source), lane i holds the i-th, sorted by id
+    // = (source rank, pushes before requests)
+    int32_t id = -1;
+    int cnt = 0;
+    if (lane == 0) {
+      int32_t cur = m.head[row];
+      int32_t buf[32];
+      while (cur >= 0 && cnt < 32) { buf[cnt++] = cur; cur = m.next[cur]; }
+      m.head[row] = -1;
+      for (int i = 1; i < cnt; ++i) {         // insertion sort (tiny)
+        int32_t x = buf[i]; int k = i - 1;
+        while (k >= 0 && buf[k] > x) { buf[k + 1] = buf[k]; --k; }
+        buf[k + 1] = x;
+      }
+      for (int i = 0; i < cnt; ++i) m.next[buf[i]] = i < cnt - 1 ? buf[i + 1] : -1;   // reuse as sorted chain
+      id = cnt ? buf[0] : -1;
+    }
+    __syncwarp();
+    cnt = __shfl_sync(0xffffffffu, cnt, 0);
+    int32_t first = __shfl_sync(0xffffffffu, id, 0);
+    float4* Wr = reinterpret_cast<float4*>(s.W + row * s.D);
+    uint32_t g = s.cg[row];
+    uint32_t validmask = 0;
+    // pass A: eviction pushes of the previous round (U4), source order
+    for (int32_t cur = first, i = 0; cur >= 0; cur = m.next[cur], ++i) {
+      const int src = cur / (int)m.CAPS;
+      const int64_t j = cur - (int64_t)src * m.CAPS;
+      if (j >= m.qpush[src]) continue;
+      const Rec r = base[cur];
+      const float4* pr = reinterpret_cast<const float4*>(reqrow(m, m.rank, src, j));
+      for (int d = lane; d < D4; d += 32) Wr[d] = f4add_p(Wr[d], pr[d]);
+      g = g > r.cc ? g : r.cc;
+      if (lane == 0) atomicAdd(&sb[3], 16ull + 4ull * s.D);
+    }
+    // pass B: condition (2) for hits that passed condition (1), c_g read now (L3)
+    for (int32_t cur = first, i = 0; cur >= 0; cur = m.next[cur], ++i) {
+      const int src = cur / (int)m.CAPS;
+      const int64_t j = cur - (int64_t)src * m.CAPS;
+      if (j < m.qpush[src]) continue;
+      const Rec r = base[cur];
+      if ((r.kind & 3) == K_NEEDQ && (g <= r.cc || g - r.cc <= s.s)) validmask |= 1u << i;
+    }
+    // pass C: sync pushes of expired hits (EXP1, EXP2), source order (L4)
+    for (int32_t cur = first, i = 0; cur >= 0; cur = m.next[cur], ++i) {
+      const int src = cur / (int)m.CAPS;
+      const int64_t j = cur - (int64_t)src * m.CAPS;
+      if (j < m.qpush[src] || ((validmask >> i) & 1)) continue;
+      const Rec r = base[cur];
+      if (!(r.kind & K_DIRTY)) continue;
+      const float4* pr = reinterpret_cast<const float4*>(reqrow(m, m.rank, src, j));
+      for (int d = lane; d < D4; d += 32) Wr[d] = f4add_p(Wr[d], pr[d]);
+      g = g > r.cc ? g : r.cc;
+    }
+    if (lane == 0) s.cg[row] = g;
+    __syncwarp();
+    // pass D: responses (L5): (c_g, status, row) straight into the requester's inbox
+    for (int32_t cur = first, i = 0; cur >= 0; cur = m.next[cur], ++i) {
+      const int src = cur / (int)m.CAPS;
+      const int64_t j = cur - (int64_t)src * m.CAPS;
+      if (j < m.qpush[src]) continue;
+      const int64_t q = j - m.qpush[src];
+      float* rec = resprec(m, src, m.rank, q);
+      const bool valid = (validmask >> i) & 1;
+      if (lane == 0) {
+        reinterpret_cast<uint32_t*>(rec)[0] = g;
+        reinterpret_cast<uint32_t*>(rec)[1] = valid ? 1u : 0u;
+        const Rec r = base[cur];
+        const bool q1 = (r.kind & 3) == K_NEEDQ;
+        atomicAdd(&sb[q1 ? 1 : 3], 16ull);                                 // request received
+        if (r.kind & K_DIRTY) atomicAdd(&sb[3], 4ull * s.D);
+        atomicAdd(&sb[valid ? 0 : 2], valid ? 8ull : 8ull + 4ull * s.D);   // response sent
+      }
+      if (!valid) {
+        float4* dst = reinterpret_cast<float4*>(rec + 4);
+        for (int d = lane; d < D4; d += 32) dst[d] = Wr[d];
+      }
+    }
+  }
+  __syncthreads();
+  bytes_flush(s, sb);
+  if (!last_block(&m.done[1])) return;
+  if (threadIdx.x < m.N) {
+    __threadfence_system();
+    st_release(&respflag(m, threadIdx.x)[m.rank].epoch, ep);
+  }
+  if (threadIdx.x == 0) { *m.nlead = 0; m.done[1] = 0; }
+}
+
+// ---------------------------------------------------------------- requester: wait + install
+__global__ void k_p2p_install(Dev s, Call c, P2P m) {
+  __shared__ int s_ok;
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ unsigned bc[2];
+  __shared__ int32_t lc[64];
+  __shared__ unsigned long long sb[4];
+  const unsigned long long ep = *m.epoch + 1;
+  bytes_init(sb);
+  dpop_init(dpop);
+  if (threadIdx.x < 2) bc[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_ok = wait_flags(respflag(m, m.rank), m.N, ep, s.ctl);
+  if (threadIdx.x < m.N) lc[threadIdx.x] = m.lcnt[threadIdx.x];
+  __syncthreads();
+  Ctl* ctl = s.ctl;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int D4 = s.D >> 2;
+  if (s_ok && !ctl->abort) {
+    for (int o = 0; o < m.N; ++o) {
+      for (int j = gw; j < lc[o]; j += nw) {
+        const int u = m.ridx[(int64_t)o * m.CAPS + j];
+        const float* rec = resprec(m, m.rank, o, j);
+        const uint32_t g = reinterpret_cast<const uint32_t*>(rec)[0];
+        const bool valid = reinterpret_cast<const uint32_t*>(rec)[1] != 0;
+        const uint8_t st = c.status[u];
+        if (lane == 0) atomicAdd(&sb[valid ? 1 : 3], valid ? 8ull : 8ull + 4ull * s.D);
+        if (st == ST_NEEDQ) {
+          if (lane == 0) {
+            c.status[u] = valid ? ST_HIT : ST_EXP2;
+            atomicAdd(&bc[valid ? 0 : 1], 1u);
+          }
+          if (valid) continue;
+        }
+        const int64_t key = c.uniq[u];
+        int32_t e;
+        if (st == ST_MISS) {
+          int32_t idx = 0;
+          if (lane == 0) idx = atomicSub(&ctl->ftop, 1) - 1;
+          idx = __shfl_sync(0xffffffffu, idx, 0);
+          if (idx < 0) {
+            if (lane == 0) raise_err(ctl, 4);
+            continue;
+          }
+          e = s.fstack[idx];
+          warp_insert(s, key, e, lane);
+          if (lane == 0) {
+            s.ekey[e] = key;
+            const uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
+            s.eprim[e] = prim;
+            if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
+            atomicMin(&ctl->min_install, prim);
+            c.uentry[u] = e;
+          }
+        } else {
+          e = c.uentry[u];
+        }
+        const float4* src = reinterpret_cast<const float4*>(rec + 4);
+        float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
+        for (int d = lane; d < D4; d += 32) vr[d] = src[d];
+        if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
+      }
+    }
+  }
+  __syncthreads();
+  dpop_flush(s, dpop);
+  bytes_flush(s, sb);
+  if (threadIdx.x == 0) {
+    if (bc[0]) atomicAdd(&s.cnt[C_HITS], (unsigned long long)bc[0]);
+    if (bc[1]) atomicAdd(&s.cnt[C_EXP2], (unsigned long long)bc[1]);
+  }
+  if (!last_block(&m.done[2])) return;
+  if (threadIdx.x == 0) { *m.epoch = ep; m.done[2] = 0; }
+}
+
+// ---------------------------------------------------------------- requester: eviction pushes
+// overflow victims (keys or entries from the selection) -> PUSH records in the
+// owners' inboxes, then delete + free locally.  Sent with the next round.
+struct EvView {  // leading fields of EvBuf
+  uint32_t* hist; uint32_t* khist; int32_t* victims; int32_t* cand; int32_t* sub; int32_t* flags;
+  int64_t* vkeys; uint8_t* vdirty; int64_t* vsel;
+};
+
+__global__ void k_p2p_pushes(Dev s, P2P m, EvView b) {
+  __shared__ unsigned long long sb[4];
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ unsigned s_dirty, s_ev;
+  dpop_init(dpop);
+  bytes_init(sb);
+  if (threadIdx.x == 0) { s_dirty = 0; s_ev = 0; }
+  __syncthreads();
+  Ctl* ctl = s.ctl;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int D4 = s.D >> 2;
+  const int count = (!ctl->abort && ctl->need > 0) ? ctl->nvict : 0;
+  for (int i = gw; i < count; i += nw) {
+    const int64_t key = ctl->vmode == 1 ? b.vsel[i] : s.ekey[b.victims[i]];
+    uint64_t slot = 0;
+    const int32_t e = warp_find_slot(s, key, lane, &slot);
+    if (e < 0) continue;
+    const uint32_t ecc = s.cc[e], ecs = s.cs[e], prim = s.eprim[e];
+    const bool dirty = ecc > ecs;
+    if (dirty) {
+      const int o = (int)(key % m.N);
+      int ps = 0;
+      if (lane == 0) ps = atomicAdd(&m.c3cnt[o], 1);
+      ps = __shfl_sync(0xffffffffu, ps, 0);
+      if (lane == 0) {
+        Rec r;
+        r.key = key; r.cc = ecc; r.kind = K_PUSH | K_DIRTY;
+        reqrec(m, o, m.rank)[ps] = r;
+        atomicAdd(&sb[2], 16ull + 4ull * s.D);
+      }
+      const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
+      float4* dst = reinterpret_cast<float4*>(reqrow(m, o, m.rank, ps));
+      for (int d = lane; d < D4; d += 32) dst[d] = pr[d];
+    }
+    if (lane == 0) {
+      s.hkey[slot] = HK_TOMB;
+      atomicAdd(&ctl->n_tomb, 1);
+      b.vkeys[i] = key;
+      b.vdirty[i] = dirty ? 1 : 0;
+      if (s.policy == 0) lfu_move(s, key, prim, EP_FREE, dpop);
+      s.eprim[e] = EP_FREE;
+      s.ekey[e] = -1;
+      s.fstack[atomicAdd(&ctl->ftop, 1)] = e;
+      atomicAdd(&s_ev, 1u);
+      if (dirty) atomicAdd(&s_dirty, 1u);
+    }
+  }
+  __syncthreads();
+  dpop_flush(s, dpop);
+  bytes_flush(s, sb);
+  if (threadIdx.x == 0) {
+    if (s_ev) atomicAdd(&s.cnt[C_EVICTIONS], (unsigned long long)s_ev);
+    if (s_dirty) atomicAdd(&s.cnt[C_DIRTY_PUSHES], (unsigned long long)s_dirty);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+struct P2PState {
+  P2P v{};
+  char* inbox = nullptr;
+  std::vector<char*> mapped;     // opened peer bases (to close)
+  std::vector<void*> allocs;
+};
+
+template <typename T>
+static bool p_alloc(P2PState* p, T** q, size_t count) {
+  void* x = nullptr;
+  if (cudaMalloc(&x, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) return false;
+  p->allocs.push_back(x);
+  *q = reinterpret_cast<T*>(x);
+  return true;
+}
+
+het_status_t p2p_create(P2PState*& out, const Dev& d, uint32_t n_max, ncclComm_t comm, cudaStream_t st) {
+  P2PState* p = new P2PState();
+  out = p;
+  P2P& v = p->v;
+  v.N = d.world;
+  v.rank = d.rank;
+  v.CAPS = 3 * (int64_t)n_max;
+  v.REC = 4 + d.D;
+  v.D = d.D;
+  const int N = v.N;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t off = 0;
+  v.off_reqflag = off; off = al(off + sizeof(Flag) * N);
+  v.off_respflag = off; off = al(off + sizeof(Flag) * N);
+  v.off_req = off; off = al(off + sizeof(Rec) * N * v.CAPS);
+  v.off_rows = off; off = al(off + sizeof(float) * N * v.CAPS * d.D);
+  v.off_resp = off; off = al(off + sizeof(float) * N * v.CAPS * v.REC);
+  if (cudaMalloc(&p->inbox, off) != cudaSuccess) return HET_ERR_OOM;
+  cudaMemsetAsync(p->inbox, 0, v.off_req, st);                      // flags: epoch 0
+  cudaIpcMemHandle_t mine;
+  if (cudaIpcGetMemHandle(&mine, p->inbox) != cudaSuccess) return HET_ERR_CUDA;
+  char* dh;
+  if (cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * N) != cudaSuccess) return HET_ERR_OOM;
+  cudaMemcpyAsync(dh + sizeof(cudaIpcMemHandle_t) * d.rank, &mine, sizeof(mine), cudaMemcpyHostToDevice, st);
+  if (ncclAllGather(dh + sizeof(cudaIpcMemHandle_t) * d.rank, dh, sizeof(cudaIpcMemHandle_t), ncclChar, comm, st) !=
+      ncclSuccess)
+    return HET_ERR_NCCL;
+  std::vector<cudaIpcMemHandle_t> all(N);
+  cudaMemcpyAsync(all.data(), dh, sizeof(cudaIpcMemHandle_t) * N, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
+  cudaFree(dh);
+  std::vector<char*> bases(N);
+  for (int r = 0; r < N; ++r) {
+    if (r == d.rank) { bases[r] = p->inbox; continue; }
+    void* q = nullptr;
+    if (cudaIpcOpenMemHandle(&q, all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return HET_ERR_CUDA;
+    bases[r] = (char*)q;
+    p->mapped.push_back((char*)q);
+  }
+  char** dbases;
+  if (!p_alloc(p, &dbases, N)) return HET_ERR_OOM;
+  cudaMemcpyAsync(dbases, bases.data(), sizeof(char*) * N, cudaMemcpyHostToDevice, st);
+  v.peer = dbases;
+  const int64_t NC = (int64_t)N * v.CAPS;
+  bool ok = p_alloc(p, &v.lcnt, N) && p_alloc(p, &v.c3cnt, N) && p_alloc(p, &v.ridx, NC) &&
+            p_alloc(p, &v.head, d.rows_local) && p_alloc(p, &v.next, NC) && p_alloc(p, &v.leaders, NC) &&
+            p_alloc(p, &v.nlead, 1) && p_alloc(p, &v.done, 4) && p_alloc(p, &v.epoch, 1) &&
+            p_alloc(p, &v.qtot, N) && p_alloc(p, &v.qpush, N);
+  if (!ok) return HET_ERR_OOM;
+  cudaMemsetAsync(v.lcnt, 0, 4 * N, st);
+  cudaMemsetAsync(v.c3cnt, 0, 4 * N, st);
+  cudaMemsetAsync(v.head, 0xFF, 4 * d.rows_local, st);
+  cudaMemsetAsync(v.nlead, 0, 4, st);
+  cudaMemsetAsync(v.done, 0, 16, st);
+  cudaMemsetAsync(v.epoch, 0, 8, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
+  return HET_OK;
+}
+
+void p2p_destroy(P2PState* p) {
+  if (!p) return;
+  for (char* q : p->mapped) cudaIpcCloseMemHandle(q);
+  for (void* q : p->allocs) cudaFree(q);
+  if (p->inbox) cudaFree(p->inbox);
+  delete p;
+}
+
+static int grid_p(int64_t units_warps) {
+  int64_t b = (units_warps + 7) / 8;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 4));
+}
+
+// one exchange round (after probe); drain = no requests, only pending pushes
+int p2p_round(P2PState* p, const Dev& d, const Call& c, int drain, cudaStream_t st) {
+  P2P& v = p->v;
+  cudaMemsetAsync(v.lcnt, 0, 4 * v.N, st);
+  k_p2p_build<<<grid_p(std::max(c.n, 1)), 256, 0, st>>>(d, c, v, drain);
+  k_p2p_link<<<148, 256, 0, st>>>(d, v);
+  k_p2p_process<<<148 * 2, 256, 0, st>>>(d, v);
+  k_p2p_install<<<148 * 2, 256, 0, st>>>(d, c, v);
+  return 4;
+}
+
+int p2p_pushes(P2PState* p, const Dev& d, void* evbuf, cudaStream_t st) {
+  EvView b = *reinterpret_cast<EvView*>(evbuf);
+  k_p2p_pushes<<<148 * 2, 256, 0, st>>>(d, p->v, b);
+  return 1;
+}
+
+}  // namespace het

@@ -1,0 +1,20 @@
+// Device-initiated multi-GPU exchange over NVLink peer memory (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "../../include/het.h"
+#include "het_internal.cuh"
+
+namespace het {
+
+struct P2PState;
+
+het_status_t p2p_create(P2PState*& out, const Dev& d, uint32_t n_max, ncclComm_t comm, cudaStream_t st);
+void p2p_destroy(P2PState* p);
+// one lookup round after the probe: build + publish, owner link + process, install
+int p2p_round(P2PState* p, const Dev& d, const Call& c, int drain, cudaStream_t st);
+// eviction pushes of the current update (sent with the next round)
+int p2p_pushes(P2PState* p, const Dev& d, void* evbuf, cudaStream_t st);
+
+}  // namespace het

@@ -240,10 +240,22 @@ k_rank_sort(const int64_t* __restrict__ keys, int n, int64_t R, int pbits, Ctl* 
   extern __shared__ uint64_t comp[];
   __shared__ int part[RANK_WARPS][32];
   int bad = 0;
-  for (int q = threadIdx.x; q < n; q += blockDim.x) {
-    int64_t k = keys[q];
-    if (k < 0 || k >= R) bad = 1;
-    comp[q] = ((uint64_t)k << pbits) | (uint64_t)q;
+  constexpr int RI = RANK_MAX / (RANK_WARPS * 32);
+  {  // all key loads of this thread in flight at once
+    int64_t kk[RI];
+#pragma unroll
+    for (int i = 0; i < RI; ++i) {
+      const int q = threadIdx.x + i * RANK_WARPS * 32;
+      kk[i] = q < n ? __ldg(&keys[q]) : 0;
+    }
+#pragma unroll
+    for (int i = 0; i < RI; ++i) {
+      const int q = threadIdx.x + i * RANK_WARPS * 32;
+      if (q < n) {
+        if (kk[i] < 0 || kk[i] >= R) bad = 1;
+        comp[q] = ((uint64_t)kk[i] << pbits) | (uint64_t)q;
+      }
+    }
   }
   if (__syncthreads_or(bad)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/);

@@ -67,10 +67,21 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
   __shared__ int s_last;
   Ctl* ctl = s.ctl;
   int bad = 0;
-  for (int q = threadIdx.x; q < n; q += blockDim.x) {
-    int64_t k = keys[q];
-    if (k < 0 || k >= s.R) bad = 1;
-    comp[q] = ((uint64_t)k << pbits) | (uint64_t)q;
+  {  // all key loads of this thread in flight at once
+    int64_t kk[DDF_ITEMS];
+#pragma unroll
+    for (int i = 0; i < DDF_ITEMS; ++i) {
+      const int q = threadIdx.x + i * DDF_THREADS;
+      kk[i] = q < n ? __ldg(&keys[q]) : 0;
+    }
+#pragma unroll
+    for (int i = 0; i < DDF_ITEMS; ++i) {
+      const int q = threadIdx.x + i * DDF_THREADS;
+      if (q < n) {
+        if (kk[i] < 0 || kk[i] >= s.R) bad = 1;
+        comp[q] = ((uint64_t)kk[i] << pbits) | (uint64_t)q;
+      }
+    }
   }
   bad = __syncthreads_or(bad);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

@@ -240,16 +240,31 @@ class HetCache:
     def update(self, keys, grads, lr):
         het_update(self.h, keys, keys.numel(), grads, lr)
 
-    def capture_step(self, keys, grads, out, lr):
-        """Capture one lookup (HET_CLOCK_AUTO) + update on static device
-        buffers into a CUDA graph; replay() runs the whole step.  Run at least
-        one uncaptured step first (lazy one-time attribute setup)."""
+    def step(self, keys, grads, out, lr, dense=None, side=None):
+        """One training step of the sparse path: lookup (HET_CLOCK_AUTO) +
+        update; with `dense` (N > 1) the dense all-reduce (Eq. 2) runs
+        concurrently on the side stream (async communication)."""
         torch = self.torch
         n = keys.numel()
+        cs = torch.cuda.current_stream()
+        if dense is not None:
+            side.wait_stream(cs)
+            with torch.cuda.stream(side):
+                het_dense_allreduce(self.h, dense, dense.numel(), stream=side)
+        het_lookup(self.h, keys, n, HET_CLOCK_AUTO, out)
+        het_update(self.h, keys, n, grads, lr)
+        if dense is not None:
+            cs.wait_stream(side)
+
+    def capture_step(self, keys, grads, out, lr, dense=None):
+        """Capture step() on static device buffers into a CUDA graph;
+        replay() runs the whole step.  Run at least one uncaptured step first
+        (lazy one-time attribute setup)."""
+        torch = self.torch
         g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream() if dense is not None else None
         with torch.cuda.graph(g, capture_error_mode="relaxed"):
-            het_lookup(self.h, keys, n, HET_CLOCK_AUTO, out)
-            het_update(self.h, keys, n, grads, lr)
+            self.step(keys, grads, out, lr, dense, side)
         return g
 
     def evict(self, keys=None):

@@ -18,11 +18,15 @@ def ngpu():
 
 @pytest.mark.skipif(ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("policy,s,frac", [(0, 10, 0.1), (1, 3, 0.05), (0, 0, 0.1), (0, 0xFFFFFFFF, 0.2)])
-def test_multi_gpu_parity(policy, s, frac):
+@pytest.mark.parametrize("p2p", ["1", "0"])
+def test_multi_gpu_parity(policy, s, frac, p2p):
+    """p2p=1: device-initiated exchange over NVLink peer memory (default);
+    p2p=0: the NCCL send/recv exchange with host-read counts."""
     n = min(ngpu(), 4)
+    env = dict(os.environ, HET_P2P=p2p)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={29500 + policy * 7 + (s % 97)}",
+           "--master-addr=127.0.0.1", f"--master-port={29500 + policy * 7 + (s % 97) + 200 * int(p2p)}",
            os.path.join(ROOT, "tests", "mgpu_worker.py"), str(policy), str(s), str(frac), "60"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert "MGPU_OK" in r.stdout
