@@ -43,7 +43,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     inc, libdir = nccl_dirs()
     os.makedirs(BUILD, exist_ok=True)
-    flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
+    extra = ["-DHET_TIMELINE"] if os.environ.get("HET_TIMELINE") else []
+    flags = ARCH + extra + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
                     "-Xptxas", "-v" if verbose else "-O3", "-I", inc, "-I", os.path.join(ROOT, "include")]
     objs = []
     procs = []

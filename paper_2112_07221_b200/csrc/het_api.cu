@@ -295,6 +295,7 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   A(d.count_by_key, d.lfu_persist ? rows : 1);
   d.bm_words = ((int64_t)rows + 31) / 32;
   d.nbk = ((int64_t)rows + (1 << LFU_BLK_SHIFT) - 1) >> LFU_BLK_SHIFT;
+  d.nbk2 = (d.nbk + 63) >> 6;
   d.lfu_cb = 0;
   if (policy == HET_LFU) {  // count bitmaps, bounded to ~1 GB
     int cb = LFU_CB_MAX;
@@ -305,6 +306,7 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   }
   A(d.bm, d.lfu_cb ? (size_t)d.lfu_cb * d.bm_words : 1);
   A(d.bcnt, d.lfu_cb ? (size_t)d.lfu_cb * d.nbk : 1);
+  A(d.bcnt2, d.lfu_cb ? (size_t)d.lfu_cb * d.nbk2 : 1);
   A(d.pop, LFU_CB_MAX);
   A(d.ctl, 1);
   A(d.cnt, C_NUM);
@@ -351,6 +353,7 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   if (d.lfu_cb) {
     cudaMemsetAsync(d.bm, 0, (size_t)d.lfu_cb * d.bm_words * 4, stream);
     cudaMemsetAsync(d.bcnt, 0, (size_t)d.lfu_cb * d.nbk * 4, stream);
+    cudaMemsetAsync(d.bcnt2, 0, (size_t)d.lfu_cb * d.nbk2 * 4, stream);
   }
   cudaMemsetAsync(d.pop, 0, LFU_CB_MAX * 4, stream);
   launch_reset_cache(d, stream);
@@ -555,6 +558,7 @@ het_status_t het_sync(het_cache_t h, het_stream_t stream_) {
   if (d.lfu_cb) {
     cudaMemsetAsync(d.bm, 0, (size_t)d.lfu_cb * d.bm_words * 4, st);
     cudaMemsetAsync(d.bcnt, 0, (size_t)d.lfu_cb * d.nbk * 4, st);
+    cudaMemsetAsync(d.bcnt2, 0, (size_t)d.lfu_cb * d.nbk2 * 4, st);
   }
   cudaMemsetAsync(d.pop, 0, LFU_CB_MAX * 4, st);
   h->have_lookup = false;

@@ -63,7 +63,12 @@ struct Ctl {
   int32_t rebuild_req;  // hash rebuild requested for the next update
   uint32_t lk_seq;      // lookup sequence number
   int32_t nsel;         // victim keys extracted by the fused update
-  int32_t pad5_;
+  uint32_t plan_seq;    // fused update: plan of round lk_seq published
+  int32_t ntask;        // fused update: non-empty bitmap blocks to extract
+  int32_t ext_next;     // work queue cursors
+  int32_t ext_done;
+  int32_t find_next;
+  int32_t pad6_;
   uint32_t lowmask;     // bit c set: some resident has LFU count c < T (snapshot for enumeration)
   int64_t Kstar;        // LFU bitmap path: largest victim key among count == T
   uint64_t t_cur;       // clock of the current call (LRU tick)
@@ -91,8 +96,8 @@ struct Dev {
   Ctl* ctl; unsigned long long* cnt;
   // LFU count bitmaps (P:632 LFU): bit (c, key) set iff
   // key is resident with count c < lfu_cb; bcnt = set bits per 4096-key block
-  int lfu_cb; int64_t bm_words; int64_t nbk;
-  uint32_t* bm; uint32_t* bcnt; int32_t* pop;
+  int lfu_cb; int64_t bm_words; int64_t nbk; int64_t nbk2;
+  uint32_t* bm; uint32_t* bcnt; uint32_t* bcnt2; int32_t* pop;   // bcnt2: per 64 blocks
 };
 
 // Per-call scratch (sized by n_max at create)
@@ -173,6 +178,31 @@ __device__ __forceinline__ int32_t warp_find_slot(const Dev& s, int64_t key, int
   return -1;
 }
 
+// Single-thread find (for many keys per warp): scans whole 32-slot windows
+// (16 x 16 B loads) with the same stop rule as warp_find.
+__device__ __forceinline__ int32_t thread_find_slot(const Dev& s, int64_t key, uint64_t* slot_out) {
+  uint64_t w = hash_home(s, key);
+  for (int it = 0; it < (1 << 20); ++it) {
+    const longlong2* win = reinterpret_cast<const longlong2*>(s.hkey + w);
+    bool empty = false;
+    int hit = -1;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const longlong2 v = win[q];
+      if (v.x == key) hit = 2 * q;
+      if (v.y == key) hit = 2 * q + 1;
+      empty |= (v.x == HK_EMPTY) | (v.y == HK_EMPTY);
+    }
+    if (hit >= 0) {
+      *slot_out = w + hit;
+      return s.hval[w + hit];
+    }
+    if (empty) return -1;
+    w = (w + 32) & s.hmask;
+  }
+  return -1;
+}
+
 // Warp-cooperative insert of a key known to be absent.  Claims the first
 // EMPTY or TOMB slot in probe order with atomicCAS.
 __device__ __forceinline__ void warp_insert(const Dev& s, int64_t key, int32_t entry, int lane) {
@@ -235,11 +265,13 @@ __device__ __forceinline__ void lfu_move(const Dev& s, int64_t key, uint32_t old
   if (oldc < (uint32_t)s.lfu_cb) {
     atomicAnd(&s.bm[(int64_t)oldc * s.bm_words + w], ~bit);
     atomicSub(&s.bcnt[(int64_t)oldc * s.nbk + blk], 1u);
+    atomicSub(&s.bcnt2[(int64_t)oldc * s.nbk2 + (blk >> 6)], 1u);
     atomicSub(&dpop[oldc], 1);
   }
   if (newc < (uint32_t)s.lfu_cb) {
     atomicOr(&s.bm[(int64_t)newc * s.bm_words + w], bit);
     atomicAdd(&s.bcnt[(int64_t)newc * s.nbk + blk], 1u);
+    atomicAdd(&s.bcnt2[(int64_t)newc * s.nbk2 + (blk >> 6)], 1u);
     atomicAdd(&dpop[newc], 1);
   }
 }

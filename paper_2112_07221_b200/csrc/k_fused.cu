@@ -25,9 +25,40 @@
 
 namespace het {
 
+// ---- optional timeline instrumentation (-DHET_TIMELINE): %globaltimer marks
+// per kernel k: [0] min block start, [1] max block start, [2] max work end,
+// [3] last-block tail start, [4] tail end
+#ifdef HET_TIMELINE
+// per-warp slots (no contention): g_tlw[mark][warp], read and reduced on the host
+constexpr int TLW = 8192;
+__device__ unsigned long long g_tlw[24 * TLW];
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_W(i) do { if ((threadIdx.x & 31) == 0) { int w_ = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; \
+  if (w_ < TLW) g_tlw[(i) * TLW + w_] = tl_now(); } } while (0)
+#define TL_MIN(i) TL_W(i)
+#define TL_MAX(i) TL_W(i)
+extern "C" int het_debug_timeline(unsigned long long* out, int marks, int warps) {
+  cudaDeviceSynchronize();
+  if (out) cudaMemcpyFromSymbol(out, g_tlw, sizeof(unsigned long long) * (size_t)marks * TLW);
+  cudaMemset((void*)0, 0, 0);
+  static unsigned long long* zero = nullptr;
+  if (!zero) zero = (unsigned long long*)calloc(24 * TLW, 8);
+  cudaMemcpyToSymbol(g_tlw, zero, sizeof(unsigned long long) * 24 * TLW);
+  (void)warps;
+  return 0;
+}
+#else
+#define TL_MIN(i) do {} while (0)
+#define TL_MAX(i) do {} while (0)
+#endif
+
 constexpr int DDF_THREADS = 512;
 constexpr int DDF_WARPS = DDF_THREADS / 32;
-constexpr int DDF_ITEMS = 16;   // FUSED_MAX / DDF_THREADS
+constexpr int DDF_ITEMS = 16;   // FUSED_MAX / DDF_THREADS (elements per lane in the finish)
 constexpr int LK_WARPS = 8;
 constexpr int UPD_THREADS = 256;
 constexpr int UPD_WARPS = UPD_THREADS / 32;
@@ -66,6 +97,7 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
   __shared__ int warp_sums[32];
   __shared__ int s_last;
   Ctl* ctl = s.ctl;
+  TL_MIN(0); TL_MAX(1);
   int bad = 0;
   {  // all key loads of this thread in flight at once
     int64_t kk[DDF_ITEMS];
@@ -84,6 +116,17 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
     }
   }
   bad = __syncthreads_or(bad);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {   // per-call begin, overlapped with the rank work
+    if (lookup) {
+      if (t == CLOCK_AUTO) { t = ctl->t_auto; ctl->t_auto = t + 1; }
+      ctl->t_cur = t;
+      ctl->lk_seq = ctl->lk_seq + 1;
+      s.cnt[C_LOOKUPS] += 1;
+      s.cnt[C_KEYS] += (unsigned long long)n;
+    }
+    ctl->abort = 0;
+    if (bad) { raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/); ctl->U = 0; c.seg_off[0] = 0; }
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int p = blockIdx.x * 32 + lane;
   if (!bad) {
@@ -100,60 +143,67 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
 #pragma unroll
       for (int w = 0; w < DDF_WARPS; ++w) r += part[w][lane];
       c.sortbuf0[r] = mine;
+      c.perm[r] = p;                 // stable position grouping, written here (distributed)
     }
   }
+  TL_MAX(2);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&ctl->dd_done, 1) == (int)gridDim.x - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // ---- last block: per-call begin + head flags / scan / outputs
-  if (threadIdx.x == 0) {
-    ctl->dd_done = 0;
-    if (lookup) {
-      if (t == CLOCK_AUTO) { t = ctl->t_auto; ctl->t_auto = t + 1; }
-      ctl->t_cur = t;
-      ctl->lk_seq = ctl->lk_seq + 1;
-      s.cnt[C_LOOKUPS] += 1;
-      s.cnt[C_KEYS] += (unsigned long long)n;
-    }
-    ctl->abort = 0;
-    if (bad) { raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/); ctl->U = 0; c.seg_off[0] = 0; }
-  }
+  TL_MAX(3);
+  // ---- last block: head flags / scan / outputs
+  if (threadIdx.x == 0) ctl->dd_done = 0;
   if (bad) return;
-  // each thread owns DDF_ITEMS consecutive sorted composites, loaded at once
+  // warp w owns the contiguous segment [w*seg, (w+1)*seg) of the sorted
+  // composites: coalesced loads, head flags by ballot, one cross-warp prefix
   const uint64_t* sorted = c.sortbuf0;
-  const int j0 = threadIdx.x * DDF_ITEMS;
-  uint64_t x[DDF_ITEMS + 1];
+  const int seg = ((n + DDF_WARPS - 1) / DDF_WARPS + 31) & ~31;
+  const int s0 = wid * seg, s1 = min(n, s0 + seg);
+  uint64_t x[DDF_ITEMS];
+  unsigned hm[DDF_ITEMS];
+  uint64_t prevlast = (s0 > 0 && s0 <= n) ? __ldcg(&sorted[s0 - 1]) : ~0ull;
 #pragma unroll
-  for (int i = 0; i <= DDF_ITEMS; ++i) {
-    const int j = j0 + i - 1;                  // x[0] = previous element
-    x[i] = (j >= 0 && j < n) ? __ldcg(&sorted[j]) : ~0ull;
+  for (int i = 0; i < DDF_ITEMS; ++i) {
+    const int j = s0 + i * 32 + lane;
+    x[i] = j < s1 ? __ldcg(&sorted[j]) : ~0ull;
   }
-  int heads = 0;
+  int wcnt = 0;
+  TL_MAX(5);
 #pragma unroll
-  for (int i = 1; i <= DDF_ITEMS; ++i) {
-    const int j = j0 + i - 1;
-    if (j < n && (j == 0 || (x[i] >> pbits) != (x[i - 1] >> pbits))) ++heads;
+  for (int i = 0; i < DDF_ITEMS; ++i) {
+    const int j = s0 + i * 32 + lane;
+    uint64_t prev = __shfl_up_sync(0xffffffffu, x[i], 1);
+    if (lane == 0) prev = prevlast;
+    const bool head = j < s1 && (j == 0 || (x[i] >> pbits) != (prev >> pbits));
+    hm[i] = __ballot_sync(0xffffffffu, head);
+    wcnt += __popc(hm[i]);
+    prevlast = __shfl_sync(0xffffffffu, x[i], 31);
   }
-  int tot;
-  int u = block_scan_int(heads, warp_sums, &tot) - 1;
+  if (lane == 0) warp_sums[wid] = wcnt;
+  __syncthreads();
+  int base = 0, tot = 0;
+  for (int w = 0; w < DDF_WARPS; ++w) {
+    const int v = warp_sums[w];
+    if (w < wid) base += v;
+    tot += v;
+  }
+  TL_MAX(6);
+  int run = base - 1;                 // unique index of the last head seen
 #pragma unroll
-  for (int i = 1; i <= DDF_ITEMS; ++i) {
-    const int j = j0 + i - 1;
-    if (j < n) {
-      const int pos = (int)(x[i] & ((1ull << pbits) - 1));
-      if (j == 0 || (x[i] >> pbits) != (x[i - 1] >> pbits)) {
-        ++u;
-        c.uniq[u] = (int64_t)(x[i] >> pbits);
-        c.seg_off[u] = j;
-      }
-      c.perm[j] = pos;
-      c.inverse[pos] = u;
+  for (int i = 0; i < DDF_ITEMS; ++i) {
+    const int j = s0 + i * 32 + lane;
+    const int u = run + __popc(hm[i] & ((2u << lane) - 1u));   // heads up to and including lane
+    if (j < s1 && ((hm[i] >> lane) & 1u)) {   // perm: rank blocks; inverse: the lookup kernel
+      c.uniq[u] = (int64_t)(x[i] >> pbits);
+      c.seg_off[u] = j;
     }
+    run += __popc(hm[i]);
   }
   if (threadIdx.x == 0) { c.seg_off[tot] = n; ctl->U = tot; }
+  TL_MAX(4);
 }
 
 // ------------------------------------------------------------------ K_look
@@ -190,6 +240,7 @@ __device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_su
     }
   }
   __syncthreads();
+  TL_MAX(7);
   if (s_T < 0) return;
   const int T = s_T;
   const int64_t needT = s_needT;
@@ -197,16 +248,36 @@ __device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_su
   const uint32_t* bm = s.bm + (int64_t)T * s.bm_words;
   if (threadIdx.x == 0) { s_done = 0; s_blk = -1; }
   __syncthreads();
+  // level 2: the 64-block super-block holding the needT-th bit (chunks of blockDim)
+  __shared__ long long s_sb, s_sbbefore;
+  const uint32_t* bc2 = s.bcnt2 + (int64_t)T * s.nbk2;
   long long carry = 0;
-  for (int64_t base = 0; base < s.nbk && !s_done; base += blockDim.x) {
+  for (int64_t base = 0; base < s.nbk2 && !s_done; base += blockDim.x) {
     const int64_t k = base + threadIdx.x;
-    const long long x = k < s.nbk ? (long long)__ldcg(&bc[k]) : 0;
+    const long long x = k < s.nbk2 ? (long long)__ldcg(&bc2[k]) : 0;
     long long tot;
     const long long ex = carry + block_excl_scan64(x, warp_sums, &tot);
-    if (x > 0 && ex < needT && ex + x >= needT) { s_blk = k; s_before = ex; s_done = 1; }
+    if (x > 0 && ex < needT && ex + x >= needT) { s_sb = k; s_sbbefore = ex; s_done = 1; }
     carry += tot;
     __syncthreads();
   }
+  // level 1: the block inside the super-block (64 counters, one warp)
+  if (s_done && threadIdx.x < 32) {
+    const int64_t b0 = s_sb << 6;
+    const int64_t k0 = b0 + 2 * threadIdx.x;
+    const long long x0 = k0 < s.nbk ? (long long)__ldcg(&bc[k0]) : 0;
+    const long long x1 = k0 + 1 < s.nbk ? (long long)__ldcg(&bc[k0 + 1]) : 0;
+    long long incl = x0 + x1;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)threadIdx.x >= o) incl += y;
+    }
+    const long long ex = s_sbbefore + incl - x0 - x1;
+    if (x0 > 0 && ex < needT && ex + x0 >= needT) { s_blk = k0; s_before = ex; }
+    if (x1 > 0 && ex + x0 < needT && ex + x0 + x1 >= needT) { s_blk = k0 + 1; s_before = ex + x0; }
+  }
+  __syncthreads();
+  TL_MAX(9);
   if (s_blk < 0) return;
   if (threadIdx.x < 32) {
     const int64_t blk = s_blk;
@@ -256,6 +327,7 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
   __shared__ long long warp_sums[32];
   if (threadIdx.x < 4) bc[threadIdx.x] = 0;
   dpop_init(dpop);
+  TL_MIN(8); TL_MAX(9);
   __syncthreads();
   Ctl* ctl = s.ctl;
   const int lane = threadIdx.x & 31;
@@ -272,6 +344,7 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
     if (lane == 1 && s.s != S_INF) gpre = s.cg[key];
     int32_t e = warp_find(s, key, lane);
     gpre = __shfl_sync(0xffffffffu, gpre, 1);
+    TL_MAX(13);
     uint8_t st = ST_MISS;
     uint32_t ecs = 0, ecc = 0;
     if (e >= 0) { ecs = s.cs[e]; ecc = s.cc[e]; }
@@ -330,6 +403,8 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
         if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
       }
     }
+    TL_MAX(14);
+    for (int k = lane; k < cnt; k += 32) c.inverse[k < 32 ? pos_lane : c.perm[j0 + k]] = u;
     if (e >= 0) {
       if (lane == 0) c.uentry[u] = e;
       // L7 Get, scattered to the occurrences of the key (128-bit stores)
@@ -337,6 +412,7 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
       float4* o4 = reinterpret_cast<float4*>(out);
       for (int d = lane; d - lane < D4; d += 32) {
         float4 val = d < D4 ? vr[d] : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (d == lane) { __syncwarp(); TL_MAX(15); }
         for (int kb = 0; kb < cnt; kb += 32) {
           const int src = kb == 0 ? pos_lane : (kb + lane < cnt ? c.perm[j0 + kb + lane] : 0);
           const int m = min(32, cnt - kb);
@@ -348,6 +424,7 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
       }
     }
   }
+  TL_MAX(10);
   __syncthreads();
   dpop_flush(s, dpop);
   if (threadIdx.x == 0) {
@@ -357,29 +434,6 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
     if (bc[3]) atomicAdd(&s.cnt[C_MISSES], (unsigned long long)bc[3]);
     if (blockIdx.x == 0 && !ctl->abort) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
   }
-  // ---- last block: this step's eviction plan (needs every install and count)
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&ctl->lk_done, 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int64_t res = s.Ecap - (int64_t)__ldcg(&ctl->ftop);
-  const int64_t need = res - s.C;
-  if (threadIdx.x == 0) {
-    ctl->lk_done = 0;
-    ctl->nvict = 0; ctl->ncand = 0; ctl->nsub = 0; ctl->vmode = 0; ctl->nsel = 0;
-    const bool none = __ldcg(&ctl->abort) || need <= 0;
-    ctl->need = none ? 0 : need;
-    ctl->emode = none ? 0 : ((s.policy == 0 && s.lfu_cb && need < res) ? 1 : 2);
-    ctl->generic = ctl->emode == 2;
-    const int64_t S = (int64_t)s.hmask + 1;
-    ctl->rebuild_req = (int64_t)__ldcg(&ctl->n_tomb) > S / 8;
-  }
-  __syncthreads();
-  if (ctl->emode == 1) lfu_threshold(s, warp_sums_i, warp_sums, need);
-  __syncthreads();
-  if (threadIdx.x == 0) ctl->generic = ctl->emode == 2;
 }
 
 // ------------------------------------------------------------------ K_upd
@@ -500,53 +554,106 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   if (threadIdx.x == 0) { s_dirty = 0; s_ev = 0; }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) { mbar_init(&bars[wid], 1); fence_mbar_init(); }
+  TL_MIN(16); TL_MAX(17);
   __syncthreads();
   const bool abort = ctl->abort;
   const int U = abort ? 0 : ctl->U;
-  const int emode = abort ? 0 : ctl->emode;
-  const bool rebuild = ctl->rebuild_req;
-  const uint32_t T = ctl->T;
-  const int64_t Kstar = ctl->Kstar;
-  const uint32_t lowmask = ctl->lowmask;
+  // ---- block 0: this step's eviction plan (need, mode, LFU threshold T / K*,
+  // hash maintenance), in parallel with the segment reduce of the other blocks
+  if (blockIdx.x == 0) {
+    __shared__ long long warp_sums[32];
+    __shared__ int warp_sums_i[32];
+    const int64_t res = s.Ecap - (int64_t)ctl->ftop;
+    const int64_t need = res - s.C;
+    if (threadIdx.x == 0) {
+      ctl->nvict = 0; ctl->ncand = 0; ctl->nsub = 0; ctl->vmode = 0; ctl->nsel = 0;
+      const bool none = abort || need <= 0;
+      ctl->need = none ? 0 : need;
+      ctl->emode = none ? 0 : ((s.policy == 0 && s.lfu_cb && need < res) ? 1 : 2);
+      const int64_t S = (int64_t)s.hmask + 1;
+      ctl->rebuild_req = (int64_t)ctl->n_tomb > S / 8;
+    }
+    __syncthreads();
+    TL_MAX(22);
+    if (ctl->emode == 1) lfu_threshold(s, warp_sums_i, warp_sums, need);
+    __syncthreads();
+    if (threadIdx.x == 0) ctl->generic = ctl->emode == 2;
+    __syncthreads();
+    // task list: every non-empty count bitmap block holding victims -- all
+    // blocks of the counts < T in lowmask, blocks up to K*'s for count T --
+    // one coalesced pass over the block counters by the whole block
+    if (ctl->emode == 1) {
+      __shared__ int s_nt;
+      if (threadIdx.x == 0) s_nt = 0;
+      __syncthreads();
+      const uint32_t T = ctl->T;
+      const int64_t kblk = ctl->Kstar >> LFU_BLK_SHIFT;
+      const uint32_t lowmask = ctl->lowmask;
+      for (uint32_t cc = 0; cc <= T; ++cc) {
+        if (cc < T && !((lowmask >> cc) & 1)) continue;
+        const int64_t nb = cc < T ? s.nbk : kblk + 1;
+        const uint32_t* bc = s.bcnt + (int64_t)cc * s.nbk;
+        for (int64_t k0 = 0; k0 < nb; k0 += (int64_t)blockDim.x * 16) {
+          uint32_t x[16];                       // 16 independent loads per thread in flight
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            const int64_t k = k0 + r * blockDim.x + threadIdx.x;
+            x[r] = k < nb ? __ldcg(&bc[k]) : 0u;
+          }
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            const int64_t k = k0 + r * blockDim.x + threadIdx.x;
+            if (x[r]) b.cand[atomicAdd(&s_nt, 1)] = (int32_t)(((int64_t)cc << 27) | k);
+          }
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) ctl->ntask = s_nt;
+    } else if (threadIdx.x == 0) {
+      ctl->ntask = 0;
+    }
+    if (threadIdx.x == 0) { ctl->ext_next = 0; ctl->ext_done = 0; ctl->find_next = 0; }
+    TL_MAX(23);
+  }
+  __syncthreads();
   const int gw = blockIdx.x * UPD_WARPS + wid;
   const int nw = gridDim.x * UPD_WARPS;
   const int D4 = s.D >> 2;
   float4* mystg = dyn + (size_t)wid * (stage_rows + 1) * D4;
   uint32_t phase = 0;
   const float4* G4 = reinterpret_cast<const float4*>(G);
-  // ---- phase 1a: ordered segment reduce + SGD + pending + clock, warp per unique key
-  for (int u = gw; u < U; u += nw) segreduce_key(s, c, G4, lr, u, lane, mystg, &bars[wid], phase, stage_rows);
-  // ---- phase 1b (LFU bitmap path): extract the victim keys -- every key of the
-  // counts < T in lowmask and the keys <= K* of count T -- into b.vsel, one
-  // 4096-key bitmap block per warp task, one atomic per warp
+  // ---- phase 1: ordered segment reduce + SGD + pending + clock, warp per unique key
+  // block 0 plans; the other blocks' warps take the unique keys
+  const int rw = gw - UPD_WARPS, nrw = nw - UPD_WARPS;
+  if (rw >= 0)
+    for (int u = rw; u < U; u += nrw) segreduce_key(s, c, G4, lr, u, lane, mystg, &bars[wid], phase, stage_rows);
+  TL_MAX(18);
+  // ---- every update done and block 0's plan + task list visible
+  grid.sync();
+  const int emode = abort ? 0 : __ldcg(&ctl->emode);
+  const bool rebuild = __ldcg(&ctl->rebuild_req);
   if (emode == 1) {
-    const int64_t kblk = Kstar >> LFU_BLK_SHIFT;
-    int64_t ntask = 0;
-    for (uint32_t cc = 0; cc < T; ++cc) ntask += ((lowmask >> cc) & 1) ? s.nbk : 0;
-    ntask += kblk + 1;
-    for (int64_t task = gw; task < ntask; task += nw) {
-      int64_t tsk = task;
-      uint32_t cc = 0;
-      for (; cc < T; ++cc) {
-        if (!((lowmask >> cc) & 1)) continue;
-        if (tsk < s.nbk) break;
-        tsk -= s.nbk;
-      }
-      const int64_t blk = tsk;
-      if (__ldcg(&s.bcnt[(int64_t)cc * s.nbk + blk]) == 0) continue;
+    // extraction of the victim keys, one listed bitmap block per warp
+    const uint32_t T = __ldcg(&ctl->T);
+    const int64_t Kstar = __ldcg(&ctl->Kstar);
+    const int ntask = __ldcg(&ctl->ntask);
+    for (int task = gw; task < ntask; task += nw) {
+      const int32_t code = __ldcg(&b.cand[task]);
+      const uint32_t cc = (uint32_t)code >> 27;
+      const int64_t blk = code & ((1 << 27) - 1);
       const uint32_t* bm = s.bm + (int64_t)cc * s.bm_words;
       uint32_t w[4];
       int cl = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + q;
+      for (int r = 0; r < 4; ++r) {
+        const int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r;
         uint32_t bits = wi < s.bm_words ? __ldcg(&bm[wi]) : 0u;
         if (cc == T) {   // keep keys <= K*
           const int64_t k0 = wi << 5;
           if (k0 > Kstar) bits = 0;
-          else if (k0 + 31 > Kstar) bits &= (Kstar - k0 == 31) ? 0xffffffffu : ((1u << (Kstar - k0 + 1)) - 1u);
+          else if (k0 + 31 > Kstar) bits &= (1u << (Kstar - k0 + 1)) - 1u;
         }
-        w[q] = bits;
+        w[r] = bits;
         cl += __popc(bits);
       }
       int incl = cl;
@@ -556,15 +663,15 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
         if (lane >= o) incl += y;
       }
       const int total = __shfl_sync(0xffffffffu, incl, 31);
-      if (total == 0) continue;
+      if (!total) continue;
       int base = 0;
       if (lane == 31) base = atomicAdd(&ctl->nsel, total);
       base = __shfl_sync(0xffffffffu, base, 31);
       int pos = base + incl - cl;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t bits = w[q];
-        const int64_t kb = ((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + q) << 5;
+      for (int r = 0; r < 4; ++r) {
+        uint32_t bits = w[r];
+        const int64_t kb = ((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r) << 5;
         while (bits) {
           b.vsel[pos++] = kb + (__ffs(bits) - 1);
           bits &= bits - 1;
@@ -572,12 +679,14 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
       }
     }
   }
-  // ---- phase 2 (LFU bitmap path): every update is done; evict, warp per victim
+  TL_MAX(19);
+  // ---- phase 2 (LFU bitmap path): every update done; evict, warp per victim
   if (emode == 1) {
     grid.sync();
+    TL_MAX(20);
     const int nsel = ctl->nsel;
     for (int i = gw; i < nsel; i += nw) {
-      const int64_t key = b.vsel[i];
+      const int64_t key = __ldcg(&b.vsel[i]);
       uint64_t slot = 0;
       const int32_t e = warp_find_slot(s, key, lane, &slot);
       if (e >= 0) evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev);
@@ -585,7 +694,6 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   }
   // ---- generic selection (LRU, LFU fallback, evict-all) after all updates
   if (emode == 2) {
-    grid.sync();
     generic_select(s, b, reinterpret_cast<uint64_t*>(dyn), h, grid);
     grid.sync();
     const int nv = ctl->nvict;
@@ -601,6 +709,7 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
       evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev);
     }
   }
+  TL_MAX(21);
   __syncthreads();
   dpop_flush(s, dpop);
   if (threadIdx.x == 0) {

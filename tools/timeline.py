@@ -1,0 +1,51 @@
+"""Fused kernels' timeline from per-warp %globaltimer marks (build with HET_TIMELINE=1)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+from paper_2112_07221_b200 import het  # noqa: E402
+from workload import gen  # noqa: E402
+
+TLW = 8192
+B, D = 128, 128
+n = B * 26
+cards = gen.scaled_cards(int(os.environ["TL_ROWS"])) if os.environ.get("TL_ROWS") else gen.cards_for("criteo")
+dev = torch.device("cuda", 0)
+c = het.HetCache(sum(cards), D, 0.1, 100, het.HET_LFU, max_keys_per_call=n)
+lib = het.load()
+lib.het_debug_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+buf = np.zeros(24 * TLW, np.uint64)
+g = gen.grads(0, 0, n, D, device=dev)
+t = 0
+while t < 6500:
+    keys = gen.criteo_keys(0, t, 500, B, cards, device=dev)
+    for j in range(500):
+        c.lookup(keys[j], het.HET_CLOCK_AUTO); c.update(keys[j], g, 0.01); t += 1
+keys = gen.criteo_keys(0, t, 20, B, cards, device=dev)
+out = torch.empty((n, D), device=dev)
+names = {0: "dd.start", 2: "dd.work", 3: "dd.tail0", 5: "dd.loaded", 6: "dd.scanned", 4: "dd.tail1",
+         22: "plan.start", 7: "plan.pop", 23: "plan.end", 8: "lk.start", 13: "lk.find", 14: "lk.install",
+         15: "lk.vread", 10: "lk.work", 11: "lk.tail0", 12: "lk.tail1", 16: "up.start", 18: "up.seg", 19: "up.finds",
+         20: "up.sync", 21: "up.evict"}
+for j in range(20):
+    torch.cuda.synchronize()
+    lib.het_debug_timeline(None, 24, TLW)
+    c.lookup(keys[j], het.HET_CLOCK_AUTO, out=out); c.update(keys[j], g, 0.01)
+    torch.cuda.synchronize()
+    lib.het_debug_timeline(buf.ctypes.data, 24, TLW)
+    if j < 17:
+        continue
+    v = buf.reshape(24, TLW).astype(np.float64)
+    t0 = v[0][v[0] > 0].min()
+    parts = []
+    for m in sorted(names):
+        x = v[m][v[m] > 0]
+        if x.size:
+            x = (x - t0) / 1000.0
+            parts.append(f"{names[m]} p50 {np.median(x):.1f} max {x.max():.1f}")
+    print(" | ".join(parts))
