@@ -14,6 +14,7 @@
 #include "../../include/het.h"
 #include "het_internal.cuh"
 #include "het_mgpu.h"
+#include "het_p2p.h"
 
 namespace het {
 void dedup_set_attrs();
@@ -402,14 +403,19 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
   c.t = clock_t;
   c.keys = keys;
   Dev& d = h->d;
-  h->fused = fused_ok(d, (int)n) && !getenv("HET_NO_FUSED");
+  h->fused = fused_ok(d, (int)n) && !getenv("HET_NO_FUSED") && (d.world == 1 || mgpu_p2p(h->mg));
   if (h->fused) {
     {
       Prof p(h, "dedup", st);
       h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st);
     }
-    Prof p(h, "lookup_fused", st);
-    h->launches += launch_lookup_fused(d, c, dout, st);
+    if (d.world == 1) {
+      Prof p(h, "lookup_fused", st);
+      h->launches += launch_lookup_fused(d, c, dout, st);
+    } else {
+      Prof p(h, "exchange_fused", st);
+      h->launches += p2p_round_fused(mgpu_p2p(h->mg), d, c, dout, st);
+    }
   } else {
     launch_begin(d, clock_t, (int)n, st);
     h->launches += 1;
@@ -485,7 +491,8 @@ het_status_t het_update(het_cache_t h, const int64_t* keys, uint32_t n, const fl
   Dev& d = h->d;
   if (h->fused) {
     Prof p(h, "update_fused", st);
-    h->launches += launch_update_fused(d, h->call, grads, lr, h->evbuf_host, st);
+    h->launches += launch_update_fused(d, h->call, grads, lr, h->evbuf_host, st,
+                                       d.world > 1 ? (const void*)p2p_view_ptr(mgpu_p2p(h->mg)) : nullptr);
     h->overflow_bound = 0;
   } else {
     {

@@ -97,6 +97,8 @@ static int bits_for(uint64_t x) {
   return b;
 }
 
+P2PState* mgpu_p2p(MgpuState* mg) { return mg ? mg->p2p : nullptr; }
+
 uint64_t mgpu_take_launches(MgpuState* mg) {
   uint64_t l = mg ? mg->launches : 0;
   if (mg) mg->launches = 0;

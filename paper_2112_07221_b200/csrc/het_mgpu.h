@@ -9,6 +9,8 @@
 namespace het {
 
 struct MgpuState;
+struct P2PState;
+P2PState* mgpu_p2p(MgpuState* mg);   // device-initiated exchange state, nullptr if NCCL v1
 
 het_status_t mgpu_create(MgpuState*& mg, const Dev& d, uint32_t n_max, const void* uid, cudaStream_t st);
 void mgpu_destroy(MgpuState* mg);

@@ -35,108 +35,9 @@
 
 #include "het_internal.cuh"
 #include "het_p2p.h"
+#include "p2p_dev.cuh"
 
 namespace het {
-
-enum : uint32_t { K_PUSH = 0, K_NEEDQ = 1, K_EXP1 = 2, K_MISS = 3, K_DIRTY = 4 };
-constexpr unsigned long long WAIT_NS = 20ull * 1000 * 1000 * 1000;  // 20 s
-
-struct alignas(16) Flag {
-  unsigned long long epoch;
-  uint32_t total;
-  uint32_t pushes;
-};
-struct alignas(16) Rec {
-  int64_t key;
-  uint32_t cc;
-  uint32_t kind;
-};
-
-// POD view passed to kernels
-struct P2P {
-  int N, rank;
-  int64_t CAPS, REC;
-  uint32_t D;
-  char* const* peer;            // [N] base of every rank's inbox (own included)
-  size_t off_reqflag, off_respflag, off_req, off_rows, off_resp;
-  int32_t* lcnt;                // [N] this round's requests per owner
-  int32_t* c3cnt;               // [N] pending eviction pushes per owner
-  int32_t* ridx;                // [N][CAPS] unique index of each request
-  int32_t* head;                // [rows_local] list head per local row (-1)
-  int32_t* next;                // [N*CAPS]
-  int32_t* leaders;             // [N*CAPS]
-  int32_t* nlead;
-  int32_t* done;                // [4] last-block counters
-  unsigned long long* epoch;    // completed rounds
-  int32_t* qtot;                // [N] received totals (owner, this round)
-  int32_t* qpush;               // [N] received pushes (owner, this round)
-};
-
-__device__ __forceinline__ Flag* reqflag(const P2P& m, int r) { return (Flag*)(m.peer[r] + m.off_reqflag); }
-__device__ __forceinline__ Flag* respflag(const P2P& m, int r) { return (Flag*)(m.peer[r] + m.off_respflag); }
-__device__ __forceinline__ Rec* reqrec(const P2P& m, int r, int src) {
-  return (Rec*)(m.peer[r] + m.off_req) + (int64_t)src * m.CAPS;
-}
-__device__ __forceinline__ float* reqrow(const P2P& m, int r, int src, int64_t j) {
-  return (float*)(m.peer[r] + m.off_rows) + ((int64_t)src * m.CAPS + j) * m.D;
-}
-__device__ __forceinline__ float* resprec(const P2P& m, int r, int owner, int64_t j) {
-  return (float*)(m.peer[r] + m.off_resp) + ((int64_t)owner * m.CAPS + j) * m.REC;
-}
-
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// wait until flags[0..N) carry `epoch`; false on timeout (sticky error raised)
-__device__ bool wait_flags(Flag* flags, int N, unsigned long long epoch, Ctl* ctl) {
-  unsigned long long t0 = gtime();
-  for (int r = 0; r < N; ++r) {
-    while (ld_acquire(&flags[r].epoch) < epoch) {
-      if (gtime() - t0 > WAIT_NS) {
-        raise_err(ctl, 7 /*HET_ERR_NCCL: peer exchange timeout*/);
-        return false;
-      }
-      __nanosleep(64);
-    }
-  }
-  return true;
-}
-
-__device__ __forceinline__ float4 f4add_p(float4 a, float4 b) {
-  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
-}
-
-// block-aggregated wire-byte counters (clock tx/rx, embedding tx/rx)
-struct Bytes {
-  unsigned long long v[4];
-};
-__device__ __forceinline__ void bytes_init(unsigned long long* b) {
-  if (threadIdx.x < 4) b[threadIdx.x] = 0;
-}
-__device__ __forceinline__ void bytes_flush(const Dev& s, unsigned long long* b) {
-  if (threadIdx.x < 4 && b[threadIdx.x]) atomicAdd(&s.cnt[C_BCLK_TX + threadIdx.x], b[threadIdx.x]);
-}
-
-__device__ __forceinline__ bool last_block(int32_t* counter) {
-  __shared__ int s_last;
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (s_last) __threadfence_system();
-  return s_last;
-}
 
 // ---------------------------------------------------------------- requester: build + publish
 __global__ void k_p2p_build(Dev s, Call c, P2P m, int drain) {
@@ -464,6 +365,200 @@ __global__ void k_p2p_pushes(Dev s, P2P m, EvView b) {
   }
 }
 
+// ---------------------------------------------------------------- fused round (n <= 8192)
+// probe + request build + publish in one kernel: warp per unique key does
+// Cache.Find, condition (1), the LFU/LRU touch, writes its positions' inverse
+// and, unless it is a valid hit, its request record (+ pending row) straight
+// into the owner's inbox; the last block publishes the round's flags.
+__global__ void __launch_bounds__(256)
+k_probe_build(Dev s, Call c, P2P m) {
+  __shared__ unsigned bc[4];
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ unsigned long long sb[4];
+  if (threadIdx.x < 4) bc[threadIdx.x] = 0;
+  dpop_init(dpop);
+  bytes_init(sb);
+  __syncthreads();
+  Ctl* ctl = s.ctl;
+  const int lane = threadIdx.x & 31;
+  const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long ep = *m.epoch + 1;
+  const int U = ctl->abort ? 0 : ctl->U;
+  const int D4 = s.D >> 2;
+  if (u < U) {
+    const int64_t key = c.uniq[u];
+    const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
+    const int cnt = j1 - j0;
+    const int pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
+    uint32_t cntk = 0;
+    if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
+    const int32_t e = warp_find(s, key, lane);
+    uint32_t ecs = 0, ecc = 0;
+    if (e >= 0) { ecs = s.cs[e]; ecc = s.cc[e]; }
+    uint8_t st = ST_MISS;
+    if (lane == 0) {
+      if (s.lfu_persist) { cntk += 1; s.count_by_key[key] = cntk; }
+      if (e >= 0) {
+        if (s.s == S_INF) st = ST_HIT;                       // R4
+        else if (ecc - ecs > s.s) st = ST_EXP1;              // cond (1)
+        else st = ST_NEEDQ;                                  // cond (2) at the owner
+        if (s.policy == 0) {
+          uint32_t oldc = s.eprim[e];
+          uint32_t newc = s.lfu_persist ? cntk : oldc + 1;
+          s.eprim[e] = newc;
+          lfu_move(s, key, oldc, newc, dpop);
+        } else {
+          s.eprim[e] = (uint32_t)ctl->t_cur;
+        }
+      }
+      c.status[u] = st;
+      c.uentry[u] = e;
+      if (st == ST_HIT) atomicAdd(&bc[0], 1u);
+      else if (st == ST_EXP1) atomicAdd(&bc[1], 1u);
+      else if (st == ST_MISS) atomicAdd(&bc[3], 1u);
+    }
+    st = __shfl_sync(0xffffffffu, st, 0);
+    for (int k = lane; k < cnt; k += 32) c.inverse[k < 32 ? pos_lane : c.perm[j0 + k]] = u;
+    if (st != ST_HIT) {
+      const int o = (int)(key % m.N);
+      const bool dirty = e >= 0 && ecc > ecs;
+      int slot = 0;
+      if (lane == 0) slot = atomicAdd(&m.lcnt[o], 1);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      const int64_t j = m.c3cnt[o] + slot;
+      if (lane == 0) {
+        Rec r;
+        r.key = key; r.cc = ecc;
+        r.kind = (st == ST_NEEDQ ? K_NEEDQ : st == ST_EXP1 ? K_EXP1 : K_MISS) | (dirty ? K_DIRTY : 0);
+        reqrec(m, o, m.rank)[j] = r;
+        m.uslot[u] = (int32_t)(o * m.CAPS + slot);
+        atomicAdd(&sb[st == ST_NEEDQ ? 0 : 2], 16ull);
+        if (dirty) atomicAdd(&sb[2], 4ull * s.D);
+      }
+      if (dirty) {
+        const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
+        float4* dst = reinterpret_cast<float4*>(reqrow(m, o, m.rank, j));
+        for (int d = lane; d < D4; d += 32) dst[d] = pr[d];
+      }
+    }
+  }
+  __syncthreads();
+  dpop_flush(s, dpop);
+  bytes_flush(s, sb);
+  if (threadIdx.x == 0) {
+    if (bc[0]) atomicAdd(&s.cnt[C_HITS], (unsigned long long)bc[0]);
+    if (bc[1]) atomicAdd(&s.cnt[C_EXP1], (unsigned long long)bc[1]);
+    if (bc[3]) atomicAdd(&s.cnt[C_MISSES], (unsigned long long)bc[3]);
+    if (blockIdx.x == 0 && !ctl->abort) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+  }
+  if (!last_block(&m.done[0])) return;
+  if (threadIdx.x < m.N) {
+    const int o = threadIdx.x;
+    Flag* f = &reqflag(m, o)[m.rank];
+    f->total = (uint32_t)(m.c3cnt[o] + m.lcnt[o]);
+    f->pushes = (uint32_t)m.c3cnt[o];
+    __threadfence_system();
+    st_release(&f->epoch, ep);
+    m.c3cnt[o] = 0;
+  }
+  if (threadIdx.x == 0) m.done[0] = 0;
+}
+
+// install + gather: wait for the owners' responses, finish the statuses of the
+// clock-checked hits, install fetched rows, scatter every key's row to its
+// occurrences (Cache.Get)
+__global__ void __launch_bounds__(256)
+k_install_gather(Dev s, Call c, P2P m, float* __restrict__ out) {
+  __shared__ int s_ok;
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ unsigned bc[2];
+  __shared__ unsigned long long sb[4];
+  const unsigned long long ep = *m.epoch + 1;
+  dpop_init(dpop);
+  bytes_init(sb);
+  if (threadIdx.x < 2) bc[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_ok = wait_flags(respflag(m, m.rank), m.N, ep, s.ctl);
+  __syncthreads();
+  Ctl* ctl = s.ctl;
+  const int lane = threadIdx.x & 31;
+  const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int U = (s_ok && !ctl->abort) ? ctl->U : 0;
+  const int D4 = s.D >> 2;
+  if (u < U) {
+    uint8_t st = c.status[u];
+    int32_t e = c.uentry[u];
+    const int64_t key = c.uniq[u];
+    const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
+    const int cnt = j1 - j0;
+    const int pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
+    bool ok = true;
+    if (st != ST_HIT) {
+      const int loc = m.uslot[u];
+      const int o = loc / (int)m.CAPS;
+      const float* rec = resprec(m, m.rank, o, loc - o * m.CAPS);
+      const uint32_t g = reinterpret_cast<const uint32_t*>(rec)[0];
+      const bool valid = reinterpret_cast<const uint32_t*>(rec)[1] != 0;
+      if (lane == 0) atomicAdd(&sb[valid ? 1 : 3], valid ? 8ull : 8ull + 4ull * s.D);
+      if (st == ST_NEEDQ) {
+        if (lane == 0) { c.status[u] = valid ? ST_HIT : ST_EXP2; atomicAdd(&bc[valid ? 0 : 1], 1u); }
+      }
+      if (!(st == ST_NEEDQ && valid)) {
+        if (st == ST_MISS) {
+          int32_t idx = 0;
+          if (lane == 0) idx = atomicSub(&ctl->ftop, 1) - 1;
+          idx = __shfl_sync(0xffffffffu, idx, 0);
+          if (idx < 0) {
+            if (lane == 0) raise_err(ctl, 4);
+            ok = false;
+          } else {
+            e = s.fstack[idx];
+            warp_insert(s, key, e, lane);
+            if (lane == 0) {
+              s.ekey[e] = key;
+              const uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
+              s.eprim[e] = prim;
+              if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
+              atomicMin(&ctl->min_install, prim);
+              c.uentry[u] = e;
+            }
+          }
+        }
+        if (ok) {
+          const float4* src = reinterpret_cast<const float4*>(rec + 4);
+          float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
+          for (int d = lane; d < D4; d += 32) vr[d] = src[d];
+          if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
+        }
+      }
+    }
+    if (ok && e >= 0) {
+      const float4* vr = reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D);
+      float4* o4 = reinterpret_cast<float4*>(out);
+      for (int d = lane; d - lane < D4; d += 32) {
+        float4 val = d < D4 ? vr[d] : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int kb = 0; kb < cnt; kb += 32) {
+          const int srcp = kb == 0 ? pos_lane : (kb + lane < cnt ? c.perm[j0 + kb + lane] : 0);
+          const int mm = min(32, cnt - kb);
+          for (int k = 0; k < mm; ++k) {
+            const int pos = __shfl_sync(0xffffffffu, srcp, k);
+            if (d < D4) __stcs(o4 + (int64_t)pos * D4 + d, val);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  dpop_flush(s, dpop);
+  bytes_flush(s, sb);
+  if (threadIdx.x == 0) {
+    if (bc[0]) atomicAdd(&s.cnt[C_HITS], (unsigned long long)bc[0]);
+    if (bc[1]) atomicAdd(&s.cnt[C_EXP2], (unsigned long long)bc[1]);
+  }
+  if (!last_block(&m.done[2])) return;
+  if (threadIdx.x == 0) { *m.epoch = ep; m.done[2] = 0; }
+}
+
+
 // ---------------------------------------------------------------- host side
 struct P2PState {
   P2P v{};
@@ -528,7 +623,7 @@ het_status_t p2p_create(P2PState*& out, const Dev& d, uint32_t n_max, ncclComm_t
   bool ok = p_alloc(p, &v.lcnt, N) && p_alloc(p, &v.c3cnt, N) && p_alloc(p, &v.ridx, NC) &&
             p_alloc(p, &v.head, d.rows_local) && p_alloc(p, &v.next, NC) && p_alloc(p, &v.leaders, NC) &&
             p_alloc(p, &v.nlead, 1) && p_alloc(p, &v.done, 4) && p_alloc(p, &v.epoch, 1) &&
-            p_alloc(p, &v.qtot, N) && p_alloc(p, &v.qpush, N);
+            p_alloc(p, &v.qtot, N) && p_alloc(p, &v.qpush, N) && p_alloc(p, &v.uslot, n_max);
   if (!ok) return HET_ERR_OOM;
   cudaMemsetAsync(v.lcnt, 0, 4 * N, st);
   cudaMemsetAsync(v.c3cnt, 0, 4 * N, st);
@@ -563,6 +658,20 @@ int p2p_round(P2PState* p, const Dev& d, const Call& c, int drain, cudaStream_t 
   k_p2p_install<<<148 * 2, 256, 0, st>>>(d, c, v);
   return 4;
 }
+
+// fused round: probe+build, owner link, owner process, install+gather
+int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaStream_t st) {
+  P2P& v = p->v;
+  cudaMemsetAsync(v.lcnt, 0, 4 * v.N, st);
+  const int blocks = std::max(1, (c.n + 7) / 8);
+  k_probe_build<<<blocks, 256, 0, st>>>(d, c, v);
+  k_p2p_link<<<148, 256, 0, st>>>(d, v);
+  k_p2p_process<<<148 * 2, 256, 0, st>>>(d, v);
+  k_install_gather<<<blocks, 256, 0, st>>>(d, c, v, out);
+  return 4;
+}
+
+P2P* p2p_view_ptr(P2PState* p) { return &p->v; }
 
 int p2p_pushes(P2PState* p, const Dev& d, void* evbuf, cudaStream_t st) {
   EvView b = *reinterpret_cast<EvView*>(evbuf);

@@ -14,6 +14,11 @@ het_status_t p2p_create(P2PState*& out, const Dev& d, uint32_t n_max, ncclComm_t
 void p2p_destroy(P2PState* p);
 // one lookup round after the probe: build + publish, owner link + process, install
 int p2p_round(P2PState* p, const Dev& d, const Call& c, int drain, cudaStream_t st);
+// fused round (n <= 8192, after k_dd_fused): probe+build, link, process, install+gather
+int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaStream_t st);
+// device view of the exchange state (for the fused update's eviction pushes)
+struct P2P;
+P2P* p2p_view_ptr(P2PState* p);
 // eviction pushes of the current update (sent with the next round)
 int p2p_pushes(P2PState* p, const Dev& d, void* evbuf, cudaStream_t st);
 

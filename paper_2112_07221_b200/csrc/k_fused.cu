@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 
 #include "evict_dev.cuh"
+#include "p2p_dev.cuh"
 
 namespace het {
 
@@ -438,19 +439,25 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
 
 // ------------------------------------------------------------------ K_upd
 // Evict push of one resident entry at N = 1 (warp-cooperative) + delete + free
+// push != nullptr (N > 1): the Evict push goes to the owner's inbox, carried
+// by the next exchange round; otherwise the local server applies it now
 __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_t e, int64_t key, uint64_t slot,
-                                            int lane, int* dpop, unsigned* s_dirty, unsigned* s_ev) {
+                                            int lane, int* dpop, unsigned* s_dirty, unsigned* s_ev,
+                                            const P2P* push = nullptr) {
   Ctl* ctl = s.ctl;
   const uint32_t ecs = s.cs[e], ecc = s.cc[e], prim = s.eprim[e];
   const bool dirty = ecc > ecs;
   const int D4 = s.D >> 2;
-  if (dirty) {
+  if (dirty && push) {
+    push_record(s, *push, e, key, ecc, lane);
+  } else if (dirty) {
     float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
     const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
     for (int d = lane; d < D4; d += 32) Wr[d] = f4add_(Wr[d], pr[d]);
   }
   if (lane == 0) {
-    if (dirty) { uint32_t g = s.cg[key]; s.cg[key] = g > ecc ? g : ecc; }
+    if (push && dirty) atomicAdd(&s.cnt[C_BEMB_TX], 16ull + 4ull * s.D);
+    if (dirty && !push) { uint32_t g = s.cg[key]; s.cg[key] = g > ecc ? g : ecc; }
     s.hkey[slot] = HK_TOMB;
     atomicAdd(&ctl->n_tomb, 1);
     int vi = atomicAdd(&ctl->nvict, 1);
@@ -542,7 +549,8 @@ __device__ __forceinline__ void segreduce_key(const Dev& s, const Call& c, const
 }
 
 __global__ void __launch_bounds__(UPD_THREADS)
-k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, int stage_rows) {
+k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, int stage_rows, P2P pm, int push) {
+  const P2P* pp = push ? &pm : nullptr;
   extern __shared__ float4 dyn[];
   __shared__ uint32_t h[NBIN];
   __shared__ uint64_t bars[UPD_WARPS];
@@ -689,7 +697,7 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
       const int64_t key = __ldcg(&b.vsel[i]);
       uint64_t slot = 0;
       const int32_t e = warp_find_slot(s, key, lane, &slot);
-      if (e >= 0) evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev);
+      if (e >= 0) evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev, pp);
     }
   }
   // ---- generic selection (LRU, LFU fallback, evict-all) after all updates
@@ -706,7 +714,7 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
       const int64_t key = s.ekey[e0];
       uint64_t slot = 0;
       int32_t e = warp_find_slot(s, key, lane, &slot);
-      evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev);
+      evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev, pp);
     }
   }
   TL_MAX(21);
@@ -741,7 +749,7 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
 // ------------------------------------------------------------------ launchers
 constexpr int FUSED_MAX = 8192;
 
-bool fused_ok(const Dev& s, int n) { return s.world == 1 && n <= FUSED_MAX; }
+bool fused_ok(const Dev& s, int n) { return n <= FUSED_MAX; }
 
 int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st) {
   static bool attr = false;
@@ -760,7 +768,8 @@ int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st
   return 1;
 }
 
-int launch_update_fused(const Dev& s, const Call& c, const float* grads, float lr, void* evbuf, cudaStream_t st) {
+int launch_update_fused(const Dev& s, const Call& c, const float* grads, float lr, void* evbuf, cudaStream_t st,
+                        const void* p2pview) {
   static int coop_blocks = 0;
   static size_t smem = 0;
   static int stage_rows = 0;
@@ -783,7 +792,10 @@ int launch_update_fused(const Dev& s, const Call& c, const float* grads, float l
   Dev sd = s;
   Call cd = c;
   int sr = stage_rows;
-  void* args[] = {(void*)&sd, (void*)&cd, (void*)&grads, (void*)&lr, (void*)&b, (void*)&sr};
+  P2P pm{};
+  int push = 0;
+  if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
+  void* args[] = {(void*)&sd, (void*)&cd, (void*)&grads, (void*)&lr, (void*)&b, (void*)&sr, (void*)&pm, (void*)&push};
   cudaLaunchCooperativeKernel((void*)k_update_fused, dim3(coop_blocks), dim3(UPD_THREADS), args, smem, st);
   return 1;
 }

@@ -336,3 +336,48 @@ def _tracked_mask(keys, track):
         x ^= x >> 31
         out[i] = x % track == 0
     return out
+
+
+def test_reddit_shaped_all_unique():
+    """BASELINE configs[2] shape (GraphSAGE on Reddit): 232,965 node ids,
+    14,208 distinct ids per worker-iteration (dedup on already-unique keys,
+    P:687), D=128, cache 10 %, s=10 -- one worker."""
+    R, D, K = gen.REDDIT_ROWS, 128, 14208
+    p = Pair(R, D, 0.1, 10, LFU, n_max=K, track_div=64)
+    p.g_policy = LFU
+    for t in range(12):
+        keys = gen.reddit_keys(0, t, K).numpy()
+        grads = gen.grads(0, t, K, D).numpy()
+        kd = torch.from_numpy(keys).cuda()
+        out = p.g.lookup(kd, t).cpu().numpy()
+        oo = p.o.lookup(t, [keys])[0]
+        sel = _tracked_mask(keys, 64)
+        assert_rows(out[sel], oo[sel])
+        gl, ol = p.g.lookup_log(), p.o.lookup_log(0)
+        assert np.array_equal(gl["unique"], ol["unique"]) and np.array_equal(gl["status"], ol["status"])
+        p.g.update(kd, torch.from_numpy(grads).cuda(), LR)
+        p.o.update([grads], LR)
+        gk, _ = p.g.victims()
+        assert np.array_equal(gk, np.sort(p.o.victims(0)[0]))
+    p.compare_stats()
+
+
+def test_scale_shaped_wide_rows():
+    """BASELINE configs[4] row shape (D=4096, 16 KB rows: the column loops,
+    no TMA staging) on a scaled table: Criteo-shaped keys over 20,000 rows."""
+    R, D = 20000, 4096
+    cards = gen.scaled_cards(R)
+    p = Pair(R, D, 0.1, 100, LFU, n_max=4096, track_div=16)
+    p.g_policy = LFU
+    for t in range(8):
+        keys = gen.criteo_keys(0, t, 1, 32, cards)[0].numpy()
+        grads = gen.grads(0, t, keys.size, D).numpy()
+        kd = torch.from_numpy(keys).cuda()
+        out = p.g.lookup(kd, t).cpu().numpy()
+        oo = p.o.lookup(t, [keys])[0]
+        sel = _tracked_mask(keys, 16)
+        assert_rows(out[sel], oo[sel])
+        assert np.array_equal(p.g.lookup_log()["status"], p.o.lookup_log(0)["status"])
+        p.g.update(kd, torch.from_numpy(grads).cuda(), LR)
+        p.o.update([grads], LR)
+    p.compare_stats()
