@@ -193,10 +193,11 @@ def run_gpu(args):
     st = torch.cuda.current_stream()
 
     side = torch.cuda.Stream() if world > 1 else None
+    use_dense = world > 1 and not os.environ.get("HET_BENCH_NO_DENSE")   # diagnostic switch
 
     def step(j):
         # dense all-reduce overlapped on a side stream (N > 1)
-        cache.step(keys_all[j], grads_all[j], out_buf, lr, dense if world > 1 else None, side)
+        cache.step(keys_all[j], grads_all[j], out_buf, lr, dense if use_dense else None, side)
 
     out_buf = torch.empty((n, D), dtype=torch.float32, device=device)
     # static input buffers of the captured step (the data loader / dense
@@ -220,7 +221,7 @@ def run_gpu(args):
         kbuf.copy_(keys_all[0]); gbuf.copy_(grads_all[0])
         step(0)
         l0 = cache.stats()["launches"]
-        graph = cache.capture_step(kbuf, gbuf, out_buf, lr, dense if world > 1 else None)
+        graph = cache.capture_step(kbuf, gbuf, out_buf, lr, dense if use_dense else None)
         graph_launches = cache.stats()["launches"] - l0
         for j in range(3):
             kbuf.copy_(keys_all[j]); gbuf.copy_(grads_all[j]); graph.replay()
@@ -304,7 +305,7 @@ def run_gpu(args):
         te0.record(st)
         het.het_lookup(cache.h, keys_h[W + j], n, AUTO, out_h)
         het.het_update(cache.h, keys_h[W + j], n, grads_h[W + j], lr)
-        if world > 1:
+        if use_dense:
             side.wait_stream(st)
             with torch.cuda.stream(side):
                 het.het_dense_allreduce(cache.h, dense, dense.numel(), stream=side)
@@ -322,7 +323,7 @@ def run_gpu(args):
         "config": {"workload": "WDL" if world == 1 else "DCN", "rows": R, "D": D, "batch_per_gpu": B,
                    "fields": F, "cache_frac": CFG["cache_frac"], "cache_entries_per_gpu": C,
                    "s": CFG["s"], "policy": CFG["policy"], "zipf_alpha": CFG["alpha"],
-                   "dense_params": CFG["dense_params"] if world > 1 else 0,
+                   "dense_params": CFG["dense_params"] if use_dense else 0,
                    "parallelism": f"hash-sharded table x{world}, dp{world}",
                    "l2": "flushed between timed steps (256 MB write outside the step events)",
                    "fill_steps": fill_steps, "fill_s": round(fill_s, 1)},

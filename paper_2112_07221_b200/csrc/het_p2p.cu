@@ -39,6 +39,23 @@
 
 namespace het {
 
+#ifdef HET_TIMELINE
+constexpr int PTLW = 8192;
+__device__ unsigned long long g_ptl[16 * PTLW];
+#define PTL(i) do { if ((threadIdx.x & 31) == 0) { int w_ = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; \
+  if (w_ < PTLW) { unsigned long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); g_ptl[(i) * PTLW + w_] = t_; } } } while (0)
+extern "C" int het_debug_timeline_p2p(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  if (out) cudaMemcpyFromSymbol(out, g_ptl, sizeof(g_ptl));
+  static unsigned long long* zero = nullptr;
+  if (!zero) zero = (unsigned long long*)calloc(16 * PTLW, 8);
+  cudaMemcpyToSymbol(g_ptl, zero, sizeof(g_ptl));
+  return 0;
+}
+#else
+#define PTL(i) do {} while (0)
+#endif
+
 // ---------------------------------------------------------------- requester: build + publish
 __global__ void k_p2p_build(Dev s, Call c, P2P m, int drain) {
   __shared__ unsigned long long sb[4];
@@ -100,8 +117,10 @@ __global__ void k_p2p_link(Dev s, P2P m) {
   __shared__ int32_t tot[64];
   const unsigned long long ep = *m.epoch + 1;
   Flag* flags = reqflag(m, m.rank);
+  PTL(3);
   if (threadIdx.x == 0) s_ok = wait_flags(flags, m.N, ep, s.ctl);
   __syncthreads();
+  PTL(4);
   if (!s_ok) return;
   if (threadIdx.x < m.N) {
     tot[threadIdx.x] = (int32_t)flags[threadIdx.x].total;
@@ -119,12 +138,14 @@ __global__ void k_p2p_link(Dev s, P2P m) {
       if (old < 0) m.leaders[atomicAdd(m.nlead, 1)] = id;
     }
   }
+  PTL(5);
 }
 
 // ---------------------------------------------------------------- owner: apply + respond
 __global__ void k_p2p_process(Dev s, P2P m) {
   __shared__ unsigned long long sb[4];
   bytes_init(sb);
+  PTL(6);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -213,6 +234,7 @@ __global__ void k_p2p_process(Dev s, P2P m) {
       }
     }
   }
+  PTL(7);
   __syncthreads();
   bytes_flush(s, sb);
   if (!last_block(&m.done[1])) return;
@@ -221,6 +243,7 @@ __global__ void k_p2p_process(Dev s, P2P m) {
     st_release(&respflag(m, threadIdx.x)[m.rank].epoch, ep);
   }
   if (threadIdx.x == 0) { *m.nlead = 0; m.done[1] = 0; }
+  PTL(8);
 }
 
 // ---------------------------------------------------------------- requester: wait + install
@@ -375,6 +398,7 @@ k_probe_build(Dev s, Call c, P2P m) {
   __shared__ unsigned bc[4];
   __shared__ int dpop[LFU_CB_MAX];
   __shared__ unsigned long long sb[4];
+  PTL(0);
   if (threadIdx.x < 4) bc[threadIdx.x] = 0;
   dpop_init(dpop);
   bytes_init(sb);
@@ -451,6 +475,7 @@ k_probe_build(Dev s, Call c, P2P m) {
     if (bc[3]) atomicAdd(&s.cnt[C_MISSES], (unsigned long long)bc[3]);
     if (blockIdx.x == 0 && !ctl->abort) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
   }
+  PTL(1);
   if (!last_block(&m.done[0])) return;
   if (threadIdx.x < m.N) {
     const int o = threadIdx.x;
@@ -462,6 +487,7 @@ k_probe_build(Dev s, Call c, P2P m) {
     m.c3cnt[o] = 0;
   }
   if (threadIdx.x == 0) m.done[0] = 0;
+  PTL(2);
 }
 
 // install + gather: wait for the owners' responses, finish the statuses of the
@@ -477,8 +503,10 @@ k_install_gather(Dev s, Call c, P2P m, float* __restrict__ out) {
   dpop_init(dpop);
   bytes_init(sb);
   if (threadIdx.x < 2) bc[threadIdx.x] = 0;
+  PTL(9);
   if (threadIdx.x == 0) s_ok = wait_flags(respflag(m, m.rank), m.N, ep, s.ctl);
   __syncthreads();
+  PTL(10);
   Ctl* ctl = s.ctl;
   const int lane = threadIdx.x & 31;
   const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;

@@ -95,9 +95,14 @@ __device__ __forceinline__ void bytes_flush(const Dev& s, unsigned long long* b)
   if (threadIdx.x < 4 && b[threadIdx.x]) atomicAdd(&s.cnt[C_BCLK_TX + threadIdx.x], b[threadIdx.x]);
 }
 
+// Last-block election.  Each block orders its writes with a GPU-scope fence
+// before the counter; the elected block then issues the system-scope fence
+// and the release store of the flag (causality is transitive: block writes
+// -> fence.gpu -> counter -> elected block -> fence.sys -> st.release.sys),
+// so only the publishing thread pays for system scope.
 __device__ __forceinline__ bool last_block(int32_t* counter) {
   __shared__ int s_last;
-  __threadfence_system();
+  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
   __syncthreads();
