@@ -48,6 +48,20 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(phase, world):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    phase's kernel from the committed `ncu --set full` capture of this workload
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), else None.
+    Cold-cache, replayed launches: compare with `achieved`'s algorithmic bytes."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        ent = t["n%d" % world][phase]
+        return float(ent["dram_bytes"])
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------------------- clocks
 class Clocks:
     def __init__(self, gpu):
@@ -136,6 +150,12 @@ def algorithmic_bytes(kernel, s, D, n_steps, resident):
         return e * (8 + 12 + 16) + ed * (3 * row + 8)
     if kernel == "evict":
         return 4 * ((R_WDL + 4095) // 4096) + 16 * e + e * (8 + 12 + 16) + ed * (3 * row + 8)
+    # fused kernels = the sum of the phases they fuse
+    if kernel in ("lookup_fused", "exchange_fused"):
+        # exchange_fused: the local HBM side of the round (records over NVLink not counted)
+        return sum(algorithmic_bytes(k, s, D, n_steps, resident) for k in ("probe", "sync_fetch", "gather"))
+    if kernel == "update_fused":
+        return sum(algorithmic_bytes(k, s, D, n_steps, resident) for k in ("segreduce_apply", "evict"))
     return None
 
 
@@ -288,7 +308,7 @@ def run_gpu(args):
     if dom:
         a = kern[dom]["achieved_gbs"]
         roof = {"bound": "hbm", "kernel": dom, "achieved": a, "peak": hbm, "unit": "GB/s",
-                "frac": (a / hbm) if a else None, "traffic": None, "peak_source": peak_kind}
+                "frac": (a / hbm) if a else None, "traffic": ncu_traffic(dom, world), "peak_source": peak_kind}
 
     # ---- e2e: same steps through the C-ABI with host (pinned) buffers
     keys_h = keys_all[:W + K].cpu().pin_memory()

@@ -57,6 +57,9 @@ struct het_cache {
   uint64_t lookups = 0, keys = 0, updates = 0, launches = 0;
   // multi-GPU
   MgpuState* mg = nullptr;
+  // segment reduce of large batches: heavy keys on a forked stream
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // profiling
   bool prof = false;
   std::vector<ProfRec> prof_pending;
@@ -278,6 +281,14 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   while (S < 4 * d.Ecap) { S <<= 1; d.hbits++; }
   d.hmask = (uint64_t)S - 1;
 
+  int prio_lo = 0, prio_hi = 0;   // heavy-key work on the side stream is scheduled first
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    het_cache_destroy(h);
+    return HET_ERR_CUDA;
+  }
   het_status_t rc = HET_OK;
 #define A(ptr, cnt)                                              \
   if (dalloc(h, &(ptr), (cnt)) != cudaSuccess) { rc = HET_ERR_OOM; goto oom; }
@@ -323,6 +334,9 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
     A(c.sortbuf0, nm);
     A(c.sortbuf1, nm);
     A(c.blockbuf, nm / 1024 + 2);
+    A(c.hlist, nm);
+    A(c.hbuf, (size_t)nm * ((D + 15) / 16) * 16);
+    c.hcap = (int)nm;
     uint32_t *hist, *khist;
     int32_t *cand, *sub, *flags;
     A(hist, 2048);
@@ -497,8 +511,7 @@ het_status_t het_update(het_cache_t h, const int64_t* keys, uint32_t n, const fl
   } else {
     {
       Prof p(h, "segreduce_apply", st);
-      launch_segreduce_apply(d, h->call, grads, lr, (int)n, st);
-      h->launches += 1;
+      h->launches += launch_segreduce_apply(d, h->call, grads, lr, (int)n, st, h->side, h->ev_fork, h->ev_join);
     }
     het_status_t rc = evict_overflow(h, st);
     if (rc) return fail(h, rc, "evict failed");
@@ -782,6 +795,9 @@ het_status_t het_cache_destroy(het_cache_t h) {
   if (!h) return HET_ERR_ARG;
   cudaDeviceSynchronize();
   if (h->mg) mgpu_destroy(h->mg);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   for (void* q : h->allocs) cudaFree(q);
   for (ProfRec& r : h->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);

@@ -78,6 +78,8 @@ struct Ctl {
   int32_t nreq;         // sync/fetch requests built this call
   int32_t npush;        // eviction pushes built this call
   int32_t pad2_;
+  // segment reduce (large batches): heavy keys per size bucket floor(log2(count))
+  int32_t nbucket[32];
 };
 
 struct Dev {
@@ -114,6 +116,9 @@ struct Call {
   uint64_t* sortbuf0;          // [n_max] composite sort buffers (large path)
   uint64_t* sortbuf1;
   int32_t* blockbuf;           // block counts for scans
+  int32_t* hlist;              // [n_max] heavy keys of the current update (segment reduce)
+  float* hbuf;                 // [ceil(D/16)][n_max][16] heavy keys' gradient rows, key-contiguous, slice-major
+  int hcap;                    // n_max (rows per hbuf slice plane)
 };
 
 __device__ __forceinline__ uint64_t fmix64(uint64_t x) {
@@ -329,8 +334,11 @@ void launch_reset_cache(const Dev& s, cudaStream_t st);
 void launch_probe(const Dev& s, const Call& c, int n_max_units, cudaStream_t st);
 void launch_sync_fetch_install_local(const Dev& s, const Call& c, int n_units, cudaStream_t st);
 void launch_gather(const Dev& s, const Call& c, float* out, cudaStream_t st);
-void launch_segreduce_apply(const Dev& s, const Call& c, const float* grads, float lr, int n_units,
-                            cudaStream_t st);
+// K7/K8 for large batches: heavy keys streamed through a TMA ring on `side`
+// (forked from and joined back into `st` with the two events), light keys on
+// `st` concurrently.  Returns the number of kernel launches.
+int launch_segreduce_apply(const Dev& s, const Call& c, const float* grads, float lr, int n, cudaStream_t st,
+                           cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
 int launch_evict_select(const Dev& s, void* evbuf, cudaStream_t st);
 int launch_evict_apply_local(const Dev& s, void* evbuf, cudaStream_t st);
 void launch_hash_rebuild(const Dev& s, cudaStream_t st);

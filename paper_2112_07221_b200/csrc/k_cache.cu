@@ -7,10 +7,7 @@
 //   K45 k_sync_fetch_local  N=1: Evict(k) push + Fetch(k) fused (P:439, P:442-443,
 //                         P:495-500; R5, R6) and the miss install
 //   K6  k_gather          Cache.Get: out[pos] = v[entry(inverse[pos])]
-//   K7  k_segreduce_apply Cache.Update + Cache.Clock: acc = sum G (ascending
-//                         position), d = -lr*acc, v += d, p += d, c_c += 1
-//                         (R11, R13, R17)
-//   (K8/K9 eviction lives in k_evict.cu)
+//   (K7 segment reduce + apply: k_segreduce.cu; K8/K9 eviction: k_evict.cu)
 #include <algorithm>
 
 #include "het_internal.cuh"
@@ -241,120 +238,6 @@ void launch_gather(const Dev& s, const Call& c, float* out, cudaStream_t st) {
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
   k_gather<<<(int)blocks, 256, 0, st>>>(s.v, c.uentry, c.inverse, out, c.n, D4, s.ctl);
-}
-
-// ------------------------------------------------------------------ K7 segment-reduce + apply
-// Heavy keys (many occurrences in the batch, e.g. the top id of a 3-value
-// Criteo field appears ~60 times in 128 samples) would serialise one row load
-// per occurrence.  Their gradient rows are staged into shared memory with TMA
-// bulk copies (cp.async.bulk, one 4D-byte row per lane, all in flight on one
-// mbarrier), then summed in ascending position from shared memory.
-constexpr int SR_WARPS = 4;
-
-__global__ void __launch_bounds__(SR_WARPS * 32)
-k_segreduce_apply(Dev s, Call c, const float* __restrict__ G, float lr, int stage_rows) {
-  extern __shared__ float4 stg[];                 // [SR_WARPS][stage_rows + 1][D4]
-  __shared__ uint64_t bars[SR_WARPS];
-  Ctl* ctl = s.ctl;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int u = blockIdx.x * SR_WARPS + wid;
-  if (ctl->abort || u >= ctl->U) return;
-  // independent loads first: segment bounds, entry, clocks, positions
-  const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
-  const int32_t e = c.uentry[u];
-  const uint32_t ecc = s.cc[e], ecs = s.cs[e];
-  const int cnt = j1 - j0;
-  const int pos_lane = lane < cnt ? __ldg(&c.perm[j0 + lane]) : 0;
-  const bool dirty = ecc > ecs;
-  const int D4 = s.D >> 2;
-  const float nlr = -lr;
-  float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
-  float4* pr = reinterpret_cast<float4*>(s.p + (int64_t)e * s.D);
-  const float4* G4 = reinterpret_cast<const float4*>(G);
-  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (stage_rows > 0 && cnt > 4) {
-    // ---- staged path
-    float4* mystg = stg + (size_t)wid * (stage_rows + 1) * D4;
-    float4* accrow = mystg + (size_t)stage_rows * D4;
-    uint64_t* bar = &bars[wid];
-    if (lane == 0) { mbar_init(bar, 1); fence_mbar_init(); }
-    __syncwarp();
-    uint32_t phase = 0;
-    const uint32_t rowbytes = s.D * 4;
-    for (int kb = 0; kb < cnt; kb += stage_rows) {
-      const int m = min(stage_rows, cnt - kb);
-      const int src = kb == 0 ? pos_lane : (kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0);
-      __syncwarp();
-      fence_proxy_async();
-      if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)m * rowbytes);
-      __syncwarp();
-      if (lane < m) bulk_g2s(mystg + (size_t)lane * D4, G4 + (int64_t)src * D4, rowbytes, bar);
-      mbar_wait(bar, phase);
-      phase ^= 1;
-      for (int d = lane; d < D4; d += 32) {
-        float4 a = kb ? accrow[d] : zero;
-        for (int k = 0; k < m; ++k) a = f4add(a, mystg[(size_t)k * D4 + d]);
-        accrow[d] = a;
-      }
-    }
-    __syncwarp();
-    for (int d = lane; d < D4; d += 32) {
-      float4 acc = accrow[d];
-      float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
-                              __fmul_rn(nlr, acc.w));
-      vr[d] = f4add(vr[d], dl);
-      pr[d] = f4add(dirty ? pr[d] : zero, dl);
-    }
-  } else {
-    // ---- register path: up to 4 independent row loads in flight
-    for (int d = lane; d - lane < D4; d += 32) {
-      const bool act = d < D4;
-      float4 vv = act ? vr[d] : zero;
-      float4 pp = (act && dirty) ? pr[d] : zero;
-      float4 acc = zero;                              // U1: +0.0f, ascending position
-      for (int kb = 0; kb < cnt; kb += 32) {
-        const int src = kb == 0 ? pos_lane : (kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0);
-        const int m = min(32, cnt - kb);
-        int k = 0;
-        for (; k + 4 <= m; k += 4) {
-          int p0 = __shfl_sync(0xffffffffu, src, k), p1 = __shfl_sync(0xffffffffu, src, k + 1);
-          int p2 = __shfl_sync(0xffffffffu, src, k + 2), p3 = __shfl_sync(0xffffffffu, src, k + 3);
-          if (act) {
-            float4 g0 = __ldcs(G4 + (int64_t)p0 * D4 + d), g1 = __ldcs(G4 + (int64_t)p1 * D4 + d);
-            float4 g2 = __ldcs(G4 + (int64_t)p2 * D4 + d), g3 = __ldcs(G4 + (int64_t)p3 * D4 + d);
-            acc = f4add(acc, g0); acc = f4add(acc, g1); acc = f4add(acc, g2); acc = f4add(acc, g3);
-          }
-        }
-        for (; k < m; ++k) {
-          int p0 = __shfl_sync(0xffffffffu, src, k);
-          if (act) acc = f4add(acc, __ldcs(G4 + (int64_t)p0 * D4 + d));
-        }
-      }
-      if (act) {
-        float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
-                                __fmul_rn(nlr, acc.w));  // U2: delta = (-lr) * acc
-        vr[d] = f4add(vv, dl);
-        pr[d] = f4add(pp, dl);                           // clean: fl(+0 + delta) (R13)
-      }
-    }
-  }
-  if (lane == 0) s.cc[e] = ecc + 1;  // Cache.Clock
-}
-
-void launch_segreduce_apply(const Dev& s, const Call& c, const float* grads, float lr, int n_units,
-                            cudaStream_t st) {
-  int blocks = (n_units + SR_WARPS - 1) / SR_WARPS;
-  if (blocks < 1) blocks = 1;
-  const int rowbytes = (int)s.D * 4;
-  int stage_rows = std::min(32, 12288 / rowbytes);   // <= 48 KB of staging per block
-  if (stage_rows < 4) stage_rows = 0;                  // wide rows: column parallelism suffices
-  size_t smem = stage_rows ? (size_t)SR_WARPS * (stage_rows + 1) * rowbytes : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_segreduce_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    attr = true;
-  }
-  k_segreduce_apply<<<blocks, SR_WARPS * 32, smem, st>>>(s, c, grads, lr, stage_rows);
 }
 
 // ------------------------------------------------------------------ hash rebuild

@@ -177,6 +177,55 @@ def test_large_batch_multi_cta_dedup():
     p.finish()
 
 
+@pytest.mark.parametrize("D,B", [(128, 4096), (36, 2048)])
+def test_heavy_key_segment_reduce(D, B):
+    """Per-phase path with Criteo-shaped batches large enough that small fields'
+    keys occur thousands of times: keys with > 32 occurrences go through the
+    TMA-ring heavy-key kernel (those with >= 2048 listed first), the rest through
+    the half-warp kernel, concurrently.  Rows, clocks and pendings after every
+    update must match the oracle's ordered sums."""
+    R = 200000
+    cards = gen.scaled_cards(R)
+    n = B * 26
+    p = Pair(R, D, 0.1, 4, LFU, n_max=n)
+    p.g_policy = LFU
+    counts = np.bincount(np.unique(gen.criteo_keys(0, 0, 1, B, cards)[0].numpy(), return_counts=True)[1])
+    assert counts.size > 2048, "workload must contain keys with >= 2048 occurrences"
+    for t in range(4):
+        keys = gen.criteo_keys(0, t, 1, B, cards)[0].numpy()
+        p.step(t, keys, gen.grads(0, t, keys.size, D).numpy())
+    p.compare_stats()
+    p.compare_cache()
+    p.finish()
+
+
+def test_heavy_key_wide_rows_unfused(monkeypatch):
+    """16 KB rows (D=4096) on the per-phase path: one row per ring stage."""
+    monkeypatch.setenv("HET_NO_FUSED", "1")
+    R, D = 20000, 4096
+    cards = gen.scaled_cards(R)
+    p = Pair(R, D, 0.1, 100, LFU, n_max=4096, track_div=16)
+    p.g_policy = LFU
+    for t in range(6):
+        keys = gen.criteo_keys(0, t, 1, 64, cards)[0].numpy()
+        grads = gen.grads(0, t, keys.size, D).numpy()
+        kd = torch.from_numpy(keys).cuda()
+        out = p.g.lookup(kd, t).cpu().numpy()
+        oo = p.o.lookup(t, [keys])[0]
+        sel = _tracked_mask(keys, 16)
+        assert_rows(out[sel], oo[sel])
+        p.g.update(kd, torch.from_numpy(grads).cuda(), LR)
+        p.o.update([grads], LR)
+    p.compare_stats()
+    keys = np.arange(R, dtype=np.int64)
+    keys = keys[_tracked_mask(keys, 16)]
+    p.g.sync(); p.o.flush()
+    gr, gcg = p.g.read_global(keys)
+    orows, ocg = p.o.read_global(keys)
+    assert np.array_equal(gcg, ocg)
+    assert_rows(gr, orows)
+
+
 def test_eviction_slow_paths():
     """LRU ticks far above the initial base (slow threshold path) and a key
     bucket with more than 16384 tied candidates (slow sub-select path)."""
