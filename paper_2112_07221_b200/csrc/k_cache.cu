@@ -146,62 +146,84 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
 
 // ------------------------------------------------------------------ K45 (N = 1)
 // Server == this rank: apply the sync push of an expired dirty hit (L4) and
-// refetch (L5) in one pass per key; keys are distinct within the call.
-__device__ __forceinline__ void sync_fetch_local_body(Dev& s, Call& c, int* dpop) {
-  Ctl* ctl = s.ctl;
-  int lane = threadIdx.x & 31;
-  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (ctl->abort || u >= ctl->U) return;
-  uint8_t st = c.status[u];
-  if (st == ST_HIT) return;
-  int64_t key = c.uniq[u];
-  int64_t row = key;  // N = 1: local row = key
-  const int D4 = s.D >> 2;
-  float4* Wr = reinterpret_cast<float4*>(s.W + row * s.D);
-  int32_t e;
-  uint32_t g;
-  if (st == ST_EXP1 || st == ST_EXP2) {
-    e = c.uentry[u];
-    uint32_t ecs = s.cs[e], ecc = s.cc[e];
-    g = s.cg[row];
-    if (ecc > ecs) {  // dirty (R13): W += p, c_g = max(c_g, c_c)
-      const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
-      for (int d = lane; d < D4; d += 32) Wr[d] = f4add(Wr[d], pr[d]);
-      g = g > ecc ? g : ecc;
-      if (lane == 0) s.cg[row] = g;
-    }
-  } else {  // MISS: take a free entry, insert into the hash table
-    int32_t idx = 0;
-    if (lane == 0) idx = atomicSub(&ctl->ftop, 1) - 1;
-    idx = __shfl_sync(0xffffffffu, idx, 0);
-    if (idx < 0) {
-      if (lane == 0) raise_err(ctl, 4 /*HET_ERR_CAPACITY*/);
-      return;
-    }
-    e = s.fstack[idx];
-    warp_insert(s, key, e, lane);
-    g = s.cg[row];
-    if (lane == 0) {
-      s.ekey[e] = key;
-      uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
-      s.eprim[e] = prim;
-      if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
-      atomicMin(&ctl->min_install, prim);
-      c.uentry[u] = e;
-    }
-  }
-  // L5: v = W[k], c_s = c_c = c_g  (p need not be zeroed: R13)
-  float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
-  for (int d = lane; d < D4; d += 32) vr[d] = Wr[d];
-  if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
-}
-
+// refetch (L5) in one pass per key; keys are distinct within the call.  Warp
+// per key.  Misses take free entries and report their primary for the
+// eviction lower bound; both go through one global atomic per block (free
+// stack pop, min_install) -- with ~10^5 misses per call, per-warp atomics on
+// those two addresses serialise in L2.  Which free entry a key gets is not
+// observable.
 __global__ void __launch_bounds__(TPB)
 k_sync_fetch_local(Dev s, Call c) {
   __shared__ int dpop[LFU_CB_MAX];
+  __shared__ int s_nmiss, s_base;
+  __shared__ unsigned s_minp;
   dpop_init(dpop);
+  if (threadIdx.x == 0) { s_nmiss = 0; s_minp = 0xFFFFFFFFu; }
   __syncthreads();
-  sync_fetch_local_body(s, c, dpop);
+  Ctl* ctl = s.ctl;
+  const int lane = threadIdx.x & 31;
+  const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const bool live = !ctl->abort && u < ctl->U;
+  const uint8_t st = live ? c.status[u] : (uint8_t)ST_HIT;
+  const int64_t key = live ? c.uniq[u] : 0;
+  const bool miss = live && st == ST_MISS;
+  int moff = 0;
+  uint32_t prim = 0;
+  if (miss) {
+    prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
+    if (lane == 0) {
+      moff = atomicAdd(&s_nmiss, 1);
+      atomicMin(&s_minp, prim);
+    }
+    moff = __shfl_sync(0xffffffffu, moff, 0);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_nmiss) {
+    s_base = atomicSub(&ctl->ftop, s_nmiss);   // entries fstack[s_base - s_nmiss, s_base)
+    atomicMin(&ctl->min_install, s_minp);
+  }
+  __syncthreads();
+  if (live && st != ST_HIT) {
+    const int64_t row = key;  // N = 1: local row = key
+    const int D4 = s.D >> 2;
+    float4* Wr = reinterpret_cast<float4*>(s.W + row * s.D);
+    int32_t e = 0;
+    uint32_t g = 0;
+    bool ok = true;
+    if (st == ST_EXP1 || st == ST_EXP2) {
+      e = c.uentry[u];
+      const uint32_t ecs = s.cs[e], ecc = s.cc[e];
+      g = s.cg[row];
+      if (ecc > ecs) {  // dirty (R13): W += p, c_g = max(c_g, c_c)
+        const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
+        for (int d = lane; d < D4; d += 32) Wr[d] = f4add(Wr[d], pr[d]);
+        g = g > ecc ? g : ecc;
+        if (lane == 0) s.cg[row] = g;
+      }
+    } else {  // MISS: take a free entry, insert into the hash table
+      const int idx = s_base - 1 - moff;
+      if (idx < 0) {
+        if (lane == 0) raise_err(ctl, 4 /*HET_ERR_CAPACITY*/);
+        ok = false;
+      } else {
+        e = s.fstack[idx];
+        warp_insert(s, key, e, lane);
+        g = s.cg[row];
+        if (lane == 0) {
+          s.ekey[e] = key;
+          s.eprim[e] = prim;
+          if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
+          c.uentry[u] = e;
+        }
+      }
+    }
+    if (ok) {
+      // L5: v = W[k], c_s = c_c = c_g  (p need not be zeroed: R13)
+      float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
+      for (int d = lane; d < D4; d += 32) vr[d] = Wr[d];
+      if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
+    }
+  }
   __syncthreads();
   dpop_flush(s, dpop);
 }
