@@ -26,10 +26,12 @@
 // Waits spin on flags in local memory written by peers (one process per GPU,
 // so the waited-for kernel always runs on another GPU); every wait has a
 // wall-clock timeout that raises a sticky error instead of hanging.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -38,6 +40,8 @@
 #include "p2p_dev.cuh"
 
 namespace het {
+
+namespace cg = cooperative_groups;
 
 #ifdef HET_TIMELINE
 constexpr int PTLW = 8192;
@@ -112,6 +116,29 @@ __global__ void k_p2p_build(Dev s, Call c, P2P m, int drain) {
 }
 
 // ---------------------------------------------------------------- owner: wait + link
+// Link every received record into its row's list (grid-stride); tot[src] =
+// records from src this round.
+__device__ __forceinline__ void link_records(const P2P& m, const int32_t* tot) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int src = 0; src < m.N; ++src) {
+    const Rec* rr = reqrec(m, m.rank, src);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot[src]; j += stride) {
+      const int64_t row = rr[j].key / m.N;
+      const int32_t id = (int32_t)(src * m.CAPS + j);
+      const int32_t old = atomicExch(&m.head[row], id);
+      m.next[id] = old;
+      // first record of a row: append the row to the leader list (one atomic per warp)
+      const unsigned am = __activemask();
+      const unsigned lm = __ballot_sync(am, old < 0);
+      const int lead = __ffs(am) - 1, lane = threadIdx.x & 31;
+      int b = 0;
+      if (lane == lead && lm) b = atomicAdd(m.nlead, __popc(lm));
+      b = __shfl_sync(am, b, lead);
+      if (old < 0) m.leaders[b + __popc(lm & ((1u << lane) - 1))] = id;
+    }
+  }
+}
+
 __global__ void k_p2p_link(Dev s, P2P m) {
   __shared__ int s_ok;
   __shared__ int32_t tot[64];
@@ -127,113 +154,122 @@ __global__ void k_p2p_link(Dev s, P2P m) {
     if (blockIdx.x == 0) { m.qtot[threadIdx.x] = (int32_t)flags[threadIdx.x].total; m.qpush[threadIdx.x] = (int32_t)flags[threadIdx.x].pushes; }
   }
   __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int src = 0; src < m.N; ++src) {
-    const Rec* rr = reqrec(m, m.rank, src);
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot[src]; j += stride) {
-      const int64_t row = rr[j].key / m.N;
-      const int32_t id = (int32_t)(src * m.CAPS + j);
-      const int32_t old = atomicExch(&m.head[row], id);
-      m.next[id] = old;
-      if (old < 0) m.leaders[atomicAdd(m.nlead, 1)] = id;
-    }
-  }
+  link_records(m, tot);
   PTL(5);
 }
 
 // ---------------------------------------------------------------- owner: apply + respond
-__global__ void k_p2p_process(Dev s, P2P m) {
-  __shared__ unsigned long long sb[4];
-  bytes_init(sb);
-  PTL(6);
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
+// Warp per linked row (warp-strided): apply the row's records in source order
+// and write the responses into the requesters' inboxes.
+__device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigned long long* sb) {
+  __shared__ int32_t wbuf[32][32];   // per warp: the row's record ids, sorted
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const unsigned long long ep = *m.epoch + 1;
   const int nl = s.ctl->abort ? 0 : *m.nlead;
   const int D4 = s.D >> 2;
+  const Rec* base = reqrec(m, m.rank, 0);
   for (int li = gw; li < nl; li += nw) {
-    const Rec* base = reqrec(m, m.rank, 0);
     const int64_t row = base[m.leaders[li]].key / m.N;
-    // the row's records (<= 2 per source), lane i holds the i-th, sorted by id
-    // = (source rank, pushes before requests)
-    int32_t id = -1;
+    // walk the row's list once (lane 0), sort by id = (source rank, pushes
+    // before requests), hand record i to lane i
     int cnt = 0;
     if (lane == 0) {
       int32_t cur = m.head[row];
       int32_t buf[32];
       while (cur >= 0 && cnt < 32) { buf[cnt++] = cur; cur = m.next[cur]; }
       m.head[row] = -1;
-      for (int i = 1; i < cnt; ++i) {         // insertion sort (tiny)
-        int32_t x = buf[i]; int k = i - 1;
+      for (int a = 1; a < cnt; ++a) {         // insertion sort (tiny)
+        int32_t x = buf[a]; int k = a - 1;
         while (k >= 0 && buf[k] > x) { buf[k + 1] = buf[k]; --k; }
         buf[k + 1] = x;
       }
-      for (int i = 0; i < cnt; ++i) m.next[buf[i]] = i < cnt - 1 ? buf[i + 1] : -1;   // reuse as sorted chain
-      id = cnt ? buf[0] : -1;
+      for (int a = 0; a < cnt; ++a) wbuf[wi][a] = buf[a];
     }
     __syncwarp();
     cnt = __shfl_sync(0xffffffffu, cnt, 0);
-    int32_t first = __shfl_sync(0xffffffffu, id, 0);
-    float4* Wr = reinterpret_cast<float4*>(s.W + row * s.D);
-    uint32_t g = s.cg[row];
-    uint32_t validmask = 0;
-    // pass A: eviction pushes of the previous round (U4), source order
-    for (int32_t cur = first, i = 0; cur >= 0; cur = m.next[cur], ++i) {
-      const int src = cur / (int)m.CAPS;
-      const int64_t j = cur - (int64_t)src * m.CAPS;
-      if (j >= m.qpush[src]) continue;
-      const Rec r = base[cur];
-      const float4* pr = reinterpret_cast<const float4*>(reqrow(m, m.rank, src, j));
-      for (int d = lane; d < D4; d += 32) Wr[d] = f4add_p(Wr[d], pr[d]);
-      g = g > r.cc ? g : r.cc;
-      if (lane == 0) atomicAdd(&sb[3], 16ull + 4ull * s.D);
+    const bool have = lane < cnt;
+    const int32_t id = have ? wbuf[wi][lane] : 0;
+    const int src = id / (int)m.CAPS;
+    const int64_t j = id - (int64_t)src * m.CAPS;
+    Rec r{};
+    bool push = false;
+    if (have) { r = base[id]; push = j < m.qpush[src]; }
+    const uint32_t g0 = s.cg[row];
+    // U4(t-1): eviction pushes raise c_g (max is order-free); L3: condition (2)
+    // for clock-checked hits against c_g after them; L4: sync pushes of the
+    // requests that are not valid hits
+    uint32_t g = g0;
+    const unsigned pushm = __ballot_sync(0xffffffffu, have && push);
+    {
+      uint32_t x = (have && push) ? r.cc : 0u;
+      for (int o = 16; o; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+      g = max(g, x);
     }
-    // pass B: condition (2) for hits that passed condition (1), c_g read now (L3)
-    for (int32_t cur = first, i = 0; cur >= 0; cur = m.next[cur], ++i) {
-      const int src = cur / (int)m.CAPS;
-      const int64_t j = cur - (int64_t)src * m.CAPS;
-      if (j < m.qpush[src]) continue;
-      const Rec r = base[cur];
-      if ((r.kind & 3) == K_NEEDQ && (g <= r.cc || g - r.cc <= s.s)) validmask |= 1u << i;
-    }
-    // pass C: sync pushes of expired hits (EXP1, EXP2), source order (L4)
-    for (int32_t cur = first, i = 0; cur >= 0; cur = m.next[cur], ++i) {
-      const int src = cur / (int)m.CAPS;
-      const int64_t j = cur - (int64_t)src * m.CAPS;
-      if (j < m.qpush[src] || ((validmask >> i) & 1)) continue;
-      const Rec r = base[cur];
-      if (!(r.kind & K_DIRTY)) continue;
-      const float4* pr = reinterpret_cast<const float4*>(reqrow(m, m.rank, src, j));
-      for (int d = lane; d < D4; d += 32) Wr[d] = f4add_p(Wr[d], pr[d]);
-      g = g > r.cc ? g : r.cc;
+    const bool req = have && !push;
+    const bool valid = req && (r.kind & 3) == K_NEEDQ && (g <= r.cc || g - r.cc <= s.s);
+    const unsigned validm = __ballot_sync(0xffffffffu, valid);
+    const bool syncp = req && !valid && (r.kind & K_DIRTY);
+    const unsigned syncm = __ballot_sync(0xffffffffu, syncp);
+    {
+      uint32_t x = syncp ? r.cc : 0u;
+      for (int o = 16; o; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+      g = max(g, x);
     }
     if (lane == 0) s.cg[row] = g;
-    __syncwarp();
-    // pass D: responses (L5): (c_g, status, row) straight into the requester's inbox
-    for (int32_t cur = first, i = 0; cur >= 0; cur = m.next[cur], ++i) {
-      const int src = cur / (int)m.CAPS;
-      const int64_t j = cur - (int64_t)src * m.CAPS;
-      if (j < m.qpush[src]) continue;
-      const int64_t q = j - m.qpush[src];
-      float* rec = resprec(m, src, m.rank, q);
-      const bool valid = (validmask >> i) & 1;
-      if (lane == 0) {
-        reinterpret_cast<uint32_t*>(rec)[0] = g;
-        reinterpret_cast<uint32_t*>(rec)[1] = valid ? 1u : 0u;
-        const Rec r = base[cur];
-        const bool q1 = (r.kind & 3) == K_NEEDQ;
-        atomicAdd(&sb[q1 ? 1 : 3], 16ull);                                 // request received
+    // byte counters: pushes received, requests received / answered
+    if (have) {
+      if (push) atomicAdd(&sb[3], 16ull + 4ull * s.D);
+      else {
+        atomicAdd(&sb[(r.kind & 3) == K_NEEDQ ? 1 : 3], 16ull);
         if (r.kind & K_DIRTY) atomicAdd(&sb[3], 4ull * s.D);
-        atomicAdd(&sb[valid ? 0 : 2], valid ? 8ull : 8ull + 4ull * s.D);   // response sent
-      }
-      if (!valid) {
-        float4* dst = reinterpret_cast<float4*>(rec + 4);
-        for (int d = lane; d < D4; d += 32) dst[d] = Wr[d];
+        atomicAdd(&sb[valid ? 0 : 2], valid ? 8ull : 8ull + 4ull * s.D);
       }
     }
+    // response headers: (c_g, valid) straight into the requester's inbox (L5)
+    float* rec_l = nullptr;
+    if (req) {
+      rec_l = resprec(m, src, m.rank, j - m.qpush[src]);
+      reinterpret_cast<uint32_t*>(rec_l)[0] = g;
+      reinterpret_cast<uint32_t*>(rec_l)[1] = valid ? 1u : 0u;
+    }
+    // row data, lane per float4, records in sorted order: pushes, then sync pushes
+    const unsigned needrow = (pushm | syncm);
+    const unsigned answer = __ballot_sync(0xffffffffu, req && !valid);
+    float4* Wr = reinterpret_cast<float4*>(s.W + row * s.D);
+    for (int d = lane; d - lane < D4; d += 32) {
+      const bool act = d < D4;
+      float4 w = act ? Wr[d] : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int pass = 0; pass < 2; ++pass) {
+        unsigned mm = pass == 0 ? pushm : syncm;
+        while (mm) {
+          const int i = __ffs(mm) - 1;
+          mm &= mm - 1;
+          const int si = __shfl_sync(0xffffffffu, src, i);
+          const int64_t ji = __shfl_sync(0xffffffffu, j, i);
+          if (act) w = f4add_p(w, reinterpret_cast<const float4*>(reqrow(m, m.rank, si, ji))[d]);
+        }
+      }
+      if (act && needrow) Wr[d] = w;
+      unsigned am = answer;
+      while (am) {
+        const int i = __ffs(am) - 1;
+        am &= am - 1;
+        float* rec = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rec_l), i));
+        if (act) reinterpret_cast<float4*>(rec + 4)[d] = w;
+      }
+    }
+    __syncwarp();
   }
+}
+
+__global__ void k_p2p_process(Dev s, P2P m) {
+  __shared__ unsigned long long sb[4];
+  bytes_init(sb);
+  PTL(6);
+  __syncthreads();
+  const unsigned long long ep = *m.epoch + 1;
+  process_rows(s, m, sb);
   PTL(7);
   __syncthreads();
   bytes_flush(s, sb);
@@ -389,10 +425,95 @@ __global__ void k_p2p_pushes(Dev s, P2P m, EvView b) {
 }
 
 // ---------------------------------------------------------------- fused round (n <= 8192)
-// probe + request build + publish in one kernel: warp per unique key does
-// Cache.Find, condition (1), the LFU/LRU touch, writes its positions' inverse
-// and, unless it is a valid hit, its request record (+ pending row) straight
-// into the owner's inbox; the last block publishes the round's flags.
+// probe + request build for one unique key (warp): Cache.Find, condition (1),
+// the LFU/LRU touch, the inverse of its positions and, unless it is a valid
+// hit, its request record (+ pending row) straight into the owner's inbox.
+__device__ __forceinline__ void probe_build_key(const Dev& s, const Call& c, const P2P& m, int u, int lane,
+                                                unsigned* bc, int* dpop, unsigned long long* sb) {
+  Ctl* ctl = s.ctl;
+  const int D4 = s.D >> 2;
+  const int64_t key = c.uniq[u];
+  const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
+  const int cnt = j1 - j0;
+  const int pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
+  uint32_t cntk = 0;
+  if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
+  const int32_t e = warp_find(s, key, lane);
+  uint32_t ecs = 0, ecc = 0;
+  if (e >= 0) { ecs = s.cs[e]; ecc = s.cc[e]; }
+  uint8_t st = ST_MISS;
+  if (lane == 0) {
+    if (s.lfu_persist) { cntk += 1; s.count_by_key[key] = cntk; }
+    if (e >= 0) {
+      if (s.s == S_INF) st = ST_HIT;                       // R4
+      else if (ecc - ecs > s.s) st = ST_EXP1;              // cond (1)
+      else st = ST_NEEDQ;                                  // cond (2) at the owner
+      if (s.policy == 0) {
+        uint32_t oldc = s.eprim[e];
+        uint32_t newc = s.lfu_persist ? cntk : oldc + 1;
+        s.eprim[e] = newc;
+        lfu_move(s, key, oldc, newc, dpop);
+      } else {
+        s.eprim[e] = (uint32_t)ctl->t_cur;
+      }
+    }
+    c.status[u] = st;
+    c.uentry[u] = e;
+    if (st == ST_HIT) atomicAdd(&bc[0], 1u);
+    else if (st == ST_EXP1) atomicAdd(&bc[1], 1u);
+    else if (st == ST_MISS) atomicAdd(&bc[3], 1u);
+  }
+  st = __shfl_sync(0xffffffffu, st, 0);
+  for (int k = lane; k < cnt; k += 32) c.inverse[k < 32 ? pos_lane : c.perm[j0 + k]] = u;
+  if (st != ST_HIT) {
+    const int o = (int)(key % m.N);
+    const bool dirty = e >= 0 && ecc > ecs;
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(&m.lcnt[o], 1);
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    const int64_t j = m.c3cnt[o] + slot;
+    if (lane == 0) {
+      Rec r;
+      r.key = key; r.cc = ecc;
+      r.kind = (st == ST_NEEDQ ? K_NEEDQ : st == ST_EXP1 ? K_EXP1 : K_MISS) | (dirty ? K_DIRTY : 0);
+      reqrec(m, o, m.rank)[j] = r;
+      m.uslot[u] = (int32_t)(o * m.CAPS + slot);
+      atomicAdd(&sb[st == ST_NEEDQ ? 0 : 2], 16ull);
+      if (dirty) atomicAdd(&sb[2], 4ull * s.D);
+    }
+    if (dirty) {
+      const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
+      float4* dst = reinterpret_cast<float4*>(reqrow(m, o, m.rank, j));
+      for (int d = lane; d < D4; d += 32) dst[d] = pr[d];
+    }
+  }
+}
+
+__device__ __forceinline__ void probe_build_flush(const Dev& s, unsigned* bc, int* dpop, unsigned long long* sb,
+                                                  int U) {
+  dpop_flush(s, dpop);
+  bytes_flush(s, sb);
+  if (threadIdx.x == 0) {
+    if (bc[0]) atomicAdd(&s.cnt[C_HITS], (unsigned long long)bc[0]);
+    if (bc[1]) atomicAdd(&s.cnt[C_EXP1], (unsigned long long)bc[1]);
+    if (bc[3]) atomicAdd(&s.cnt[C_MISSES], (unsigned long long)bc[3]);
+    if (blockIdx.x == 0 && !s.ctl->abort) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+  }
+}
+
+// the round's request flags: records to owner o = carried pushes + requests
+__device__ __forceinline__ void publish_requests(const P2P& m, unsigned long long ep) {
+  if (threadIdx.x < m.N) {
+    const int o = threadIdx.x;
+    Flag* f = &reqflag(m, o)[m.rank];
+    f->total = (uint32_t)(m.c3cnt[o] + m.lcnt[o]);
+    f->pushes = (uint32_t)m.c3cnt[o];
+    __threadfence_system();
+    st_release(&f->epoch, ep);
+    m.c3cnt[o] = 0;
+  }
+}
+
 __global__ void __launch_bounds__(256)
 k_probe_build(Dev s, Call c, P2P m) {
   __shared__ unsigned bc[4];
@@ -408,91 +529,96 @@ k_probe_build(Dev s, Call c, P2P m) {
   const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const unsigned long long ep = *m.epoch + 1;
   const int U = ctl->abort ? 0 : ctl->U;
-  const int D4 = s.D >> 2;
-  if (u < U) {
-    const int64_t key = c.uniq[u];
-    const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
-    const int cnt = j1 - j0;
-    const int pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
-    uint32_t cntk = 0;
-    if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
-    const int32_t e = warp_find(s, key, lane);
-    uint32_t ecs = 0, ecc = 0;
-    if (e >= 0) { ecs = s.cs[e]; ecc = s.cc[e]; }
-    uint8_t st = ST_MISS;
-    if (lane == 0) {
-      if (s.lfu_persist) { cntk += 1; s.count_by_key[key] = cntk; }
-      if (e >= 0) {
-        if (s.s == S_INF) st = ST_HIT;                       // R4
-        else if (ecc - ecs > s.s) st = ST_EXP1;              // cond (1)
-        else st = ST_NEEDQ;                                  // cond (2) at the owner
-        if (s.policy == 0) {
-          uint32_t oldc = s.eprim[e];
-          uint32_t newc = s.lfu_persist ? cntk : oldc + 1;
-          s.eprim[e] = newc;
-          lfu_move(s, key, oldc, newc, dpop);
-        } else {
-          s.eprim[e] = (uint32_t)ctl->t_cur;
-        }
-      }
-      c.status[u] = st;
-      c.uentry[u] = e;
-      if (st == ST_HIT) atomicAdd(&bc[0], 1u);
-      else if (st == ST_EXP1) atomicAdd(&bc[1], 1u);
-      else if (st == ST_MISS) atomicAdd(&bc[3], 1u);
-    }
-    st = __shfl_sync(0xffffffffu, st, 0);
-    for (int k = lane; k < cnt; k += 32) c.inverse[k < 32 ? pos_lane : c.perm[j0 + k]] = u;
-    if (st != ST_HIT) {
-      const int o = (int)(key % m.N);
-      const bool dirty = e >= 0 && ecc > ecs;
-      int slot = 0;
-      if (lane == 0) slot = atomicAdd(&m.lcnt[o], 1);
-      slot = __shfl_sync(0xffffffffu, slot, 0);
-      const int64_t j = m.c3cnt[o] + slot;
-      if (lane == 0) {
-        Rec r;
-        r.key = key; r.cc = ecc;
-        r.kind = (st == ST_NEEDQ ? K_NEEDQ : st == ST_EXP1 ? K_EXP1 : K_MISS) | (dirty ? K_DIRTY : 0);
-        reqrec(m, o, m.rank)[j] = r;
-        m.uslot[u] = (int32_t)(o * m.CAPS + slot);
-        atomicAdd(&sb[st == ST_NEEDQ ? 0 : 2], 16ull);
-        if (dirty) atomicAdd(&sb[2], 4ull * s.D);
-      }
-      if (dirty) {
-        const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
-        float4* dst = reinterpret_cast<float4*>(reqrow(m, o, m.rank, j));
-        for (int d = lane; d < D4; d += 32) dst[d] = pr[d];
-      }
-    }
-  }
+  if (u < U) probe_build_key(s, c, m, u, lane, bc, dpop, sb);
   __syncthreads();
-  dpop_flush(s, dpop);
-  bytes_flush(s, sb);
-  if (threadIdx.x == 0) {
-    if (bc[0]) atomicAdd(&s.cnt[C_HITS], (unsigned long long)bc[0]);
-    if (bc[1]) atomicAdd(&s.cnt[C_EXP1], (unsigned long long)bc[1]);
-    if (bc[3]) atomicAdd(&s.cnt[C_MISSES], (unsigned long long)bc[3]);
-    if (blockIdx.x == 0 && !ctl->abort) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
-  }
+  probe_build_flush(s, bc, dpop, sb, U);
   PTL(1);
   if (!last_block(&m.done[0])) return;
-  if (threadIdx.x < m.N) {
-    const int o = threadIdx.x;
-    Flag* f = &reqflag(m, o)[m.rank];
-    f->total = (uint32_t)(m.c3cnt[o] + m.lcnt[o]);
-    f->pushes = (uint32_t)m.c3cnt[o];
-    __threadfence_system();
-    st_release(&f->epoch, ep);
-    m.c3cnt[o] = 0;
-  }
+  publish_requests(m, ep);
   if (threadIdx.x == 0) m.done[0] = 0;
   PTL(2);
 }
 
-// install + gather: wait for the owners' responses, finish the statuses of the
-// clock-checked hits, install fetched rows, scatter every key's row to its
-// occurrences (Cache.Get)
+// install + gather for one unique key (warp): finish the status of a
+// clock-checked hit from the owner's answer, install a fetched row, scatter
+// the key's row to its occurrences (Cache.Get)
+__device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, const P2P& m, int u, int lane,
+                                                   float* __restrict__ out, unsigned* bc, int* dpop,
+                                                   unsigned long long* sb) {
+  Ctl* ctl = s.ctl;
+  const int D4 = s.D >> 2;
+  uint8_t st = c.status[u];
+  int32_t e = c.uentry[u];
+  const int64_t key = c.uniq[u];
+  const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
+  const int cnt = j1 - j0;
+  const int pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
+  bool ok = true;
+  if (st != ST_HIT) {
+    const int loc = m.uslot[u];
+    const int o = loc / (int)m.CAPS;
+    const float* rec = resprec(m, m.rank, o, loc - o * m.CAPS);
+    const uint32_t g = reinterpret_cast<const uint32_t*>(rec)[0];
+    const bool valid = reinterpret_cast<const uint32_t*>(rec)[1] != 0;
+    if (lane == 0) atomicAdd(&sb[valid ? 1 : 3], valid ? 8ull : 8ull + 4ull * s.D);
+    if (st == ST_NEEDQ) {
+      if (lane == 0) { c.status[u] = valid ? ST_HIT : ST_EXP2; atomicAdd(&bc[valid ? 0 : 1], 1u); }
+    }
+    if (!(st == ST_NEEDQ && valid)) {
+      if (st == ST_MISS) {
+        int32_t idx = 0;
+        if (lane == 0) idx = atomicSub(&ctl->ftop, 1) - 1;
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx < 0) {
+          if (lane == 0) raise_err(ctl, 4);
+          ok = false;
+        } else {
+          e = s.fstack[idx];
+          warp_insert(s, key, e, lane);
+          if (lane == 0) {
+            s.ekey[e] = key;
+            const uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
+            s.eprim[e] = prim;
+            if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
+            atomicMin(&ctl->min_install, prim);
+            c.uentry[u] = e;
+          }
+        }
+      }
+      if (ok) {
+        const float4* src = reinterpret_cast<const float4*>(rec + 4);
+        float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
+        for (int d = lane; d < D4; d += 32) vr[d] = src[d];
+        if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
+      }
+    }
+  }
+  if (ok && e >= 0) {
+    const float4* vr = reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    for (int d = lane; d - lane < D4; d += 32) {
+      float4 val = d < D4 ? vr[d] : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int kb = 0; kb < cnt; kb += 32) {
+        const int srcp = kb == 0 ? pos_lane : (kb + lane < cnt ? c.perm[j0 + kb + lane] : 0);
+        const int mm = min(32, cnt - kb);
+        for (int k = 0; k < mm; ++k) {
+          const int pos = __shfl_sync(0xffffffffu, srcp, k);
+          if (d < D4) __stcs(o4 + (int64_t)pos * D4 + d, val);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void install_gather_flush(const Dev& s, unsigned* bc, int* dpop, unsigned long long* sb) {
+  dpop_flush(s, dpop);
+  bytes_flush(s, sb);
+  if (threadIdx.x == 0) {
+    if (bc[0]) atomicAdd(&s.cnt[C_HITS], (unsigned long long)bc[0]);
+    if (bc[1]) atomicAdd(&s.cnt[C_EXP2], (unsigned long long)bc[1]);
+  }
+}
+
 __global__ void __launch_bounds__(256)
 k_install_gather(Dev s, Call c, P2P m, float* __restrict__ out) {
   __shared__ int s_ok;
@@ -511,81 +637,94 @@ k_install_gather(Dev s, Call c, P2P m, float* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int U = (s_ok && !ctl->abort) ? ctl->U : 0;
-  const int D4 = s.D >> 2;
-  if (u < U) {
-    uint8_t st = c.status[u];
-    int32_t e = c.uentry[u];
-    const int64_t key = c.uniq[u];
-    const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
-    const int cnt = j1 - j0;
-    const int pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
-    bool ok = true;
-    if (st != ST_HIT) {
-      const int loc = m.uslot[u];
-      const int o = loc / (int)m.CAPS;
-      const float* rec = resprec(m, m.rank, o, loc - o * m.CAPS);
-      const uint32_t g = reinterpret_cast<const uint32_t*>(rec)[0];
-      const bool valid = reinterpret_cast<const uint32_t*>(rec)[1] != 0;
-      if (lane == 0) atomicAdd(&sb[valid ? 1 : 3], valid ? 8ull : 8ull + 4ull * s.D);
-      if (st == ST_NEEDQ) {
-        if (lane == 0) { c.status[u] = valid ? ST_HIT : ST_EXP2; atomicAdd(&bc[valid ? 0 : 1], 1u); }
-      }
-      if (!(st == ST_NEEDQ && valid)) {
-        if (st == ST_MISS) {
-          int32_t idx = 0;
-          if (lane == 0) idx = atomicSub(&ctl->ftop, 1) - 1;
-          idx = __shfl_sync(0xffffffffu, idx, 0);
-          if (idx < 0) {
-            if (lane == 0) raise_err(ctl, 4);
-            ok = false;
-          } else {
-            e = s.fstack[idx];
-            warp_insert(s, key, e, lane);
-            if (lane == 0) {
-              s.ekey[e] = key;
-              const uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
-              s.eprim[e] = prim;
-              if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
-              atomicMin(&ctl->min_install, prim);
-              c.uentry[u] = e;
-            }
-          }
-        }
-        if (ok) {
-          const float4* src = reinterpret_cast<const float4*>(rec + 4);
-          float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
-          for (int d = lane; d < D4; d += 32) vr[d] = src[d];
-          if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
-        }
-      }
-    }
-    if (ok && e >= 0) {
-      const float4* vr = reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D);
-      float4* o4 = reinterpret_cast<float4*>(out);
-      for (int d = lane; d - lane < D4; d += 32) {
-        float4 val = d < D4 ? vr[d] : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int kb = 0; kb < cnt; kb += 32) {
-          const int srcp = kb == 0 ? pos_lane : (kb + lane < cnt ? c.perm[j0 + kb + lane] : 0);
-          const int mm = min(32, cnt - kb);
-          for (int k = 0; k < mm; ++k) {
-            const int pos = __shfl_sync(0xffffffffu, srcp, k);
-            if (d < D4) __stcs(o4 + (int64_t)pos * D4 + d, val);
-          }
-        }
-      }
-    }
-  }
+  if (u < U) install_gather_key(s, c, m, u, lane, out, bc, dpop, sb);
   __syncthreads();
-  dpop_flush(s, dpop);
-  bytes_flush(s, sb);
-  if (threadIdx.x == 0) {
-    if (bc[0]) atomicAdd(&s.cnt[C_HITS], (unsigned long long)bc[0]);
-    if (bc[1]) atomicAdd(&s.cnt[C_EXP2], (unsigned long long)bc[1]);
-  }
+  install_gather_flush(s, bc, dpop, sb);
   if (!last_block(&m.done[2])) return;
   if (threadIdx.x == 0) { *m.epoch = ep; m.done[2] = 0; }
 }
 
+// ---------------------------------------------------------------- the whole round, one cooperative kernel
+// One block per SM (so concurrent NCCL kernels always find room: no
+// cross-GPU resource cycle), grid syncs between the phases instead of kernel
+// boundaries.  Every block reaches every grid sync (no early returns).
+__global__ void __launch_bounds__(512)
+k_exchange(Dev s, Call c, P2P m, float* __restrict__ out) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned bc[4];
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ unsigned long long sb[4];
+  __shared__ int s_ok;
+  __shared__ int32_t tot[64];
+  Ctl* ctl = s.ctl;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long ep = *m.epoch + 1;
+  // ---- requester: probe + build
+  if (threadIdx.x < 4) bc[threadIdx.x] = 0;
+  dpop_init(dpop);
+  bytes_init(sb);
+  __syncthreads();
+  PTL(0);
+  const int U = ctl->abort ? 0 : ctl->U;
+  for (int u = gw; u < U; u += nw) probe_build_key(s, c, m, u, lane, bc, dpop, sb);
+  __syncthreads();
+  probe_build_flush(s, bc, dpop, sb, U);
+  PTL(1);
+  __threadfence();
+  grid.sync();
+  if (blockIdx.x == 0) publish_requests(m, ep);
+  PTL(2);
+  // ---- owner: wait for every source, link
+  PTL(3);
+  if (threadIdx.x == 0) s_ok = wait_flags(reqflag(m, m.rank), m.N, ep, ctl);
+  __syncthreads();
+  PTL(4);
+  const bool ok1 = s_ok;
+  if (threadIdx.x < m.N) {
+    const Flag* flags = reqflag(m, m.rank);
+    tot[threadIdx.x] = ok1 ? (int32_t)flags[threadIdx.x].total : 0;
+    if (blockIdx.x == 0) {
+      m.qtot[threadIdx.x] = ok1 ? (int32_t)flags[threadIdx.x].total : 0;
+      m.qpush[threadIdx.x] = ok1 ? (int32_t)flags[threadIdx.x].pushes : 0;
+    }
+  }
+  bytes_init(sb);
+  __syncthreads();
+  link_records(m, tot);
+  PTL(5);
+  grid.sync();
+  // ---- owner: apply + respond
+  PTL(6);
+  process_rows(s, m, sb);
+  PTL(7);
+  __syncthreads();
+  bytes_flush(s, sb);
+  __threadfence();
+  grid.sync();
+  if (blockIdx.x == 0) {
+    if (threadIdx.x < m.N) {
+      __threadfence_system();
+      st_release(&respflag(m, threadIdx.x)[m.rank].epoch, ep);
+    }
+    if (threadIdx.x == 0) *m.nlead = 0;
+  }
+  PTL(8);
+  // ---- requester: wait for every owner, install + gather
+  if (threadIdx.x < 4) bc[threadIdx.x] = 0;
+  dpop_init(dpop);
+  bytes_init(sb);
+  PTL(9);
+  if (threadIdx.x == 0) s_ok = wait_flags(respflag(m, m.rank), m.N, ep, ctl);
+  __syncthreads();
+  PTL(10);
+  const int U2 = (s_ok && !ctl->abort) ? ctl->U : 0;
+  for (int u = gw; u < U2; u += nw) install_gather_key(s, c, m, u, lane, out, bc, dpop, sb);
+  __syncthreads();
+  install_gather_flush(s, bc, dpop, sb);
+  if (last_block(&m.done[2]) && threadIdx.x == 0) { *m.epoch = ep; m.done[2] = 0; }
+}
 
 // ---------------------------------------------------------------- host side
 struct P2PState {
@@ -691,6 +830,19 @@ int p2p_round(P2PState* p, const Dev& d, const Call& c, int drain, cudaStream_t 
 int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaStream_t st) {
   P2P& v = p->v;
   cudaMemsetAsync(v.lcnt, 0, 4 * v.N, st);
+  static const bool split = getenv("HET_P2P_SPLIT") != nullptr;   // diagnostic: the four-kernel round
+  if (!split) {
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    Dev dd = d;
+    Call cc = c;
+    P2P vv = v;
+    float* oo = out;
+    void* args[] = {&dd, &cc, &vv, &oo};
+    if (cudaLaunchCooperativeKernel((void*)k_exchange, dim3(nsm), dim3(512), args, 0, st) == cudaSuccess) return 1;
+    cudaGetLastError();   // fall through to the split round
+  }
   const int blocks = std::max(1, (c.n + 7) / 8);
   k_probe_build<<<blocks, 256, 0, st>>>(d, c, v);
   k_p2p_link<<<148, 256, 0, st>>>(d, v);
