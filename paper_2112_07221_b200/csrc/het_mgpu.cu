@@ -499,7 +499,15 @@ het_status_t mgpu_create(MgpuState*& mg, const Dev& d, uint32_t n_max, const voi
   m->REC = 4 + d.D;
   ncclUniqueId id;
   std::memcpy(&id, uid, sizeof(id));
-  if (ncclCommInitRank(&m->comm, d.world, id, d.rank) != ncclSuccess) return HET_ERR_NCCL;
+  // NCCL's kernels (the dense all-reduce, overlapped on a side stream) are
+  // capped at NCCL_CTAS blocks, and the cooperative hot-path kernels leave that
+  // many SMs free (het::coop_sm_reserve), so neither waits for the other's SMs.
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  if (!getenv("HET_NCCL_DEFAULT")) {   // diagnostic: NCCL's own CTA choice
+    cfg.maxCTAs = coop_sm_reserve();
+    cfg.minCTAs = std::min(4, cfg.maxCTAs);
+  }
+  if (ncclCommInitRankConfig(&m->comm, d.world, id, d.rank, &cfg) != ncclSuccess) return HET_ERR_NCCL;
   const int64_t NC = (int64_t)m->N * m->CAPS;
   bool ok = mg_alloc(m, &m->qkeys, NC) && mg_alloc(m, &m->qidx, NC) && mg_alloc(m, &m->rqkeys, NC) &&
             mg_alloc(m, &m->ans, NC) && mg_alloc(m, &m->ansr, NC) && mg_alloc(m, &m->hdr, NC) &&

@@ -111,6 +111,7 @@ __global__ void k_p2p_build(Dev s, Call c, P2P m, int drain) {
     __threadfence_system();
     st_release(&f->epoch, ep);
     m.c3cnt[o] = 0;
+    m.lcnt[o] = 0;
   }
   if (threadIdx.x == 0) m.done[0] = 0;
 }
@@ -511,6 +512,7 @@ __device__ __forceinline__ void publish_requests(const P2P& m, unsigned long lon
     __threadfence_system();
     st_release(&f->epoch, ep);
     m.c3cnt[o] = 0;
+    m.lcnt[o] = 0;   // counted; zero for the next round (no memset node in the step graph)
   }
 }
 
@@ -721,9 +723,12 @@ k_exchange(Dev s, Call c, P2P m, float* __restrict__ out) {
   PTL(10);
   const int U2 = (s_ok && !ctl->abort) ? ctl->U : 0;
   for (int u = gw; u < U2; u += nw) install_gather_key(s, c, m, u, lane, out, bc, dpop, sb);
+  PTL(11);
   __syncthreads();
   install_gather_flush(s, bc, dpop, sb);
-  if (last_block(&m.done[2]) && threadIdx.x == 0) { *m.epoch = ep; m.done[2] = 0; }
+  // every block read the epoch at entry, before three grid syncs: block 0 can
+  // advance it without a fence (the next round is ordered by the kernel boundary)
+  if (blockIdx.x == 0 && threadIdx.x == 0) *m.epoch = ep;
 }
 
 // ---------------------------------------------------------------- host side
@@ -828,8 +833,7 @@ int p2p_round(P2PState* p, const Dev& d, const Call& c, int drain, cudaStream_t 
 
 // fused round: probe+build, owner link, owner process, install+gather
 int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaStream_t st) {
-  P2P& v = p->v;
-  cudaMemsetAsync(v.lcnt, 0, 4 * v.N, st);
+  P2P& v = p->v;   // lcnt is zero here: the previous round's publish reset it
   static const bool split = getenv("HET_P2P_SPLIT") != nullptr;   // diagnostic: the four-kernel round
   if (!split) {
     int dev = 0, nsm = 0;
@@ -840,7 +844,9 @@ int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaSt
     P2P vv = v;
     float* oo = out;
     void* args[] = {&dd, &cc, &vv, &oo};
-    if (cudaLaunchCooperativeKernel((void*)k_exchange, dim3(nsm), dim3(512), args, 0, st) == cudaSuccess) return 1;
+    if (cudaLaunchCooperativeKernel((void*)k_exchange, dim3(nsm - coop_sm_reserve()), dim3(512), args, 0, st) ==
+        cudaSuccess)
+      return 1;
     cudaGetLastError();   // fall through to the split round
   }
   const int blocks = std::max(1, (c.n + 7) / 8);

@@ -21,6 +21,9 @@
 //                  selection then apply.  Hash rebuild, when requested.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "evict_dev.cuh"
 #include "p2p_dev.cuh"
 
@@ -768,6 +771,15 @@ int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st
   return 1;
 }
 
+int coop_sm_reserve() {
+  static int r = -1;
+  if (r < 0) {
+    const char* e = getenv("HET_NCCL_CTAS");
+    r = e ? std::max(1, atoi(e)) : 32;
+  }
+  return r;
+}
+
 int launch_update_fused(const Dev& s, const Call& c, const float* grads, float lr, void* evbuf, cudaStream_t st,
                         const void* p2pview) {
   static int coop_blocks = 0;
@@ -785,7 +797,8 @@ int launch_update_fused(const Dev& s, const Call& c, const float* grads, float l
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_update_fused, UPD_THREADS, smem);
-    coop_blocks = sms * std::max(per, 1);
+    // N > 1: leave NCCL's SMs free (the overlapped dense all-reduce)
+    coop_blocks = (s.world > 1 ? sms - coop_sm_reserve() : sms) * std::max(per, 1);
     forD = s.D;
   }
   EvBuf& b = *reinterpret_cast<EvBuf*>(evbuf);
