@@ -5,12 +5,16 @@ synthetic input: het_lookup (dedup, probe, CheckValid, sync/fetch, gather)
 + het_update (segment-reduce, SGD apply + pending, overflow eviction) and,
 with N > 1, the dense all-reduce of the MLP gradients.
 
-N = 1 workload: BASELINE.json configs[1] "WDL on Criteo-shaped synthetic":
-26 Zipf(0.7) fields, 33,762,577 rows, D = 128, batch 128, cache 10 %,
-s = 100, LFU.  N > 1: configs[3] "DCN", the same per-GPU batch with the
-table hash-sharded over the GPUs (weak scaling).
+Default workload (the driver's lines): N = 1 -> BASELINE.json configs[1]
+"WDL on Criteo-shaped synthetic": 26 Zipf(0.7) fields, 33,762,577 rows,
+D = 128, batch 128, cache 10 %, s = 100, LFU.  N > 1 -> configs[3] "DCN", the
+same per-GPU batch with the table hash-sharded over the GPUs (weak scaling).
+`--workload reddit` = configs[2] (232,965 node ids, 14,208 distinct ids per
+GPU-iteration, D = 128, s = 10); `--workload scale` = configs[4] (D = 4096,
+Criteo-shaped fields scaled to 3,000,000 rows per GPU, i.e. 24M rows at N = 8).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--sweep]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload auto|wdl|dcn|reddit|scale] [--no-sweep]
 """
 from __future__ import annotations
 
@@ -35,8 +39,38 @@ from workload import gen  # noqa: E402
 METRIC = "embedding rows/s (lookup+update)"
 UNIT = "rows/s"
 R_WDL = sum(gen.CRITEO_CARDS)
-CFG = dict(rows=R_WDL, D=128, batch=128, fields=26, cache_frac=0.1, s=100, policy="LFU", alpha=0.7,
-           lr=0.01, dense_params=1 << 20)
+SCALE_ROWS_PER_GPU = 3_000_000          # configs[4]: 24M rows over 8 GPUs
+
+
+def workload_cfg(name, world):
+    """BASELINE.json configs as bench workloads (SURVEY.md §8 per-config table).
+    `keys` names the generator; n = batch*fields (Criteo-shaped) or K (Reddit)."""
+    base = dict(D=128, batch=128, fields=26, cache_frac=0.1, policy="LFU", lr=0.01, dense_params=1 << 20)
+    if name == "auto":
+        name = "wdl" if world == 1 else "dcn"
+    if name in ("wdl", "dcn"):
+        c = dict(base, rows=R_WDL, s=100, alpha=0.7, keys="criteo", n=128 * 26)
+    elif name == "reddit":
+        # GraphSAGE-shaped: 128 seeds x (1 + 10 + 100) sampled ids, all distinct (P:687)
+        c = dict(base, rows=gen.REDDIT_ROWS, s=10, alpha=1.0, keys="reddit", n=14208, fields=None)
+    elif name == "scale":
+        c = dict(base, rows=SCALE_ROWS_PER_GPU * world, D=4096, s=100, alpha=0.7, keys="scale", n=128 * 26)
+    else:
+        raise ValueError(name)
+    c["name"] = {"wdl": "WDL", "dcn": "DCN", "reddit": "Reddit-GraphSAGE", "scale": "scale-D4096"}[name]
+    return c
+
+
+CFG = workload_cfg("wdl", 1)       # mutated by main() for the selected workload
+
+
+def make_keys(rank, t0, T, device):
+    """[T, n] int64 keys of worker `rank`, iterations t0..t0+T-1."""
+    if CFG["keys"] == "reddit":
+        return torch.stack([gen.reddit_keys(rank, t0 + j, CFG["n"], CFG["rows"], CFG["alpha"], device=device)
+                            for j in range(T)])
+    cards = gen.cards_for("criteo") if CFG["keys"] == "criteo" else gen.scaled_cards(CFG["rows"])
+    return gen.criteo_keys(rank, t0, T, CFG["batch"], cards, CFG["alpha"], device=device)
 
 
 def peaks():
@@ -144,12 +178,12 @@ def algorithmic_bytes(kernel, s, D, n_steps, resident):
         return n * row + 4 * n + U * 4 * row + 8 * U
     if kernel == "evict_select":
         # LFU bitmap path: the threshold count's block counters + bitmap words, victim keys out
-        return 4 * ((R_WDL + 4095) // 4096) + 16 * e
+        return 4 * ((CFG["rows"] + 4095) // 4096) + 16 * e
     if kernel == "evict_apply":
         # per victim: key, hash slot, entry metadata; dirty: p read, W read+write, c_g
         return e * (8 + 12 + 16) + ed * (3 * row + 8)
     if kernel == "evict":
-        return 4 * ((R_WDL + 4095) // 4096) + 16 * e + e * (8 + 12 + 16) + ed * (3 * row + 8)
+        return 4 * ((CFG["rows"] + 4095) // 4096) + 16 * e + e * (8 + 12 + 16) + ed * (3 * row + 8)
     # fused kernels = the sum of the phases they fuse
     if kernel in ("lookup_fused", "exchange_fused"):
         # exchange_fused: the local HBM side of the round (records over NVLink not counted)
@@ -169,10 +203,9 @@ def run_gpu(args):
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=device)
     B, D, F = CFG["batch"], CFG["D"], CFG["fields"]
-    n = B * F
+    n = CFG["n"]
     R = CFG["rows"]
     lr = CFG["lr"]
-    cards = gen.cards_for("criteo")
     uid = None
     if world > 1:
         obj = [het.het_get_unique_id() if rank == 0 else None]
@@ -182,18 +215,24 @@ def run_gpu(args):
                          unique_id=uid, max_keys_per_call=n)
     C = int(math.floor(CFG["cache_frac"] * R))
 
+    # gradient pool: distinct seeded grads per step up to ~2 GB (cache decisions
+    # do not depend on gradient values, SURVEY §8(c) "value-independence")
+    W, K = args.warmup, args.steps
+    G = max(4, min(W + 2 * K, int(2e9 // (n * D * 4))))
+    grads_all = [gen.grads(rank, j, n, D, device=device) for j in range(G)]
+
     # ---- fill: run the hot path until the cache holds C entries (untimed setup)
     t = 0
-    chunk = 500
+    chunk = 500 if CFG["keys"] != "reddit" else 4
     fill_steps = 0
     t_fill0 = time.time()
     AUTO = het.HET_CLOCK_AUTO
     while True:
-        keys_blk = gen.criteo_keys(rank, t, chunk, B, cards, CFG["alpha"], device=device)
+        keys_blk = make_keys(rank, t, chunk, device)
         for j in range(chunk):
             k = keys_blk[j]
             cache.lookup(k, AUTO)
-            cache.update(k, gen.grads(rank, t, n, D, device=device), lr)
+            cache.update(k, grads_all[t % G], lr)
             t += 1
         fill_steps += chunk
         res = cache.stats()["resident"]
@@ -205,9 +244,7 @@ def run_gpu(args):
     fill_s = time.time() - t_fill0
 
     # ---- inputs of the measured steps, resident in HBM before timing
-    W, K = args.warmup, args.steps
-    keys_all = gen.criteo_keys(rank, t, W + 2 * K, B, cards, CFG["alpha"], device=device)
-    grads_all = [gen.grads(rank, t + j, n, D, device=device) for j in range(W + 2 * K)]
+    keys_all = make_keys(rank, t, W + 2 * K, device)
     dense = gen.dense_grads(rank, 0, CFG["dense_params"], device=device)   # the step's dense gradients
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)   # > 126 MB L2
     align_t = torch.zeros(1, device=device)
@@ -226,7 +263,7 @@ def run_gpu(args):
 
     def step(j):
         # dense all-reduce overlapped on a side stream (N > 1)
-        cache.step(keys_all[j], grads_all[j], out_buf, lr, dense if use_dense else None, side)
+        cache.step(keys_all[j], grads_all[j % G], out_buf, lr, dense if use_dense else None, side)
 
     out_buf = torch.empty((n, D), dtype=torch.float32, device=device)
     # static input buffers of the captured step (the data loader / dense
@@ -253,7 +290,7 @@ def run_gpu(args):
         graph = cache.capture_step(kbuf, gbuf, out_buf, lr, dense if use_dense else None)
         graph_launches = cache.stats()["launches"] - l0
         for j in range(3):
-            kbuf.copy_(keys_all[j]); gbuf.copy_(grads_all[j]); graph.replay()
+            kbuf.copy_(keys_all[j]); gbuf.copy_(grads_all[j % G]); graph.replay()
     barrier(world, device)
     s0 = cache.stats()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
@@ -262,7 +299,7 @@ def run_gpu(args):
     for j in range(K):
         between_steps(j)
         if use_graph:
-            kbuf.copy_(keys_all[W + j]); gbuf.copy_(grads_all[W + j])
+            kbuf.copy_(keys_all[W + j]); gbuf.copy_(grads_all[(W + j) % G])
             ev[j][0].record(st)
             graph.replay()
             ev[j][1].record(st)
@@ -321,19 +358,20 @@ def run_gpu(args):
 
     # ---- e2e: same steps through the C-ABI with host (pinned) buffers
     keys_h = keys_all[:W + K].cpu().pin_memory()
-    grads_h = [g.cpu().pin_memory() for g in grads_all[:W + K]]
+    grads_h = [grads_all[j % G].cpu().pin_memory() for j in range(min(W + K, G))]
+    GH = len(grads_h)
     out_h = torch.empty((n, D), dtype=torch.float32).pin_memory()
     te0, te1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for j in range(W):
         het.het_lookup(cache.h, keys_h[j], n, AUTO, out_h)
-        het.het_update(cache.h, keys_h[j], n, grads_h[j], lr)
+        het.het_update(cache.h, keys_h[j], n, grads_h[j % GH], lr)
     barrier(world, device)
     e2e_ms = 0.0
     for j in range(K):
         between_steps(j)
         te0.record(st)
         het.het_lookup(cache.h, keys_h[W + j], n, AUTO, out_h)
-        het.het_update(cache.h, keys_h[W + j], n, grads_h[W + j], lr)
+        het.het_update(cache.h, keys_h[W + j], n, grads_h[(W + j) % GH], lr)
         if use_dense:
             side.wait_stream(st)
             with torch.cuda.stream(side):
@@ -345,18 +383,22 @@ def run_gpu(args):
     e2e_ms = max_over_ranks(e2e_ms / K, world, device)
 
     value = n * world / (ms * 1e-3)
+    DATA = {"criteo": "synthetic (seeded Zipf Criteo-shaped keys, counter-hash fp32 grads)",
+            "scale": "synthetic (seeded Zipf Criteo-shaped keys over fields scaled to the table, counter-hash fp32 grads)",
+            "reddit": "synthetic (seeded Zipf(1.0) Reddit-shaped node ids, all distinct per step; counter-hash fp32 grads)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (seeded Zipf Criteo-shaped keys, counter-hash fp32 grads)",
-        "config": {"workload": "WDL" if world == 1 else "DCN", "rows": R, "D": D, "batch_per_gpu": B,
-                   "fields": F, "cache_frac": CFG["cache_frac"], "cache_entries_per_gpu": C,
+        "dtype": "f32", "data": DATA[CFG["keys"]],
+        "config": {"workload": CFG["name"], "rows": R, "D": D, "batch_per_gpu": B,
+                   "keys_per_gpu_step": n, "fields": F, "cache_frac": CFG["cache_frac"],
+                   "cache_entries_per_gpu": C,
                    "s": CFG["s"], "policy": CFG["policy"], "zipf_alpha": CFG["alpha"],
                    "dense_params": CFG["dense_params"] if use_dense else 0,
                    "parallelism": f"hash-sharded table x{world}, dp{world}",
                    "l2": "flushed between timed steps (256 MB write outside the step events)"
                    + ("; ranks re-aligned after the flush by a 1-element all-reduce, outside the events" if world > 1 else ""),
-                   "fill_steps": fill_steps, "fill_s": round(fill_s, 1)},
+                   "fill_steps": fill_steps, "fill_s": round(fill_s, 1), "grad_pool": G},
         "samples_per_s": B * world / (ms * 1e-3),
         "unique_rows_per_s": sd["unique"] / K * world / (ms * 1e-3),
         "step_counters": {k: v / K for k, v in sd.items()},
@@ -372,11 +414,11 @@ def run_gpu(args):
     }
     del graph
     torch.cuda.synchronize()
-    if not args.no_sweep and world == 1:
+    if not args.no_sweep and world == 1 and CFG["name"] == "WDL":
         line["hbm_sweep"] = run_sweep(het, device)
     barrier(world, device)
     cache.close()
-    if rank == 0:
+    if rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(args)
     return line, rank, world
 
@@ -419,32 +461,37 @@ def run_sweep(het, device):
 
 
 # ----------------------------------------------------------------------------- oracle legs
-def oracle_sample(steps, warmup):
-    """The CPU oracle (as it stands) on the WDL workload from a cold cache:
-    `warmup` untimed + `steps` timed iterations, full D=128 rows, 1 thread."""
+def oracle_sample(steps, warmup, world=1, budget_s=15.0):
+    """The CPU oracle (as it stands) on the selected workload from a cold
+    cache, simulating `world` lock-step workers on one core: `warmup` untimed
+    iterations, then up to `steps` timed ones, stopping early once `budget_s`
+    of CPU time is spent (a bounded sample).  Full D rows.  Returns
+    (rows/s, seconds, timed iterations)."""
     from oracle.oracle import Oracle, capacity
-    B, D, F = CFG["batch"], CFG["D"], CFG["fields"]
-    n = B * F
-    R = CFG["rows"]
-    o = Oracle(R=R, D=D, C=capacity(CFG["cache_frac"], R), s=CFG["s"])
-    cards = gen.cards_for("criteo")
-    keys = gen.criteo_keys(0, 0, warmup + steps, B, cards, CFG["alpha"]).numpy()
-    grads = [gen.grads(0, j, n, D).numpy() for j in range(warmup + steps)]
+    n, D, R = CFG["n"], CFG["D"], CFG["rows"]
+    o = Oracle(R=R, D=D, C=capacity(CFG["cache_frac"], R), s=CFG["s"], N=world)
+    keys = [make_keys(i, 0, warmup + steps, "cpu").numpy() for i in range(world)]
+    G = max(4, min(warmup + steps, int(1e9 // (n * D * 4 * world))))
+    grads = [[gen.grads(i, j, n, D).numpy() for i in range(world)] for j in range(G)]
     for j in range(warmup):
-        o.lookup(j, [keys[j]])
-        o.update([grads[j]], CFG["lr"])
+        o.lookup(j, [keys[i][j] for i in range(world)], want_out=False)
+        o.update(grads[j % G], CFG["lr"])
+    done = 0
     t0 = time.perf_counter()
     for j in range(warmup, warmup + steps):
-        o.lookup(j, [keys[j]])
-        o.update([grads[j]], CFG["lr"])
+        o.lookup(j, [keys[i][j] for i in range(world)])
+        o.update(grads[j % G], CFG["lr"])
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
     dt = time.perf_counter() - t0
-    return n * steps / dt, dt
+    return n * world * done / dt, dt, done
 
 
 def cpu_baseline(args, steps=300):
-    v, dt = oracle_sample(steps, 5)
+    v, dt, done = oracle_sample(steps, 5)
     return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"WDL config, iterations 5..{5 + steps} from a cold cache (full D=128 rows), "
+            "sample": f"{CFG['name']} config, iterations 5..{5 + done} from a cold cache (full D={CFG['D']} rows), "
                       f"single-threaded C++ oracle, {dt:.1f} s; host: {os.cpu_count()} cores, "
                       f"{_cpu_model()}"}
 
@@ -460,22 +507,25 @@ def _cpu_model():
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle of the paper's protocol (there is no
+    reference code to install), on this arm's workload with
+    `world` simulated workers, rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return None
-    v, dt = oracle_sample(args.steps, args.warmup)
-    n = CFG["batch"] * CFG["fields"]
-    ms = dt / args.steps * 1e3
+    v, dt, done = oracle_sample(args.steps, args.warmup, world, budget_s=120.0)
+    ms = dt / done * 1e3
+    sample = (f"{CFG['name']} iterations {args.warmup}..{args.warmup + done} from a cold cache, {world} worker(s) "
+              f"simulated in lock step, single-threaded C++ oracle of the paper's protocol"
+              + (f" (stopped after {done} of {args.steps} steps: 120 s budget)" if done < args.steps else "")
+              + f"; {os.cpu_count()} host cores, {_cpu_model()}")
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "WDL" if world == 1 else "DCN", "rows": CFG["rows"], "D": CFG["D"],
-                       "batch_per_gpu": CFG["batch"], "cache_frac": CFG["cache_frac"], "s": CFG["s"],
-                       "policy": CFG["policy"]},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"first {args.warmup}+{args.steps} WDL iterations from a cold cache, "
-                                       f"single-threaded C++ oracle of the paper's protocol; "
-                                       f"{os.cpu_count()} host cores, {_cpu_model()}"},
+            "config": {"workload": CFG["name"], "rows": CFG["rows"], "D": CFG["D"],
+                       "batch_per_gpu": CFG["batch"], "keys_per_gpu_step": CFG["n"],
+                       "cache_frac": CFG["cache_frac"], "s": CFG["s"], "policy": CFG["policy"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -486,8 +536,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-sweep", action="store_true", help="skip the D=128 n-sweep (HBM regime)")
+    ap.add_argument("--workload", default="auto", choices=["auto", "wdl", "dcn", "reddit", "scale"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    CFG.clear()
+    CFG.update(workload_cfg(args.workload, dist_env()[1]))
     if args.impl == "reference":
         line = run_reference(args)
         if line is not None:

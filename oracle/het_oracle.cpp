@@ -22,12 +22,16 @@
 //   L5  install expired hits and misses: v = W[u], p = 0,
 //       cs = cc = cg[u]                                            (Cache.Fetch; R6)
 //   L6  count_i[u] += 1, tick[u] = t                               (LFU/LRU; R7, R8)
+//       light-LFU (R27): a pinned entry skips the count update;
+//       an unpinned one reaching count >= theta is pinned, ascending key,
+//       while fewer than floor(C/2) entries are pinned
 //   L7  out[pos] = v[K_i[pos]]                                     (Cache.Get)
 //   U1  acc = +0.0f; acc += G[pos] for pos ascending among u's
 //       occurrences                                                (Cache.Update, Alg.3 l.2; R11)
 //   U2  d = (-lr)*acc; v += d; p += d; cc += 1                     (Cache.Update + Cache.Clock)
 //   U3  while |cache_i| > C: evict min (count,key) [LFU] or
 //       (tick,key) [LRU]; dirty (cc > cs) victims push (k,p,cc)    (Cache.Evict(); R9, R13)
+//       light-LFU: pinned entries are exempt                        (R27)
 //   U4  server applies eviction pushes rank asc, key asc
 //   flush (het_sync): every worker pushes all dirty entries
 //       (rank asc, key asc) and empties its cache                  (R16)
@@ -74,6 +78,7 @@ struct Entry {
   uint32_t cc = 0;       // current clock c_c
   uint32_t tick = 0;     // LRU recency (R8)
   uint32_t own_count = 0;  // LFU count when lfu_persist == 0 (reset on install)
+  bool pinned = false;     // light-LFU direct-access entry (R27)
 };
 
 struct Push { int64_t key; std::vector<float> p; uint32_t cc; };
@@ -81,7 +86,8 @@ struct Push { int64_t key; std::vector<float> p; uint32_t cc; };
 struct Worker {
   std::map<int64_t, Entry> cache;                 // the cache embedding table
   std::unordered_map<int64_t, uint32_t> count;    // persistent LFU count per key (R7)
-  std::set<std::pair<uint64_t, int64_t>> order;   // (policy primary, key) of residents
+  std::set<std::pair<uint64_t, int64_t>> order;   // (policy primary, key) of unpinned residents
+  int64_t npinned = 0;                            // light-LFU pinned residents
   // last lookup (L1-L3) — kept for the matching update (het_update contract)
   std::vector<int64_t> keys, uniq;
   std::vector<int32_t> inverse, perm, seg_off;
@@ -94,6 +100,7 @@ struct Worker {
 
 struct Oracle {
   int64_t R; uint32_t D; int64_t C; uint32_t s; int policy; int N; int lfu_persist;
+  uint32_t pin_thr = 0;    // light-LFU threshold theta (policy 2), R27
   uint64_t seed0; int64_t track_div;
   // server: global embedding table W (lazy rows) and global clocks c_g
   std::unordered_map<int64_t, std::vector<float>> W;
@@ -119,8 +126,11 @@ struct Oracle {
     return e.own_count;
   }
   uint64_t primary(Worker& wk, int64_t k, const Entry& e) {
-    return policy == 0 ? (uint64_t)lfu_count(wk, k, e) : (uint64_t)e.tick;
+    return policy == 1 ? (uint64_t)e.tick : (uint64_t)lfu_count(wk, k, e);   // 0 LFU, 2 light-LFU
   }
+  // light-LFU pin cap (R27): at most floor(C/2) pinned entries, so an
+  // overflow can always be evicted among the unpinned ones
+  int64_t pin_max() const { return C / 2; }
 
   // Server side of Cache.Evict(key): W += p, c_g = max(c_g, c_c)
   void server_apply(int64_t k, const std::vector<float>& p, uint32_t cc) {
@@ -191,23 +201,29 @@ struct Oracle {
         if (wk.status[u] == HIT) continue;
         int64_t k = wk.uniq[u];
         auto it = wk.cache.find(k);
-        if (it != wk.cache.end()) wk.order.erase({primary(wk, k, it->second), k});
+        if (it != wk.cache.end() && !it->second.pinned) wk.order.erase({primary(wk, k, it->second), k});
         Entry& e = wk.cache[k];
         if (tracked(k)) { e.v = Wrow(k); e.p.assign(D, 0.0f); }
         e.cs = e.cc = get_cg(k);
         if (wk.status[u] == MISS) e.own_count = 0;  // reset-LFU reading only
-        wk.order.insert({primary(wk, k, e), k});
+        if (!e.pinned) wk.order.insert({primary(wk, k, e), k});
       }
     }
     // L6: LFU count +1 per unique key per lookup, LRU tick = t (R7, R8)
     for (int i = 0; i < N; ++i) {
       Worker& wk = w[i];
-      for (int64_t k : wk.uniq) {
+      for (int64_t k : wk.uniq) {                  // ascending key
         Entry& e = wk.cache.at(k);
+        if (e.pinned) continue;                    // light-LFU: no frequency maintenance
         wk.order.erase({primary(wk, k, e), k});
         wk.count[k] += 1;
         e.own_count += 1;
         e.tick = (uint32_t)t;
+        if (policy == 2 && lfu_count(wk, k, e) >= pin_thr && wk.npinned < pin_max()) {
+          e.pinned = true;                         // direct access index
+          wk.npinned += 1;
+          continue;
+        }
         wk.order.insert({primary(wk, k, e), k});
       }
     }
@@ -264,7 +280,8 @@ struct Oracle {
     if (dirty) out.push_back({k, e.p, e.cc});
     wk.victims.push_back(k);
     wk.victim_dirty.push_back(dirty ? 1 : 0);
-    wk.order.erase({primary(wk, k, e), k});
+    if (e.pinned) wk.npinned -= 1;
+    else wk.order.erase({primary(wk, k, e), k});
     wk.cache.erase(k);
     wk.st[7] += 1; if (dirty) wk.st[8] += 1;
   }
@@ -318,6 +335,7 @@ struct Oracle {
         if (kv.second.cc > kv.second.cs) pushes[i].push_back({kv.first, kv.second.p, kv.second.cc});
       wk.cache.clear();
       wk.order.clear();
+      wk.npinned = 0;
       wk.have_lookup = false;
     }
     apply_pushes(pushes);
@@ -330,9 +348,10 @@ struct Oracle {
 extern "C" {
 
 void* orc_create(int64_t R, uint32_t D, int64_t C, uint32_t s, int policy, int N,
-                 int lfu_persist, uint64_t seed0, int64_t track_div) {
+                 int lfu_persist, uint64_t seed0, int64_t track_div, uint32_t pin_thr) {
   Oracle* o = new Oracle();
   o->R = R; o->D = D; o->C = C; o->s = s; o->policy = policy; o->N = N;
+  o->pin_thr = pin_thr;
   o->lfu_persist = lfu_persist; o->seed0 = seed0; o->track_div = track_div;
   o->w.resize(N);
   return o;
@@ -381,7 +400,7 @@ void orc_dump_cache(void* h, int i, int64_t* keys, float* v, float* p, uint32_t*
     if (cs) cs[j] = e.cs;
     if (cc) cc[j] = e.cc;
     if (count) count[j] = o->lfu_count(wk, kv.first, e);
-    if (tick) tick[j] = e.tick;
+    if (tick) tick[j] = e.pinned ? 0xFFFFFFFEu : e.tick;   // light-LFU: pinned marker
     ++j;
   }
 }

@@ -24,7 +24,9 @@ SRC = os.path.join(HERE, "het_oracle.cpp")
 LIB = os.path.join(HERE, "liboracle.so")
 
 S_INF = 0xFFFFFFFF
-LFU, LRU = 0, 1
+LFU, LRU, LIGHT_LFU = 0, 1, 2
+PIN_DEFAULT = 64        # light-LFU promotion threshold (R27)
+PINNED = 0xFFFFFFFE     # dump_cache()["tick"] of a pinned (direct-access) entry
 HIT, EXP1, EXP2, MISS = 0, 1, 2, 3
 INIT_SEED = 2112072210
 STAT_NAMES = ["lookups", "keys", "unique", "hits", "exp1", "exp2", "misses",
@@ -49,7 +51,7 @@ def _load():
         lib = ctypes.CDLL(build())
         P, I64, U32, U64, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
         lib.orc_create.restype = P
-        lib.orc_create.argtypes = [I64, U32, I64, U32, I, I, I, U64, I64]
+        lib.orc_create.argtypes = [I64, U32, I64, U32, I, I, I, U64, I64, U32]
         lib.orc_destroy.argtypes = [P]
         lib.orc_lookup.restype = I
         lib.orc_lookup.argtypes = [P, U64, P, P, P]
@@ -91,10 +93,15 @@ class Oracle:
     """N lock-step workers + the global table (one logical server)."""
 
     def __init__(self, R: int, D: int, C: int, s: int, policy: int = LFU, N: int = 1,
-                 lfu_persist: int = 1, seed0: int = INIT_SEED, track_div: int = 1):
+                 lfu_persist: int = 1, seed0: int = INIT_SEED, track_div: int = 1,
+                 pin_threshold: int = PIN_DEFAULT):
+        """policy: LFU, LRU or LIGHT_LFU (an entry whose count reaches
+        `pin_threshold` gets a direct access index -- pinned, no more count
+        maintenance, exempt from eviction; at most floor(C/2) pinned, R27)."""
         self.lib = _load()
         self.R, self.D, self.C, self.s, self.policy, self.N = R, D, C, s, policy, N
-        self.h = self.lib.orc_create(R, D, C, s, policy, N, lfu_persist, seed0, track_div)
+        self.h = self.lib.orc_create(R, D, C, s, policy, N, lfu_persist, seed0, track_div,
+                                     pin_threshold if policy == LIGHT_LFU else 0)
         self._n = [0] * N
 
     def __del__(self):

@@ -35,8 +35,13 @@ def init_value(seed0, key, d):
 
 
 class Brute:
-    def __init__(self, R, D, C, s, policy=0, N=1, lfu_persist=1, seed0=2112072210):
+    def __init__(self, R, D, C, s, policy=0, N=1, lfu_persist=1, seed0=2112072210, pin_thr=64):
+        """policy 0 LFU, 1 LRU, 2 light-LFU: a key whose LFU count
+        reaches pin_thr is pinned (no more count updates, never a victim),
+        keys taken in ascending order while fewer than C // 2 are pinned (R27)."""
         self.R, self.D, self.C, self.s, self.policy, self.N = R, D, C, s, policy, N
+        self.pin_thr = pin_thr
+        self.pinned = [set() for _ in range(N)]
         self.persist = lfu_persist
         self.seed0 = seed0
         self.W = {}      # key -> list of F32 (server rows, lazily initialised)
@@ -103,9 +108,13 @@ class Brute:
                                          own=old["own"] if (old and st != "MISS") else 0)
         for i in range(self.N):
             for k in self.logs[i]["uniq"]:
+                if k in self.pinned[i]:
+                    continue
                 self.counts[i][k] = self.counts[i].get(k, 0) + 1
                 self.caches[i][k]["own"] += 1
                 self.caches[i][k]["tick"] = t
+                if self.policy == 2 and self._prim(i, k) >= self.pin_thr and len(self.pinned[i]) < self.C // 2:
+                    self.pinned[i].add(k)
         outs = []
         for i in range(self.N):
             keys = self.logs[i]["keys"]
@@ -116,7 +125,7 @@ class Brute:
     # ---------------------------------------------------------------- write
     def _prim(self, i, k):
         e = self.caches[i][k]
-        if self.policy == 0:
+        if self.policy in (0, 2):
             return self.counts[i].get(k, 0) if self.persist else e["own"]
         return e["tick"]
 
@@ -140,6 +149,8 @@ class Brute:
             while len(self.caches[i]) > self.C:
                 best = None
                 for k in self.caches[i]:              # linear scan over all residents
+                    if k in self.pinned[i]:
+                        continue
                     key = (self._prim(i, k), k)
                     if best is None or key < best:
                         best = key
@@ -160,6 +171,7 @@ class Brute:
                 if e["cc"] > e["cs"]:
                     self._push(k, e["p"], e["cc"])
             self.caches[i] = {}
+            self.pinned[i] = set()
 
     def global_row(self, k):
         return np.array(self._row(k), dtype=np.float32), self.cg.get(k, 0)

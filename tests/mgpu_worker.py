@@ -27,14 +27,26 @@ def main():
     from paper_2112_07221_b200 import het
     obj = [het.het_get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    R, D, lr = 1000, 8, 0.01
-    cards = gen.cards_for("toy")
-    g = het.HetCache(R, D, frac, s, policy, rank=rank, world=world, unique_id=obj[0], max_keys_per_call=4096)
+    # shape: toy (BASELINE configs[0] rows, D=8), reddit (configs[2]: 232,965 ids,
+    # 14,208 distinct ids per worker-iteration -> the large-n exchange path),
+    # wide (Criteo-shaped fields over 5,000 rows with 4 KB rows, D=1024)
+    shape = sys.argv[5] if len(sys.argv) > 5 else "toy"
+    lr = 0.01
+    if shape == "reddit":
+        R, D, n_max = gen.REDDIT_ROWS, 128, 14208
+    elif shape == "wide":
+        R, D, n_max, cards = 5000, 1024, 4096, gen.scaled_cards(5000)
+    else:
+        R, D, n_max, cards = 1000, 8, 4096, gen.cards_for("toy")
+    g = het.HetCache(R, D, frac, s, policy, rank=rank, world=world, unique_id=obj[0], max_keys_per_call=n_max)
     o = Oracle(R=R, D=D, C=capacity(frac, R), s=s, policy=policy, N=world)
     for t in range(T):
-        keys = [gen.criteo_keys(i, t, 1, 128, cards)[0].numpy() for i in range(world)]
+        if shape == "reddit":
+            keys = [gen.reddit_keys(i, t, n_max).numpy() for i in range(world)]
+        else:
+            keys = [gen.criteo_keys(i, t, 1, 128, cards)[0].numpy() for i in range(world)]
         if t % 7 == 3:                        # ragged: some workers send fewer keys
-            keys = [k[: 100 * (i + 1)] for i, k in enumerate(keys)]
+            keys = [k[: (k.size // 33) * (i + 1)] for i, k in enumerate(keys)]
         grads = [gen.grads(i, t, k.size, D).numpy() for i, k in enumerate(keys)]
         kd = torch.from_numpy(keys[rank]).cuda()
         out = g.lookup(kd, t).cpu().numpy()
@@ -69,7 +81,7 @@ def main():
     g.close()
     dist.barrier()
     if rank == 0:
-        print(f"MGPU_OK world={world} policy={policy} s={s} frac={frac} exp2={os_['exp2']} "
+        print(f"MGPU_OK world={world} shape={shape} policy={policy} s={s} frac={frac} exp2={os_['exp2']} "
               f"evictions={os_['evictions']}", flush=True)
 
 

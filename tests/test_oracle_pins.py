@@ -13,7 +13,7 @@ import random
 import numpy as np
 import pytest
 
-from oracle.oracle import Oracle, S_INF, LFU, LRU, HIT, EXP1, EXP2, MISS, INIT_SEED
+from oracle.oracle import Oracle, S_INF, LFU, LRU, LIGHT_LFU, PINNED, HIT, EXP1, EXP2, MISS, INIT_SEED
 from brute import Brute, init_value
 
 F32 = np.float32
@@ -464,6 +464,91 @@ def test_brute_force_replay(seed):
     for k in range(R):
         br, bcg = b.global_row(k)
         assert np.array_equal(rows[k], br) and int(cg[k]) == bcg
+
+
+# ----------------------------------------------------------------------------- light-LFU (R27)
+@pytest.mark.parametrize("seed", range(24))
+def test_brute_force_replay_light_lfu(seed):
+    """P14 for light-LFU: oracle == brute force on random tiny traces with
+    small promotion thresholds (pins happen, the floor(C/2) cap binds)."""
+    rng = np.random.default_rng(1000 + seed)
+    R = int(rng.integers(2, 40))
+    D = int(rng.integers(1, 4))
+    N = int(rng.integers(1, 4))
+    s = [0, 1, 3, S_INF][int(rng.integers(0, 4))]
+    C = int(rng.integers(1, R + 1))
+    persist = int(rng.integers(0, 2))
+    thr = int(rng.integers(1, 5))
+    o = Oracle(R=R, D=D, C=C, s=s, policy=LIGHT_LFU, N=N, lfu_persist=persist, pin_threshold=thr)
+    b = Brute(R=R, D=D, C=C, s=s, policy=2, N=N, lfu_persist=persist, pin_thr=thr)
+    names = {HIT: "HIT", EXP1: "EXP1", EXP2: "EXP2", MISS: "MISS"}
+    pinned_seen = 0
+    for t in range(40):
+        ks = [list(rng.integers(0, R, size=rng.integers(0, 12))) for _ in range(N)]
+        gs = [rnd_grads(rng, len(k), D) for k in ks]
+        oo = o.lookup(t, ks)
+        bo = b.lookup(t, ks)
+        for i in range(N):
+            assert np.array_equal(oo[i], bo[i])
+            log = o.lookup_log(i)
+            assert [names[x] for x in log["status"].tolist()] == b.logs[i]["status"]
+        o.update(gs, LR)
+        b.update(gs, LR)
+        for i in range(N):
+            vk, vd = o.victims(i)
+            assert list(zip(vk.tolist(), vd.astype(bool).tolist())) == b.victims[i]
+            c = o.dump_cache(i)
+            pins = {k for k, tk in zip(c["keys"].tolist(), c["tick"].tolist()) if tk == PINNED}
+            assert pins == b.pinned[i] and len(pins) <= C // 2
+            pinned_seen += len(pins)
+            for j, k in enumerate(c["keys"].tolist()):
+                assert np.array_equal(c["v"][j], np.array(b.caches[i][k]["v"], np.float32))
+                assert int(c["count"][j]) == (b.counts[i].get(k, 0) if persist else b.caches[i][k]["own"])
+    o.flush()
+    b.flush()
+    rows, cg = o.read_global(np.arange(R))
+    for k in range(R):
+        br, bcg = b.global_row(k)
+        assert np.array_equal(rows[k], br) and int(cg[k]) == bcg
+    if C >= 2:
+        assert pinned_seen > 0
+
+
+def test_light_lfu_three_gets_promote():
+    """SPEC S:289 vector: LightLFU threshold=3 -- three gets promote the entry;
+    a pinned entry is never a victim and its count stops."""
+    o = Oracle(R=10, D=1, C=2, s=S_INF, policy=LIGHT_LFU, pin_threshold=3)
+    for t in range(3):
+        o.lookup(t, [[5]])
+        o.update(None, LR)
+        c = o.dump_cache(0)
+        assert (int(c["tick"][0]) == PINNED) == (t == 2)
+    # keys 1 and 2 have count 1 < count(5) = 3 but 5 is pinned: the overflow
+    # victims are chosen among the unpinned only, smallest (count, key) first
+    for t in range(3, 6):
+        o.lookup(t, [[5, 1, 2]])
+        o.update(None, LR)
+    c = o.dump_cache(0)
+    assert 5 in c["keys"].tolist()
+    assert int(c["count"][c["keys"].tolist().index(5)]) == 3      # no maintenance after the pin
+
+
+def test_light_lfu_miss_rate_close_to_lfu():
+    """light-LFU's miss rate stays within 2 percentage points of
+    exact LFU on the same Zipf trace (P:632 'similar miss rate')."""
+    from workload import gen
+    cards = gen.scaled_cards(20000)
+    rates = {}
+    for pol in (LFU, LIGHT_LFU):
+        o = Oracle(R=20000, D=0, C=2000, s=S_INF, policy=pol, pin_threshold=64)
+        for t in range(400):
+            o.lookup(t, [gen.criteo_keys(0, t, 1, 128, cards)[0].numpy()], want_out=False)
+            o.update(None, LR)
+            if t == 199:
+                s0 = o.stats(0)
+        s1 = o.stats(0)
+        rates[pol] = (s1["misses"] - s0["misses"]) / (s1["unique"] - s0["unique"])
+    assert abs(rates[LFU] - rates[LIGHT_LFU]) <= 0.02, rates
 
 
 # ----------------------------------------------------------------------------- init (R14)

@@ -212,18 +212,18 @@ def reddit_keys(i: int, t: int, K: int, R: int = REDDIT_ROWS, alpha: float = 1.0
                 seed: int = SEED, device="cpu", chunk: int = 16384) -> torch.Tensor:
     """K distinct node ids for worker i, iteration t (draw order kept)."""
     assert K <= R
-    seen = torch.zeros(R, dtype=torch.bool)
+    seen = torch.zeros(R, dtype=torch.bool, device=device)
     got = []
     have = 0
     j0 = 0
     while have < K:
-        j = torch.arange(j0, j0 + chunk, dtype=torch.int64)
+        j = torch.arange(j0, j0 + chunk, dtype=torch.int64, device=device)
         j0 += chunk
         ids = permute(zipf_rank(uniform(stream(seed, i, t, j)), R, alpha), R, 0xEDD17)
         # first occurrence within the chunk, in draw order
         uniq, inv = torch.unique(ids, return_inverse=True)
-        first = torch.full((uniq.numel(),), chunk, dtype=torch.int64)
-        first.scatter_reduce_(0, inv, torch.arange(chunk, dtype=torch.int64), reduce="amin")
+        first = torch.full((uniq.numel(),), chunk, dtype=torch.int64, device=device)
+        first.scatter_reduce_(0, inv, torch.arange(chunk, dtype=torch.int64, device=device), reduce="amin")
         order = torch.sort(first).values
         cand = ids[order]
         cand = cand[~seen[cand]]
@@ -231,7 +231,7 @@ def reddit_keys(i: int, t: int, K: int, R: int = REDDIT_ROWS, alpha: float = 1.0
         seen[cand] = True
         got.append(cand)
         have += cand.numel()
-    return torch.cat(got).to(device)
+    return torch.cat(got)
 
 
 def grads(i: int, t: int, n: int, D: int, seed: int = SEED, device="cpu") -> torch.Tensor:
