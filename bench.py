@@ -172,6 +172,8 @@ def algorithmic_bytes(kernel, s, D, n_steps, resident):
         return U * (8 + 12 + 8 + 4 + 8 + 4 + 5)  # key, one slot, clocks, c_g, count r/w, prim, status+entry
     if kernel == "sync_fetch":
         return (m + v) * (2 * row + 8) + v * 2 * row   # W read + v write (+ p read, W write for syncs)
+    if kernel == "exchange":          # N > 1 per-phase round: the local HBM side, as sync_fetch
+        return algorithmic_bytes("sync_fetch", s, D, n_steps, resident)
     if kernel == "gather":
         return U * row + n * row + 4 * n + 4 * U
     if kernel == "segreduce_apply":
@@ -338,6 +340,7 @@ def run_gpu(args):
     het.het_profile_enable(cache.h, False)
     p1 = cache.stats()
     pd = {k: p1[k] - p0[k] for k in sd}
+    wire = {k: (p1[k] - p0[k]) / K for k in ("bytes_clock_tx", "bytes_emb_tx", "bytes_clock_rx", "bytes_emb_rx")}
     resident = p1["resident"]
     hbm, peak_kind = peaks()
     kern = {}
@@ -408,6 +411,7 @@ def run_gpu(args):
         "ms_per_step_stream_launch": ms_stream,
         "roofline": roof,
         "kernels": kern,
+        "nvlink": nvlink_fraction(kern, wire, world, device) if world > 1 else None,
         "clocks": clocks,
         "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": n * 8 + n * D * 4, "d2h_bytes_per_step": n * D * 4},
@@ -421,6 +425,34 @@ def run_gpu(args):
     if rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(args)
     return line, rank, world
+
+
+def nvlink_fraction(kern, wire, world, device):
+    """SURVEY §8(d) %NVLink: exchange payload bytes each GPU sends per step
+    (records + rows, device-counted) / the exchange kernel's mean time, against
+    an NCCL all-to-all of 64 MB per GPU timed here (per-direction bytes to
+    peers / time) and against 900 GB/s nominal."""
+    ex = kern.get("exchange_fused") or kern.get("exchange")
+    if not ex:
+        return None
+    n = 64 << 20
+    a = torch.empty(n // 4, dtype=torch.float32, device=device)
+    b = torch.empty_like(a)
+    for _ in range(3):
+        torch.distributed.all_to_all_single(b, a)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        torch.distributed.all_to_all_single(b, a)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 10 * 1e-3
+    peak = n * (world - 1) / world / t / 1e9
+    sent = wire["bytes_clock_tx"] + wire["bytes_emb_tx"]
+    ach = sent / (ex["ms_per_launch"] * 1e-3) / 1e9
+    return {"bytes_sent_per_gpu_step": sent, "exchange_ms": ex["ms_per_launch"], "achieved_GBs": ach,
+            "nccl_alltoall_64MB_GBs": peak, "frac": ach / peak, "frac_of_900_nominal": ach / 900.0}
 
 
 def run_sweep(het, device):

@@ -44,7 +44,12 @@ extern "C" {
 typedef struct het_cache* het_cache_t;     /* opaque; the library owns all table/cache/hash/comm state */
 typedef struct CUstream_st* het_stream_t;  /* == cudaStream_t */
 
-typedef enum { HET_LFU = 0, HET_LRU = 1 } het_policy_t;
+/* HET_LIGHT_LFU ("a light-weighted version of LFU"): an entry whose LFU
+ * count reaches opts.pin_threshold (default 64) gets a direct
+ * access index -- pinned: no more count maintenance, never an overflow victim
+ * (S:275); never demoted.  Promotions go in ascending key order while
+ * fewer than floor(C/2) entries are pinned (reading R27). */
+typedef enum { HET_LFU = 0, HET_LRU = 1, HET_LIGHT_LFU = 2 } het_policy_t;
 
 typedef enum {
   HET_OK = 0,
@@ -73,6 +78,7 @@ typedef struct {
   uint64_t init_seed;          /* seed of the initial table W0 (R14); 0 = default 2112072210 */
   int lfu_persist;             /* 1 (default): LFU counts persist across evictions (R7); 0: reset */
   int debug_log;               /* reserved */
+  uint32_t pin_threshold;      /* HET_LIGHT_LFU promotion count; 0 = default 64 */
 } het_opts_t;
 
 typedef struct {
@@ -81,6 +87,7 @@ typedef struct {
   uint64_t launches;           /* kernels launched by the library so far */
   uint32_t resident, capacity; /* |cache| and C */
   int sticky_error;            /* het_status_t latched on the device, 0 = none */
+  uint32_t pinned;             /* HET_LIGHT_LFU: pinned (direct-access) entries */
 } het_stats_t;
 
 /* ncclUniqueId (128 bytes) for multi-GPU bootstrap; call on rank 0, broadcast. */
@@ -91,7 +98,7 @@ het_status_t het_get_unique_id(void* out128);
  *   D          embedding dimension, multiple of 4
  *   cache_frac C = floor(cache_frac * R) cache entries per worker (R10); 0 = no cache
  *   s          staleness threshold, HET_S_INF = infinity
- *   policy     LFU or LRU eviction
+ *   policy     LFU, LRU or light-LFU eviction
  *   dist       NULL for a single worker, else rank/world/ncclUniqueId
  *   opt        NULL for defaults (n_max = 65536)
  * Allocates everything up front (no allocation on the hot path) and writes

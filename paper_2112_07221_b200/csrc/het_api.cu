@@ -174,6 +174,7 @@ __global__ void k_evict_keys_local(Dev s, Call c) {
       warp_erase(s, key, lane);
       if (lane == 0) {
         if (s.policy == 0) lfu_move(s, key, s.eprim[e], EP_FREE, dpop);
+        unpin_count(s, s.eprim[e]);
         s.eprim[e] = EP_FREE;
         s.ekey[e] = -1;
         s.fstack[atomicAdd(&ctl->ftop, 1)] = e;
@@ -247,7 +248,7 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   *out = nullptr;
   if (rows == 0 || rows > (1ull << 32) || D == 0 || (D % 4) != 0 || D > (1u << 16)) return HET_ERR_ARG;
   if (!(cache_frac >= 0.0 && cache_frac <= 1.0)) return HET_ERR_ARG;
-  if (policy != HET_LFU && policy != HET_LRU) return HET_ERR_ARG;
+  if (policy != HET_LFU && policy != HET_LRU && policy != HET_LIGHT_LFU) return HET_ERR_ARG;
   int rank = 0, world = 1;
   if (dist) {
     rank = dist->rank;
@@ -267,7 +268,9 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   d.D = D;
   d.C = h->C;
   d.s = s;
-  d.policy = (int)policy;
+  d.policy = policy == HET_LRU ? 1 : 0;   // light-LFU is LFU plus pinning (R27)
+  d.pin_thr = policy == HET_LIGHT_LFU ? ((opt && opt->pin_threshold) ? opt->pin_threshold : 64u) : 0u;
+  d.pin_max = h->C / 2;
   d.lfu_persist = opt ? (opt->lfu_persist != 0) : 1;
   if (!opt) d.lfu_persist = 1;
   d.rank = rank;
@@ -309,7 +312,7 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   d.nbk = ((int64_t)rows + (1 << LFU_BLK_SHIFT) - 1) >> LFU_BLK_SHIFT;
   d.nbk2 = (d.nbk + 63) >> 6;
   d.lfu_cb = 0;
-  if (policy == HET_LFU) {  // count bitmaps, bounded to ~1 GB
+  if (policy != HET_LRU) {  // count bitmaps, bounded to ~1 GB
     int cb = LFU_CB_MAX;
     while (cb > 2 && (double)cb * d.bm_words * 4 > 1.0e9) cb >>= 1;
     d.lfu_cb = cb;
@@ -322,6 +325,8 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   A(d.pop, LFU_CB_MAX);
   A(d.ctl, 1);
   A(d.cnt, C_NUM);
+  A(d.pin_k, d.pin_thr ? h->n_max : 1);
+  A(d.pin_e, d.pin_thr ? h->n_max : 1);
   {
     Call& c = h->call;
     uint32_t nm = h->n_max;
@@ -417,11 +422,18 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
   c.t = clock_t;
   c.keys = keys;
   Dev& d = h->d;
-  h->fused = fused_ok(d, (int)n) && !getenv("HET_NO_FUSED") && (d.world == 1 || mgpu_p2p(h->mg));
+  // fused path: N = 1 up to FUSED_LOOKUP_MAX keys (beyond, the large-batch
+  // per-phase kernels with the sliced heavy-key segment reduce), N > 1 over
+  // the peer-memory exchange for every n; the dedup kernel follows n
+  h->fused = !getenv("HET_NO_FUSED") && (d.world == 1 ? (int)n <= FUSED_LOOKUP_MAX : mgpu_p2p(h->mg) != nullptr);
   if (h->fused) {
-    {
+    if (fused_ok(d, (int)n)) {
       Prof p(h, "dedup", st);
       h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st);
+    } else {
+      launch_begin(d, clock_t, (int)n, st);
+      Prof p(h, "dedup", st);
+      h->launches += 1 + launch_dedup(c, (int)n, d.R, h->pbits, d.ctl, st);
     }
     if (d.world == 1) {
       Prof p(h, "lookup_fused", st);
@@ -458,6 +470,7 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
       h->launches += 1;
     }
   }
+  if (d.pin_thr) h->launches += launch_pin_apply(d, st);   // light-LFU promotions of this lookup
   if (out_host) CUDA_TRY(h, cudaMemcpyAsync(out, dout, (size_t)n * h->D * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaGetLastError());
   h->have_lookup = true;
@@ -618,6 +631,7 @@ het_status_t het_stats(het_cache_t h, het_stats_t* out) {
   out->resident = (uint32_t)(h->d.Ecap - ctl.ftop);
   out->capacity = (uint32_t)h->C;
   out->sticky_error = ctl.err;
+  out->pinned = (uint32_t)ctl.npinned;
   return HET_OK;
 }
 

@@ -21,6 +21,7 @@ constexpr uint32_t S_INF = 0xFFFFFFFFu;
 constexpr int64_t HK_EMPTY = -1;
 constexpr int64_t HK_TOMB = -2;
 constexpr uint32_t EP_FREE = 0xFFFFFFFFu;  // eprim of a free entry
+constexpr uint32_t EP_PIN = 0xFFFFFFFEu;   // eprim of a light-LFU pinned entry (R27): never a victim
 constexpr int LFU_CB_MAX = 16;             // LFU count values kept in key bitmaps
 constexpr int LFU_BLK_SHIFT = 12;          // 4096 keys per bitmap block counter
 
@@ -80,6 +81,10 @@ struct Ctl {
   int32_t pad2_;
   // segment reduce (large batches): heavy keys per size bucket floor(log2(count))
   int32_t nbucket[32];
+  // light-LFU (R27): promotion candidates of the current lookup, pinned entries
+  int32_t npin_cand;
+  int32_t pad7_;
+  int64_t npinned;
 };
 
 struct Dev {
@@ -100,7 +105,24 @@ struct Dev {
   // key is resident with count c < lfu_cb; bcnt = set bits per 4096-key block
   int lfu_cb; int64_t bm_words; int64_t nbk; int64_t nbk2;
   uint32_t* bm; uint32_t* bcnt; uint32_t* bcnt2; int32_t* pop;   // bcnt2: per 64 blocks
+  // light-LFU (R27): promotion threshold (0 = off), cap floor(C/2),
+  // candidates (key, entry) of the current lookup, applied by k_pin_apply
+  uint32_t pin_thr; int64_t pin_max; int64_t* pin_k; int32_t* pin_e;
 };
+
+// light-LFU touch (lane 0 of the key's warp): an entry that just reached the
+// threshold becomes a promotion candidate; k_pin_apply pins the candidates in
+// ascending key order while fewer than pin_max entries are pinned
+__device__ __forceinline__ void unpin_count(const Dev& s, uint32_t prim) {   // a pinned entry leaves the cache
+  if (prim == EP_PIN) atomicAdd(reinterpret_cast<unsigned long long*>(&s.ctl->npinned), ~0ull);
+}
+__device__ __forceinline__ void pin_candidate(const Dev& s, int64_t key, int32_t e, uint32_t newc) {
+  if (s.pin_thr && newc >= s.pin_thr && newc != EP_PIN && newc != EP_FREE) {
+    const int i = atomicAdd(&s.ctl->npin_cand, 1);
+    s.pin_k[i] = key;
+    s.pin_e[i] = e;
+  }
+}
 
 // Per-call scratch (sized by n_max at create)
 struct Call {
@@ -344,6 +366,8 @@ int launch_evict_apply_local(const Dev& s, void* evbuf, cudaStream_t st);
 void launch_hash_rebuild(const Dev& s, cudaStream_t st);
 // fused single-GPU step (k_fused.cu)
 bool fused_ok(const Dev& s, int n);
+int launch_pin_apply(const Dev& s, cudaStream_t st);
+constexpr int FUSED_LOOKUP_MAX = 16384;   // N = 1: fused lookup/update up to this n
 int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st);
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st);
 // SMs left free by the cooperative kernels for NCCL's blocks at N > 1

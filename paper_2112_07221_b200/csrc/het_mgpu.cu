@@ -321,7 +321,7 @@ __global__ void k_install(Dev s, Call c, MgpuState m_) {
           s.ekey[e] = key;
           uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
           s.eprim[e] = prim;
-          if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
+          if (s.policy == 0) { lfu_move(s, key, EP_FREE, prim, dpop); pin_candidate(s, key, e, prim); }
           atomicMin(&ctl->min_install, prim);
           c.uentry[u] = e;
         }
@@ -398,6 +398,7 @@ __global__ void k_build_pushes(Dev s, Call c, MgpuState m_, const int64_t* vsel,
       atomicAdd(&ctl->n_tomb, 1);
       if (mode == 0) { vkeys[i] = key; vdirty[i] = dirty ? 1 : 0; }
       if (s.policy == 0) lfu_move(s, key, prim, EP_FREE, dpop);
+      unpin_count(s, prim);
       s.eprim[e] = EP_FREE;
       s.ekey[e] = -1;
       s.fstack[atomicAdd(&ctl->ftop, 1)] = e;

@@ -43,6 +43,22 @@ namespace het {
 
 namespace cg = cooperative_groups;
 
+// Row moves of one warp in batches of RB float4 per lane: the loads of a batch
+// are issued before its stores, so wide rows (D = 4096: 32 float4 per lane)
+// take D/(128*RB) memory round trips instead of D/128.
+constexpr int RB = 4;
+__device__ __forceinline__ void warp_copy_row(float4* dst, const float4* src, int D4, int lane) {
+  for (int d0 = lane; d0 < D4; d0 += 32 * RB) {
+    float4 t[RB];
+#pragma unroll
+    for (int b = 0; b < RB; ++b)
+      if (d0 + 32 * b < D4) t[b] = src[d0 + 32 * b];
+#pragma unroll
+    for (int b = 0; b < RB; ++b)
+      if (d0 + 32 * b < D4) dst[d0 + 32 * b] = t[b];
+  }
+}
+
 #ifdef HET_TIMELINE
 constexpr int PTLW = 8192;
 __device__ unsigned long long g_ptl[16 * PTLW];
@@ -95,9 +111,8 @@ __global__ void k_p2p_build(Dev s, Call c, P2P m, int drain) {
       if (dirty) atomicAdd(&sb[2], 4ull * s.D);
     }
     if (dirty) {
-      const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
-      float4* dst = reinterpret_cast<float4*>(reqrow(m, o, m.rank, j));
-      for (int d = lane; d < D4; d += 32) dst[d] = pr[d];
+      warp_copy_row(reinterpret_cast<float4*>(reqrow(m, o, m.rank, j)),
+                    reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D), D4, lane);
     }
   }
   __syncthreads();
@@ -110,8 +125,7 @@ __global__ void k_p2p_build(Dev s, Call c, P2P m, int drain) {
     f->pushes = (uint32_t)m.c3cnt[o];
     __threadfence_system();
     st_release(&f->epoch, ep);
-    m.c3cnt[o] = 0;
-    m.lcnt[o] = 0;
+    m.c3cnt[o] = 0;     // lcnt stays: k_p2p_install reads it, its last block zeroes it
   }
   if (threadIdx.x == 0) m.done[0] = 0;
 }
@@ -238,9 +252,10 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
     const unsigned needrow = (pushm | syncm);
     const unsigned answer = __ballot_sync(0xffffffffu, req && !valid);
     float4* Wr = reinterpret_cast<float4*>(s.W + row * s.D);
-    for (int d = lane; d - lane < D4; d += 32) {
-      const bool act = d < D4;
-      float4 w = act ? Wr[d] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int d0 = lane; d0 - lane < D4; d0 += 32 * RB) {   // RB columns per lane per pass (wide rows)
+      float4 w[RB];
+#pragma unroll
+      for (int b = 0; b < RB; ++b) w[b] = d0 + 32 * b < D4 ? Wr[d0 + 32 * b] : make_float4(0.f, 0.f, 0.f, 0.f);
       for (int pass = 0; pass < 2; ++pass) {
         unsigned mm = pass == 0 ? pushm : syncm;
         while (mm) {
@@ -248,16 +263,26 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
           mm &= mm - 1;
           const int si = __shfl_sync(0xffffffffu, src, i);
           const int64_t ji = __shfl_sync(0xffffffffu, j, i);
-          if (act) w = f4add_p(w, reinterpret_cast<const float4*>(reqrow(m, m.rank, si, ji))[d]);
+          const float4* rr = reinterpret_cast<const float4*>(reqrow(m, m.rank, si, ji));
+          float4 x[RB];
+#pragma unroll
+          for (int b = 0; b < RB; ++b) if (d0 + 32 * b < D4) x[b] = rr[d0 + 32 * b];
+#pragma unroll
+          for (int b = 0; b < RB; ++b) if (d0 + 32 * b < D4) w[b] = f4add_p(w[b], x[b]);
         }
       }
-      if (act && needrow) Wr[d] = w;
+      if (needrow) {
+#pragma unroll
+        for (int b = 0; b < RB; ++b) if (d0 + 32 * b < D4) Wr[d0 + 32 * b] = w[b];
+      }
       unsigned am = answer;
       while (am) {
         const int i = __ffs(am) - 1;
         am &= am - 1;
         float* rec = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rec_l), i));
-        if (act) reinterpret_cast<float4*>(rec + 4)[d] = w;
+#pragma unroll
+        for (int b = 0; b < RB; ++b)
+          if (d0 + 32 * b < D4) reinterpret_cast<float4*>(rec + 4)[d0 + 32 * b] = w[b];
       }
     }
     __syncwarp();
@@ -334,16 +359,15 @@ __global__ void k_p2p_install(Dev s, Call c, P2P m) {
             s.ekey[e] = key;
             const uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
             s.eprim[e] = prim;
-            if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
+            if (s.policy == 0) { lfu_move(s, key, EP_FREE, prim, dpop); pin_candidate(s, key, e, prim); }
             atomicMin(&ctl->min_install, prim);
             c.uentry[u] = e;
           }
         } else {
           e = c.uentry[u];
         }
-        const float4* src = reinterpret_cast<const float4*>(rec + 4);
-        float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
-        for (int d = lane; d < D4; d += 32) vr[d] = src[d];
+        warp_copy_row(reinterpret_cast<float4*>(s.v + (int64_t)e * s.D), reinterpret_cast<const float4*>(rec + 4),
+                      D4, lane);
         if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
       }
     }
@@ -356,6 +380,7 @@ __global__ void k_p2p_install(Dev s, Call c, P2P m) {
     if (bc[1]) atomicAdd(&s.cnt[C_EXP2], (unsigned long long)bc[1]);
   }
   if (!last_block(&m.done[2])) return;
+  if (threadIdx.x < m.N) m.lcnt[threadIdx.x] = 0;   // every block read it at entry; zero for the next round
   if (threadIdx.x == 0) { *m.epoch = ep; m.done[2] = 0; }
 }
 
@@ -399,9 +424,8 @@ __global__ void k_p2p_pushes(Dev s, P2P m, EvView b) {
         reqrec(m, o, m.rank)[ps] = r;
         atomicAdd(&sb[2], 16ull + 4ull * s.D);
       }
-      const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
-      float4* dst = reinterpret_cast<float4*>(reqrow(m, o, m.rank, ps));
-      for (int d = lane; d < D4; d += 32) dst[d] = pr[d];
+      warp_copy_row(reinterpret_cast<float4*>(reqrow(m, o, m.rank, ps)),
+                    reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D), D4, lane);
     }
     if (lane == 0) {
       s.hkey[slot] = HK_TOMB;
@@ -409,6 +433,7 @@ __global__ void k_p2p_pushes(Dev s, P2P m, EvView b) {
       b.vkeys[i] = key;
       b.vdirty[i] = dirty ? 1 : 0;
       if (s.policy == 0) lfu_move(s, key, prim, EP_FREE, dpop);
+      unpin_count(s, prim);
       s.eprim[e] = EP_FREE;
       s.ekey[e] = -1;
       s.fstack[atomicAdd(&ctl->ftop, 1)] = e;
@@ -444,16 +469,20 @@ __device__ __forceinline__ void probe_build_key(const Dev& s, const Call& c, con
   if (e >= 0) { ecs = s.cs[e]; ecc = s.cc[e]; }
   uint8_t st = ST_MISS;
   if (lane == 0) {
-    if (s.lfu_persist) { cntk += 1; s.count_by_key[key] = cntk; }
+    const uint32_t oldc = (e >= 0 && s.policy == 0) ? s.eprim[e] : 0u;
+    const bool pinned = oldc == EP_PIN;                    // light-LFU: no frequency maintenance
+    if (s.lfu_persist && !pinned) { cntk += 1; s.count_by_key[key] = cntk; }
     if (e >= 0) {
       if (s.s == S_INF) st = ST_HIT;                       // R4
       else if (ecc - ecs > s.s) st = ST_EXP1;              // cond (1)
       else st = ST_NEEDQ;                                  // cond (2) at the owner
       if (s.policy == 0) {
-        uint32_t oldc = s.eprim[e];
-        uint32_t newc = s.lfu_persist ? cntk : oldc + 1;
-        s.eprim[e] = newc;
-        lfu_move(s, key, oldc, newc, dpop);
+        if (!pinned) {
+          uint32_t newc = s.lfu_persist ? cntk : oldc + 1;
+          s.eprim[e] = newc;
+          lfu_move(s, key, oldc, newc, dpop);
+          pin_candidate(s, key, e, newc);
+        }
       } else {
         s.eprim[e] = (uint32_t)ctl->t_cur;
       }
@@ -482,11 +511,9 @@ __device__ __forceinline__ void probe_build_key(const Dev& s, const Call& c, con
       atomicAdd(&sb[st == ST_NEEDQ ? 0 : 2], 16ull);
       if (dirty) atomicAdd(&sb[2], 4ull * s.D);
     }
-    if (dirty) {
-      const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
-      float4* dst = reinterpret_cast<float4*>(reqrow(m, o, m.rank, j));
-      for (int d = lane; d < D4; d += 32) dst[d] = pr[d];
-    }
+    if (dirty)
+      warp_copy_row(reinterpret_cast<float4*>(reqrow(m, o, m.rank, j)),
+                    reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D), D4, lane);
   }
 }
 
@@ -581,16 +608,15 @@ __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, 
             s.ekey[e] = key;
             const uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
             s.eprim[e] = prim;
-            if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
+            if (s.policy == 0) { lfu_move(s, key, EP_FREE, prim, dpop); pin_candidate(s, key, e, prim); }
             atomicMin(&ctl->min_install, prim);
             c.uentry[u] = e;
           }
         }
       }
       if (ok) {
-        const float4* src = reinterpret_cast<const float4*>(rec + 4);
-        float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
-        for (int d = lane; d < D4; d += 32) vr[d] = src[d];
+        warp_copy_row(reinterpret_cast<float4*>(s.v + (int64_t)e * s.D), reinterpret_cast<const float4*>(rec + 4),
+                      D4, lane);
         if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
       }
     }
@@ -598,14 +624,18 @@ __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, 
   if (ok && e >= 0) {
     const float4* vr = reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D);
     float4* o4 = reinterpret_cast<float4*>(out);
-    for (int d = lane; d - lane < D4; d += 32) {
-      float4 val = d < D4 ? vr[d] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int d0 = lane; d0 - lane < D4; d0 += 32 * RB) {
+      float4 val[RB];
+#pragma unroll
+      for (int b = 0; b < RB; ++b) val[b] = d0 + 32 * b < D4 ? vr[d0 + 32 * b] : make_float4(0.f, 0.f, 0.f, 0.f);
       for (int kb = 0; kb < cnt; kb += 32) {
         const int srcp = kb == 0 ? pos_lane : (kb + lane < cnt ? c.perm[j0 + kb + lane] : 0);
         const int mm = min(32, cnt - kb);
         for (int k = 0; k < mm; ++k) {
           const int pos = __shfl_sync(0xffffffffu, srcp, k);
-          if (d < D4) __stcs(o4 + (int64_t)pos * D4 + d, val);
+#pragma unroll
+          for (int b = 0; b < RB; ++b)
+            if (d0 + 32 * b < D4) __stcs(o4 + (int64_t)pos * D4 + d0 + 32 * b, val[b]);
         }
       }
     }

@@ -46,6 +46,8 @@ __global__ void k_reset_cache(Dev s) {
   if (i0 == 0) {
     s.ctl->ftop = (int32_t)s.Ecap;
     s.ctl->n_tomb = 0;
+    s.ctl->npinned = 0;      // light-LFU: the cache is empty
+    s.ctl->npin_cand = 0;
     s.ctl->T_last = 0;
     s.ctl->min_install = 0xFFFFFFFFu;
   }
@@ -96,7 +98,9 @@ k_probe(Dev s, Call c) {
     gpre = __shfl_sync(0xffffffffu, gpre, 1);
     if (lane == 0) {
       uint8_t st;
-      if (s.lfu_persist) { cnt += 1; s.count_by_key[key] = cnt; }
+      const uint32_t oldc = (e >= 0 && s.policy == 0) ? s.eprim[e] : 0u;
+      const bool pinned = oldc == EP_PIN;            // light-LFU: no frequency maintenance
+      if (s.lfu_persist && !pinned) { cnt += 1; s.count_by_key[key] = cnt; }
       if (e < 0) {
         st = ST_MISS;
       } else {
@@ -109,10 +113,12 @@ k_probe(Dev s, Call c) {
         } else st = ST_NEEDQ;                               // ask the owner (C1)
         // L6: LFU count +1 / LRU tick = t for resident entries
         if (s.policy == 0) {
-          uint32_t oldc = s.eprim[e];
-          uint32_t newc = s.lfu_persist ? cnt : oldc + 1;
-          s.eprim[e] = newc;
-          lfu_move(s, key, oldc, newc, dpop);
+          if (!pinned) {
+            uint32_t newc = s.lfu_persist ? cnt : oldc + 1;
+            s.eprim[e] = newc;
+            lfu_move(s, key, oldc, newc, dpop);
+            pin_candidate(s, key, e, newc);
+          }
         } else {
           s.eprim[e] = (uint32_t)ctl->t_cur;
         }
@@ -212,7 +218,7 @@ k_sync_fetch_local(Dev s, Call c) {
         if (lane == 0) {
           s.ekey[e] = key;
           s.eprim[e] = prim;
-          if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
+          if (s.policy == 0) { lfu_move(s, key, EP_FREE, prim, dpop); pin_candidate(s, key, e, prim); }
           c.uentry[u] = e;
         }
       }

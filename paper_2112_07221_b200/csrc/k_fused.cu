@@ -353,16 +353,21 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
     uint32_t ecs = 0, ecc = 0;
     if (e >= 0) { ecs = s.cs[e]; ecc = s.cc[e]; }
     if (lane == 0) {
-      if (s.lfu_persist) { cntk += 1; s.count_by_key[key] = cntk; }
+      // light-LFU: a pinned entry skips the frequency maintenance
+      const uint32_t oldc = (e >= 0 && s.policy == 0) ? s.eprim[e] : 0u;
+      const bool pinned = oldc == EP_PIN;
+      if (s.lfu_persist && !pinned) { cntk += 1; s.count_by_key[key] = cntk; }
       if (e >= 0) {
         if (s.s == S_INF) st = ST_HIT;                       // R4
         else if (ecc - ecs > s.s) st = ST_EXP1;              // cond (1)
         else st = (gpre <= ecc || gpre - ecc <= s.s) ? ST_HIT : ST_EXP2;   // cond (2)
         if (s.policy == 0) {                                 // L6
-          uint32_t oldc = s.eprim[e];
-          uint32_t newc = s.lfu_persist ? cntk : oldc + 1;
-          s.eprim[e] = newc;
-          lfu_move(s, key, oldc, newc, dpop);
+          if (!pinned) {
+            uint32_t newc = s.lfu_persist ? cntk : oldc + 1;
+            s.eprim[e] = newc;
+            lfu_move(s, key, oldc, newc, dpop);
+            pin_candidate(s, key, e, newc);
+          }
         } else {
           s.eprim[e] = (uint32_t)ctl->t_cur;
         }
@@ -396,7 +401,7 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
             s.ekey[e] = key;
             uint32_t prim = s.policy == 0 ? (s.lfu_persist ? cntk : 1u) : (uint32_t)ctl->t_cur;
             s.eprim[e] = prim;
-            if (s.policy == 0) lfu_move(s, key, EP_FREE, prim, dpop);
+            if (s.policy == 0) { lfu_move(s, key, EP_FREE, prim, dpop); pin_candidate(s, key, e, prim); }
             atomicMin(&ctl->min_install, prim);
           }
         }
@@ -440,6 +445,139 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
   }
 }
 
+// ------------------------------------------------------------------ K_look, wide rows
+// D >= 1024 (BASELINE configs[4], D = 4096: 16 KB rows): G = D/512 warps per
+// unique key (up to the 8 warps of the block).  The group's first warp takes
+// every decision of k_lookup_fused (Find, CheckValid, touch, sync push clock,
+// install allocation); after a block barrier the G warps move the row bytes,
+// each its own 512-column slice: the Evict push W += p, the Fetch v = W and
+// the Get scatter to every occurrence.  Same semantics, same order per column.
+struct LkMeta { int64_t key; int32_t e; int32_t j0; int32_t cnt; uint32_t g; uint8_t st; uint8_t push; };
+
+__global__ void __launch_bounds__(LK_WARPS * 32)
+k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
+  __shared__ unsigned bc[4];
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ LkMeta meta[LK_WARPS];
+  if (threadIdx.x < 4) bc[threadIdx.x] = 0;
+  dpop_init(dpop);
+  __syncthreads();
+  Ctl* ctl = s.ctl;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int grp = wib / G, gw = wib % G;
+  const int u = blockIdx.x * (LK_WARPS / G) + grp;
+  const int U = ctl->U;
+  const bool live = !ctl->abort && u < U;
+  if (live && gw == 0) {
+    const int64_t key = c.uniq[u];
+    const int j0 = c.seg_off[u], cnt = c.seg_off[u + 1] - j0;
+    uint32_t cntk = 0, gpre = 0;
+    if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
+    if (lane == 1 && s.s != S_INF) gpre = s.cg[key];
+    int32_t e = warp_find(s, key, lane);
+    gpre = __shfl_sync(0xffffffffu, gpre, 1);
+    uint8_t st = ST_MISS;
+    uint32_t ecs = 0, ecc = 0;
+    if (e >= 0) { ecs = s.cs[e]; ecc = s.cc[e]; }
+    if (lane == 0) {
+      const uint32_t oldc = (e >= 0 && s.policy == 0) ? s.eprim[e] : 0u;
+      const bool pinned = oldc == EP_PIN;
+      if (s.lfu_persist && !pinned) { cntk += 1; s.count_by_key[key] = cntk; }
+      if (e >= 0) {
+        if (s.s == S_INF) st = ST_HIT;                       // R4
+        else if (ecc - ecs > s.s) st = ST_EXP1;              // cond (1)
+        else st = (gpre <= ecc || gpre - ecc <= s.s) ? ST_HIT : ST_EXP2;   // cond (2)
+        if (s.policy == 0) {                                 // L6
+          if (!pinned) {
+            uint32_t newc = s.lfu_persist ? cntk : oldc + 1;
+            s.eprim[e] = newc;
+            lfu_move(s, key, oldc, newc, dpop);
+            pin_candidate(s, key, e, newc);
+          }
+        } else {
+          s.eprim[e] = (uint32_t)ctl->t_cur;
+        }
+      }
+      c.status[u] = st;
+      atomicAdd(&bc[st == ST_HIT ? 0 : st == ST_EXP1 ? 1 : st == ST_EXP2 ? 2 : 3], 1u);
+    }
+    st = __shfl_sync(0xffffffffu, st, 0);
+    uint32_t g = gpre;
+    bool push = false;
+    if (st != ST_HIT) {
+      if (s.s == S_INF || st == ST_MISS) g = s.cg[key];
+      if (st != ST_MISS) {
+        if (ecc > ecs) {            // dirty sync push (L4): c_g = max (rows below)
+          push = true;
+          g = g > ecc ? g : ecc;
+          if (lane == 0) s.cg[key] = g;
+        }
+      } else {                      // miss: free entry + hash insert
+        int32_t idx = 0;
+        if (lane == 0) idx = atomicSub(&ctl->ftop, 1) - 1;
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx < 0) {
+          if (lane == 0) raise_err(ctl, 4 /*HET_ERR_CAPACITY*/);
+          e = -1;
+        } else {
+          e = s.fstack[idx];
+          warp_insert(s, key, e, lane);
+          if (lane == 0) {
+            s.ekey[e] = key;
+            uint32_t prim = s.policy == 0 ? (s.lfu_persist ? cntk : 1u) : (uint32_t)ctl->t_cur;
+            s.eprim[e] = prim;
+            if (s.policy == 0) { lfu_move(s, key, EP_FREE, prim, dpop); pin_candidate(s, key, e, prim); }
+            atomicMin(&ctl->min_install, prim);
+          }
+        }
+      }
+      if (e >= 0 && lane == 0) { s.cs[e] = g; s.cc[e] = g; }   // L5 clocks (rows below)
+    }
+    for (int k = lane; k < cnt; k += 32) c.inverse[c.perm[j0 + k]] = u;
+    if (lane == 0) {
+      if (e >= 0) c.uentry[u] = e;
+      meta[grp] = LkMeta{key, e, j0, cnt, g, st, (uint8_t)push};
+    }
+  }
+  __syncthreads();
+  if (live) {
+    const LkMeta mt = meta[grp];
+    const int D4 = s.D >> 2;
+    const int d0 = gw * (D4 / G), d1 = d0 + D4 / G;
+    if (mt.e >= 0) {
+      float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)mt.e * s.D);
+      if (mt.st != ST_HIT) {
+        float4* Wr = reinterpret_cast<float4*>(s.W + mt.key * s.D);
+        const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)mt.e * s.D);
+        for (int d = d0 + lane; d < d1; d += 32) {
+          float4 w = Wr[d];
+          if (mt.push) { w = f4add_(w, pr[d]); Wr[d] = w; }   // Evict push
+          vr[d] = w;                                           // Fetch
+        }
+      }
+      // L7 Get: this warp's slice of the row to every occurrence (128-bit stores)
+      float4* o4 = reinterpret_cast<float4*>(out);
+      for (int kb = 0; kb < mt.cnt; kb += 32) {
+        const int src = kb + lane < mt.cnt ? c.perm[mt.j0 + kb + lane] : 0;
+        const int m = min(32, mt.cnt - kb);
+        for (int d = d0 + lane; d < d1; d += 32) {
+          const float4 val = vr[d];
+          for (int k = 0; k < m; ++k) __stcs(o4 + (int64_t)__shfl_sync(0xffffffffu, src, k) * D4 + d, val);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  dpop_flush(s, dpop);
+  if (threadIdx.x == 0) {
+    if (bc[0]) atomicAdd(&s.cnt[C_HITS], (unsigned long long)bc[0]);
+    if (bc[1]) atomicAdd(&s.cnt[C_EXP1], (unsigned long long)bc[1]);
+    if (bc[2]) atomicAdd(&s.cnt[C_EXP2], (unsigned long long)bc[2]);
+    if (bc[3]) atomicAdd(&s.cnt[C_MISSES], (unsigned long long)bc[3]);
+    if (blockIdx.x == 0 && !ctl->abort) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+  }
+}
+
 // ------------------------------------------------------------------ K_upd
 // Evict push of one resident entry at N = 1 (warp-cooperative) + delete + free
 // push != nullptr (N > 1): the Evict push goes to the owner's inbox, carried
@@ -456,7 +594,13 @@ __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_
   } else if (dirty) {
     float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
     const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
-    for (int d = lane; d < D4; d += 32) Wr[d] = f4add_(Wr[d], pr[d]);
+    for (int d0 = lane; d0 < D4; d0 += 32 * 4) {   // 4 columns per lane in flight (wide rows)
+      float4 w[4], x[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) if (d0 + 32 * b < D4) { w[b] = Wr[d0 + 32 * b]; x[b] = pr[d0 + 32 * b]; }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) if (d0 + 32 * b < D4) Wr[d0 + 32 * b] = f4add_(w[b], x[b]);
+    }
   }
   if (lane == 0) {
     if (push && dirty) atomicAdd(&s.cnt[C_BEMB_TX], 16ull + 4ull * s.D);
@@ -467,6 +611,7 @@ __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_
     b.vkeys[vi] = key;
     b.vdirty[vi] = dirty ? 1 : 0;
     if (s.policy == 0) lfu_move(s, key, prim, EP_FREE, dpop);
+    unpin_count(s, prim);
     s.eprim[e] = EP_FREE;
     s.ekey[e] = -1;
     s.fstack[atomicAdd(&ctl->ftop, 1)] = e;
@@ -549,6 +694,59 @@ __device__ __forceinline__ void segreduce_key(const Dev& s, const Call& c, const
     }
   }
   if (lane == 0) s.cc[e] = ecc + 1;
+}
+
+// Wide rows (D >= 1024): item (u, slice) of 512 columns per warp, so a
+// key's columns are reduced on several SMs at once.  Per column the order is
+// unchanged (+0.0f, then ascending batch position, R11); each lane keeps four
+// column accumulators and four occurrences in flight (16 loads).  The clock
+// step c_c += 1 is taken after the grid sync (every slice read the dirty flag
+// first).
+__device__ __forceinline__ void segreduce_slice(const Dev& s, const Call& c, const float4* __restrict__ G4,
+                                                float lr, int u, int sl, int lane) {
+  const int j0 = c.seg_off[u], cnt = c.seg_off[u + 1] - j0;
+  const int32_t e = c.uentry[u];
+  const bool dirty = s.cc[e] > s.cs[e];
+  const int D4 = s.D >> 2;
+  const int base = sl * 128 + lane;
+  const float nlr = -lr;
+  float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
+  float4* pr = reinterpret_cast<float4*>(s.p + (int64_t)e * s.D);
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 vv[4], pp[4], acc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    vv[j] = vr[base + 32 * j];
+    pp[j] = dirty ? pr[base + 32 * j] : zero;
+    acc[j] = zero;
+  }
+  for (int kb = 0; kb < cnt; kb += 32) {
+    const int src = kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0;
+    const int m = min(32, cnt - kb);
+    for (int k = 0; k < m; k += 4) {
+      float4 g[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int pq = __shfl_sync(0xffffffffu, src, min(k + q, m - 1));
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          g[q][j] = k + q < m ? __ldcs(G4 + (int64_t)pq * D4 + base + 32 * j) : zero;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (k + q < m) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[j] = f4add_(acc[j], g[q][j]);
+        }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 dl = make_float4(__fmul_rn(nlr, acc[j].x), __fmul_rn(nlr, acc[j].y), __fmul_rn(nlr, acc[j].z),
+                                  __fmul_rn(nlr, acc[j].w));
+    vr[base + 32 * j] = f4add_(vv[j], dl);
+    pr[base + 32 * j] = f4add_(pp[j], dl);
+  }
 }
 
 __global__ void __launch_bounds__(UPD_THREADS)
@@ -636,11 +834,20 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   // ---- phase 1: ordered segment reduce + SGD + pending + clock, warp per unique key
   // block 0 plans; the other blocks' warps take the unique keys
   const int rw = gw - UPD_WARPS, nrw = nw - UPD_WARPS;
-  if (rw >= 0)
-    for (int u = rw; u < U; u += nrw) segreduce_key(s, c, G4, lr, u, lane, mystg, &bars[wid], phase, stage_rows);
+  const int S = (D4 >= 256 && D4 % 128 == 0) ? D4 / 128 : 1;   // wide rows: 512-column slices on separate warps
+  if (rw >= 0) {
+    if (S == 1)
+      for (int u = rw; u < U; u += nrw) segreduce_key(s, c, G4, lr, u, lane, mystg, &bars[wid], phase, stage_rows);
+    else
+      for (int it = rw; it < U * S; it += nrw) segreduce_slice(s, c, G4, lr, it / S, it % S, lane);
+  }
   TL_MAX(18);
   // ---- every update done and block 0's plan + task list visible
   grid.sync();
+  if (S > 1) {                                  // Cache.Clock once per key, after every slice
+    for (int u = gw * 32 + lane; u < U; u += nw * 32) s.cc[c.uentry[u]] += 1;
+    grid.sync();
+  }
   const int emode = abort ? 0 : __ldcg(&ctl->emode);
   const bool rebuild = __ldcg(&ctl->rebuild_req);
   if (emode == 1) {
@@ -766,6 +973,14 @@ int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, i
 }
 
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st) {
+  const int D4 = (int)s.D / 4;
+  if (D4 >= 256 && D4 % 128 == 0) {            // wide rows: G warps per key (a power of two)
+    int G = 1;
+    while (G * 2 <= std::min(LK_WARPS, D4 / 128)) G *= 2;
+    const int blocks = std::max(1, (c.n + LK_WARPS / G - 1) / (LK_WARPS / G));
+    k_lookup_wide<<<blocks, LK_WARPS * 32, 0, st>>>(s, c, out, G);
+    return 1;
+  }
   int blocks = std::max(1, (c.n + LK_WARPS - 1) / LK_WARPS);
   k_lookup_fused<<<blocks, LK_WARPS * 32, 0, st>>>(s, c, out);
   return 1;

@@ -125,7 +125,14 @@ __device__ __forceinline__ void push_record(const Dev& s, const P2P& m, int32_t 
   }
   const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
   float4* dst = reinterpret_cast<float4*>(reqrow(m, o, m.rank, ps));
-  for (int d = lane; d < (int)(s.D >> 2); d += 32) dst[d] = pr[d];
+  const int D4 = (int)(s.D >> 2);
+  for (int d0 = lane; d0 < D4; d0 += 32 * 4) {   // loads of 4 columns before their stores (wide rows)
+    float4 t[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) if (d0 + 32 * b < D4) t[b] = pr[d0 + 32 * b];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) if (d0 + 32 * b < D4) dst[d0 + 32 * b] = t[b];
+  }
 }
 
 }  // namespace het

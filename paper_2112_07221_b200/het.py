@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhet.so")
 
-HET_LFU, HET_LRU = 0, 1
+HET_LFU, HET_LRU, HET_LIGHT_LFU = 0, 1, 2
 HET_S_INF = 0xFFFFFFFF
 HET_CLOCK_AUTO = 0xFFFFFFFFFFFFFFFF
 STATUS = {0: "HET_OK", 1: "HET_ERR_ARG", 2: "HET_ERR_KEY_RANGE", 3: "HET_ERR_PROTOCOL",
@@ -35,7 +35,8 @@ class het_dist_t(ctypes.Structure):
 
 class het_opts_t(ctypes.Structure):
     _fields_ = [("max_keys_per_call", ctypes.c_uint32), ("init_seed", ctypes.c_uint64),
-                ("lfu_persist", ctypes.c_int), ("debug_log", ctypes.c_int)]
+                ("lfu_persist", ctypes.c_int), ("debug_log", ctypes.c_int),
+                ("pin_threshold", ctypes.c_uint32)]
 
 
 class het_stats_t(ctypes.Structure):
@@ -43,7 +44,7 @@ class het_stats_t(ctypes.Structure):
                 ["lookups", "keys", "unique", "hits", "exp1", "exp2", "misses", "evictions",
                  "dirty_pushes", "bytes_clock_tx", "bytes_clock_rx", "bytes_emb_tx", "bytes_emb_rx",
                  "launches"]] + [("resident", ctypes.c_uint32), ("capacity", ctypes.c_uint32),
-                                 ("sticky_error", ctypes.c_int)]
+                                 ("sticky_error", ctypes.c_int), ("pinned", ctypes.c_uint32)]
 
     def as_dict(self):
         return {f[0]: int(getattr(self, f[0])) for f in self._fields_}
@@ -134,14 +135,14 @@ def het_get_unique_id() -> bytes:
 
 
 def het_cache_create(rows, D, cache_frac, s, policy=HET_LFU, rank=0, world=1, unique_id=None,
-                     max_keys_per_call=65536, init_seed=0, lfu_persist=1, stream=None):
+                     max_keys_per_call=65536, init_seed=0, lfu_persist=1, stream=None, pin_threshold=0):
     lib = load()
     dist = None
     uid = None
     if world > 1:
         uid = ctypes.create_string_buffer(bytes(unique_id), 128)
         dist = het_dist_t(rank, world, ctypes.cast(uid, ctypes.c_void_p))
-    opts = het_opts_t(max_keys_per_call, init_seed, lfu_persist, 0)
+    opts = het_opts_t(max_keys_per_call, init_seed, lfu_persist, 0, pin_threshold)
     h = ctypes.c_void_p()
     rc = lib.het_cache_create(rows, D, cache_frac, s, policy,
                               ctypes.byref(dist) if dist is not None else None,
@@ -210,13 +211,13 @@ class HetCache:
     """One worker's cache (torch tensors in, torch tensors out)."""
 
     def __init__(self, rows, D, cache_frac, s, policy=HET_LFU, rank=0, world=1, unique_id=None,
-                 max_keys_per_call=65536, init_seed=0, lfu_persist=1):
+                 max_keys_per_call=65536, init_seed=0, lfu_persist=1, pin_threshold=0):
         import torch
         self.torch = torch
         self.rows, self.D, self.world, self.rank = rows, D, world, rank
         self.n_max = max_keys_per_call
         self.h = het_cache_create(rows, D, cache_frac, s, policy, rank, world, unique_id,
-                                  max_keys_per_call, init_seed, lfu_persist)
+                                  max_keys_per_call, init_seed, lfu_persist, pin_threshold=pin_threshold)
 
     def close(self):
         if self.h:

@@ -31,6 +31,7 @@ def main():
     # 14,208 distinct ids per worker-iteration -> the large-n exchange path),
     # wide (Criteo-shaped fields over 5,000 rows with 4 KB rows, D=1024)
     shape = sys.argv[5] if len(sys.argv) > 5 else "toy"
+    pin = int(sys.argv[6]) if len(sys.argv) > 6 else 64      # light-LFU threshold (policy 2)
     lr = 0.01
     if shape == "reddit":
         R, D, n_max = gen.REDDIT_ROWS, 128, 14208
@@ -38,8 +39,9 @@ def main():
         R, D, n_max, cards = 5000, 1024, 4096, gen.scaled_cards(5000)
     else:
         R, D, n_max, cards = 1000, 8, 4096, gen.cards_for("toy")
-    g = het.HetCache(R, D, frac, s, policy, rank=rank, world=world, unique_id=obj[0], max_keys_per_call=n_max)
-    o = Oracle(R=R, D=D, C=capacity(frac, R), s=s, policy=policy, N=world)
+    g = het.HetCache(R, D, frac, s, policy, rank=rank, world=world, unique_id=obj[0], max_keys_per_call=n_max,
+                     pin_threshold=pin)
+    o = Oracle(R=R, D=D, C=capacity(frac, R), s=s, policy=policy, N=world, pin_threshold=pin)
     for t in range(T):
         if shape == "reddit":
             keys = [gen.reddit_keys(i, t, n_max).numpy() for i in range(world)]
@@ -66,6 +68,8 @@ def main():
     for k in ["lookups", "keys", "unique", "hits", "exp1", "exp2", "misses", "evictions", "dirty_pushes"]:
         assert gs[k] == os_[k], (k, gs[k], os_[k])
     assert gs["bytes_emb_tx"] > 0
+    if policy == 2:
+        assert gs["pinned"] > 0
     g.sync()
     o.flush()
     owned = np.arange(rank, R, world, dtype=np.int64)

@@ -34,7 +34,7 @@ def test_multi_gpu_parity(policy, s, frac, p2p):
 
 @pytest.mark.skipif(ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("shape,policy,s,frac,T", [("reddit", 0, 10, 0.1, 12), ("wide", 0, 3, 0.1, 30),
-                                                   ("wide", 1, 100, 0.05, 30)])
+                                                   ("wide", 1, 100, 0.05, 30), ("toy", 2, 10, 0.1, 60)])
 @pytest.mark.parametrize("p2p", ["1", "0"])
 def test_multi_gpu_parity_shapes(shape, policy, s, frac, T, p2p):
     """BASELINE configs[2]-shaped batches (14,208 distinct ids per worker: the
@@ -44,7 +44,7 @@ def test_multi_gpu_parity_shapes(shape, policy, s, frac, T, p2p):
     port = 31000 + 10 * policy + (s % 7) + 100 * int(p2p) + (0 if shape == "reddit" else 50)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}",
-           os.path.join(ROOT, "tests", "mgpu_worker.py"), str(policy), str(s), str(frac), str(T), shape]
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), str(policy), str(s), str(frac), str(T), shape, "4"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert "MGPU_OK" in r.stdout

@@ -10,7 +10,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-from oracle.oracle import Oracle, capacity, S_INF, LFU, LRU  # noqa: E402
+from oracle.oracle import Oracle, capacity, S_INF, LFU, LRU, LIGHT_LFU, PINNED  # noqa: E402
 from workload import gen  # noqa: E402
 
 LR = 0.01
@@ -27,12 +27,13 @@ def assert_rows(a, b):
 
 
 class Pair:
-    def __init__(self, R, D, frac, s, policy=LFU, persist=1, n_max=4096, track_div=1):
+    def __init__(self, R, D, frac, s, policy=LFU, persist=1, n_max=4096, track_div=1, pin=64):
         het = _het()
         self.R, self.D = R, D
         self.o = Oracle(R=R, D=D, C=capacity(frac, R), s=s, policy=policy, lfu_persist=persist,
-                        track_div=track_div)
-        self.g = het.HetCache(R, D, frac, s, policy, max_keys_per_call=n_max, lfu_persist=persist)
+                        track_div=track_div, pin_threshold=pin)
+        self.g = het.HetCache(R, D, frac, s, policy, max_keys_per_call=n_max, lfu_persist=persist,
+                              pin_threshold=pin)
         self.exact_rows = 0
 
     def step(self, t, keys, grads, check_logs=True, check_victims=True):
@@ -73,7 +74,11 @@ class Pair:
         assert np.array_equal(gc["keys"], oc["keys"])
         assert np.array_equal(gc["cs"], oc["cs"])
         assert np.array_equal(gc["cc"], oc["cc"])
-        prim = oc["count"] if self.g_policy == LFU else oc["tick"]
+        if self.g_policy == LIGHT_LFU:   # pinned entries carry the EP_PIN marker
+            prim = np.where(oc["tick"] == PINNED, np.uint32(PINNED), oc["count"])
+            assert self.g.stats()["pinned"] == int((oc["tick"] == PINNED).sum())
+        else:
+            prim = oc["count"] if self.g_policy == LFU else oc["tick"]
         assert np.array_equal(gc["prim"], prim)
         assert_rows(gc["v"], oc["v"])
         assert_rows(gc["p"], oc["p"])
@@ -116,6 +121,28 @@ def test_toy_full_parity(policy, s, persist, frac, fused, monkeypatch):
         p.step(t, keys, grads)
     p.compare_stats()
     p.compare_cache()
+    p.finish()
+
+
+@pytest.mark.parametrize("persist,pin,frac", [(1, 8, 0.1), (0, 3, 0.1), (1, 2, 0.05)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_light_lfu_parity(persist, pin, frac, fused, monkeypatch):
+    """Light-LFU (R27): promotions (ascending key, floor(C/2) cap --
+    the cap binds with these thresholds), no count maintenance for pinned
+    entries, pinned entries never victims; everything bit-exact vs the oracle."""
+    if not fused:
+        monkeypatch.setenv("HET_NO_FUSED", "1")
+    R, D = 1000, 8
+    p = Pair(R, D, frac, 10, LIGHT_LFU, persist, pin=pin)
+    p.g_policy = LIGHT_LFU
+    for t in range(150):
+        keys = toy_keys(t)
+        p.step(t, keys, gen.grads(0, t, keys.size, D).numpy())
+        if t % 37 == 5:
+            p.compare_cache()
+    p.compare_stats()
+    p.compare_cache()
+    assert p.g.stats()["pinned"] == capacity(frac, R) // 2     # the cap binds
     p.finish()
 
 
@@ -387,10 +414,14 @@ def _tracked_mask(keys, track):
     return out
 
 
-def test_reddit_shaped_all_unique():
+@pytest.mark.parametrize("fused", [True, False])
+def test_reddit_shaped_all_unique(fused, monkeypatch):
     """BASELINE configs[2] shape (GraphSAGE on Reddit): 232,965 node ids,
     14,208 distinct ids per worker-iteration (dedup on already-unique keys,
-    P:687), D=128, cache 10 %, s=10 -- one worker."""
+    P:687), D=128, cache 10 %, s=10 -- one worker; the fused lookup/update
+    after the cluster dedup, and the per-phase kernels."""
+    if not fused:
+        monkeypatch.setenv("HET_NO_FUSED", "1")
     R, D, K = gen.REDDIT_ROWS, 128, 14208
     p = Pair(R, D, 0.1, 10, LFU, n_max=K, track_div=64)
     p.g_policy = LFU
@@ -411,15 +442,17 @@ def test_reddit_shaped_all_unique():
     p.compare_stats()
 
 
-def test_scale_shaped_wide_rows():
-    """BASELINE configs[4] row shape (D=4096, 16 KB rows: the column loops,
-    no TMA staging) on a scaled table: Criteo-shaped keys over 20,000 rows."""
-    R, D = 20000, 4096
+@pytest.mark.parametrize("D,B,T", [(4096, 32, 8), (4096, 128, 16), (1024, 128, 24)])
+def test_scale_shaped_wide_rows(D, B, T):
+    """BASELINE configs[4] row shape (D=4096, 16 KB rows) on a scaled table:
+    Criteo-shaped keys over 20,000 rows.  Wide rows run with several warps per
+    key (k_lookup_wide) and 512-column slices in the update (segreduce_slice)."""
+    R = 20000
     cards = gen.scaled_cards(R)
     p = Pair(R, D, 0.1, 100, LFU, n_max=4096, track_div=16)
     p.g_policy = LFU
-    for t in range(8):
-        keys = gen.criteo_keys(0, t, 1, 32, cards)[0].numpy()
+    for t in range(T):
+        keys = gen.criteo_keys(0, t, 1, B, cards)[0].numpy()
         grads = gen.grads(0, t, keys.size, D).numpy()
         kd = torch.from_numpy(keys).cuda()
         out = p.g.lookup(kd, t).cpu().numpy()
