@@ -143,6 +143,29 @@ __device__ __forceinline__ float4 f4add_(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
 }
 
+// First bin where the running count of a shared-memory histogram reaches
+// `need` (block-wide: per-thread chunks, one block scan, then a short serial
+// walk in the crossing chunk).  *s_bin = -1 if the total stays below need.
+__device__ __forceinline__ void block_find_cross(const uint32_t* hs, int nb, int64_t need, int* s_bin,
+                                                 long long* s_before) {
+  __shared__ long long ws[32];
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
+  long long loc = 0;
+  for (int q = b0; q < b1; ++q) loc += hs[q];
+  if (threadIdx.x == 0) *s_bin = -1;
+  long long tot;
+  const long long ex = block_excl_scan64(loc, ws, &tot);
+  if (loc > 0 && ex < need && ex + loc >= need) {
+    long long cum = ex;
+    for (int q = b0; q < b1; ++q) {
+      if (cum + hs[q] >= need) { *s_bin = q; *s_before = cum; break; }
+      cum += hs[q];
+    }
+  }
+  __syncthreads();
+}
+
 // generic exact selection (all blocks of a cooperative grid); sm64 needs SUBMAX*8 bytes
 __device__ __forceinline__ void generic_select(const Dev& s, const EvBuf& b, uint64_t* sm64, uint32_t* h,
                                               cg::grid_group& grid) {
@@ -179,19 +202,21 @@ __device__ __forceinline__ void generic_select(const Dev& s, const EvBuf& b, uin
       if (h[i]) atomicAdd(&b.hist[i], h[i]);
   }
   grid.sync();
-  // P2: threshold T, needT (block 0)
+  // P2: threshold T, needT (block 0; the histogram scanned block-wide)
   if (blockIdx.x == 0) {
-    __shared__ int s_found;
+    __shared__ int s_found, s_bin;
+    __shared__ long long s_before;
     if (all) {
       if (threadIdx.x == 0) { ctl->T = 0xFFFFFFFFu; ctl->needT = -1; s_found = 1; }
-    } else if (threadIdx.x == 0) {
-      s_found = 0;
-      if (!b.flags[0]) {
-        int64_t cum = 0;
-        for (int bb = 0; bb < NBIN - 1; ++bb) {
-          uint32_t hb = b.hist[bb];
-          if (cum + hb >= need) { ctl->T = base + (uint32_t)bb; ctl->needT = need - cum; s_found = 1; break; }
-          cum += hb;
+    } else {
+      if (threadIdx.x == 0) s_found = 0;
+      const bool bad = b.flags[0] != 0;
+      for (int i = threadIdx.x; i < NBIN; i += blockDim.x) h[i] = b.hist[i];
+      __syncthreads();
+      if (!bad) {
+        block_find_cross(h, NBIN - 1, need, &s_bin, &s_before);
+        if (threadIdx.x == 0 && s_bin >= 0) {
+          ctl->T = base + (uint32_t)s_bin; ctl->needT = need - s_before; s_found = 1;
         }
       }
     }
@@ -240,23 +265,21 @@ __device__ __forceinline__ void generic_select(const Dev& s, const EvBuf& b, uin
   for (int i = threadIdx.x; i < NBIN; i += blockDim.x)
     if (h[i]) atomicAdd(&b.khist[i], h[i]);
   grid.sync();
-  // P4: key-top bucket kb1 of the boundary (block 0)
+  // P4: key-top bucket kb1 of the boundary (block 0; block-wide scan)
   if (blockIdx.x == 0) {
+    __shared__ int s_kb;
+    __shared__ long long s_kbefore;
+    const bool scan = needT > 0 && needT < ctl->ncand;
     if (threadIdx.x == 0) {
       ctl->kb1 = 0xFFFFFFFFu;
       ctl->need2 = 0;
-      if (needT > 0) {
-        if (needT >= ctl->ncand) {
-          ctl->kb1 = NBIN;
-        } else {
-          int64_t cum = 0;
-          for (int bb = 0; bb < NBIN; ++bb) {
-            uint32_t hb = b.khist[bb];
-            if (cum + hb >= needT) { ctl->kb1 = bb; ctl->need2 = needT - cum; break; }
-            cum += hb;
-          }
-        }
-      }
+      if (needT > 0 && !scan) ctl->kb1 = NBIN;
+    }
+    if (scan) {
+      for (int i = threadIdx.x; i < NBIN; i += blockDim.x) h[i] = b.khist[i];
+      __syncthreads();
+      block_find_cross(h, NBIN, needT, &s_kb, &s_kbefore);
+      if (threadIdx.x == 0 && s_kb >= 0) { ctl->kb1 = (uint32_t)s_kb; ctl->need2 = needT - s_kbefore; }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < NBIN; i += blockDim.x) b.khist[i] = 0;

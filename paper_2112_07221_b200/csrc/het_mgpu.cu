@@ -583,7 +583,8 @@ het_status_t mgpu_lookup(MgpuState* m, const Dev& d, const Call& c, void* prof, 
   {
     void* pr = prof_begin(prof, "sync_fetch", st);
     cudaMemsetAsync(m->scnt, 0, sizeof(int32_t) * 2 * N, st);
-    k_build_requests<<<grid_for(std::max(n, 1), 8), MG_TPB, 0, st>>>(d, c, *m);
+    // warp per unique key, not grid-strided: one warp for every key (n may exceed grid_for's cap)
+    k_build_requests<<<std::max(1, (n + 7) / 8), MG_TPB, 0, st>>>(d, c, *m);
     if ((rc = exchange_counts(m, st))) return rc;
     if ((rc = alltoallv(m, m->hdr, m->rhdr, m->h_scnt, m->h_rcnt, 2, sizeof(ReqHdr), m->CAPS * sizeof(ReqHdr), st)))
       return rc;
