@@ -83,7 +83,7 @@ def auc(y: np.ndarray, p: np.ndarray) -> float:
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--s", type=int, default=10, help="staleness threshold (-1 = infinity)")
+    ap.add_argument("--staleness", type=int, default=10, help="staleness threshold s (-1 = infinity)")
     ap.add_argument("--steps", type=int, default=600)
     ap.add_argument("--rows", type=int, default=1_000_000)
     ap.add_argument("--D", type=int, default=16)
@@ -105,7 +105,7 @@ def main():
         uid = obj[0]
     F, D, B = 26, args.D, args.batch
     cards = gen.scaled_cards(args.rows)
-    s = het.HET_S_INF if args.s < 0 else args.s
+    s = het.HET_S_INF if args.staleness < 0 else args.staleness
     cache = het.HetCache(args.rows, D, args.cache_frac, s, het.HET_LFU, rank=rank, world=world,
                          unique_id=uid, max_keys_per_call=B * F)
     torch.manual_seed(0)                              # same dense init on every worker
@@ -153,7 +153,7 @@ def main():
         torch.distributed.all_gather(gp, pr)
         torch.distributed.all_gather(gy, yy)
         pr, yy = torch.cat(gp), torch.cat(gy)
-    res = {"s": "inf" if args.s < 0 else args.s, "n_gpus": world, "steps": args.steps, "batch_per_gpu": B,
+    res = {"s": "inf" if args.staleness < 0 else args.staleness, "n_gpus": world, "steps": args.steps, "batch_per_gpu": B,
            "rows": args.rows, "D": D, "progressive_auc": auc(yy.cpu().numpy(), pr.cpu().numpy()),
            "loss_second_half": float(torch.stack(losses).mean()),
            "samples_per_s": B * world * args.steps / dt,

@@ -749,6 +749,55 @@ __device__ __forceinline__ void segreduce_slice(const Dev& s, const Call& c, con
   }
 }
 
+// Victim keys of one listed count-bitmap block (task = (count << 27) | block):
+// all set bits for counts < T, bits of keys <= K* for count T; appended to
+// b.vsel at a warp-aggregated cursor (ctl->nsel).
+__device__ __forceinline__ void extract_task(const Dev& s, const EvBuf& b, int task, uint32_t T, int64_t Kstar,
+                                             int lane) {
+  Ctl* ctl = s.ctl;
+  const int32_t code = __ldcg(&b.cand[task]);
+  const uint32_t cc = (uint32_t)code >> 27;
+  const int64_t blk = code & ((1 << 27) - 1);
+  const uint32_t* bm = s.bm + (int64_t)cc * s.bm_words;
+  uint32_t w[4];
+  int cl = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r;
+    uint32_t bits = wi < s.bm_words ? __ldcg(&bm[wi]) : 0u;
+    if (cc == T) {   // keep keys <= K*
+      const int64_t k0 = wi << 5;
+      if (k0 > Kstar) bits = 0;
+      else if (k0 + 31 > Kstar) bits &= (1u << (Kstar - k0 + 1)) - 1u;
+    }
+    w[r] = bits;
+    cl += __popc(bits);
+  }
+  int incl = cl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (!total) return;
+  int base = 0;
+  if (lane == 31) base = atomicAdd(&ctl->nsel, total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  int pos = base + incl - cl;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    uint32_t bits = w[r];
+    const int64_t kb = ((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r) << 5;
+    while (bits) {
+      b.vsel[pos++] = kb + (__ffs(bits) - 1);
+      bits &= bits - 1;
+    }
+  }
+}
+
+constexpr int EXT_IN_PLAN = UPD_WARPS;   // block 0 extracts the victims itself up to one listed block per warp
+
 __global__ void __launch_bounds__(UPD_THREADS)
 k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, int stage_rows, P2P pm, int push) {
   const P2P* pp = push ? &pm : nullptr;
@@ -817,11 +866,18 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
         }
       }
       __syncthreads();
-      if (threadIdx.x == 0) ctl->ntask = s_nt;
+      if (threadIdx.x == 0) { ctl->ntask = s_nt; ctl->ext_done = s_nt <= EXT_IN_PLAN; }
+      // few listed blocks (the common steady state): block 0 extracts the
+      // victim keys now, in parallel with the segment reduce, so the grid
+      // skips the extraction phase and its grid sync
+      if (s_nt <= EXT_IN_PLAN)
+        for (int task = threadIdx.x >> 5; task < s_nt; task += UPD_WARPS)
+          extract_task(s, b, task, T, ctl->Kstar, threadIdx.x & 31);
     } else if (threadIdx.x == 0) {
       ctl->ntask = 0;
+      ctl->ext_done = 0;
     }
-    if (threadIdx.x == 0) { ctl->ext_next = 0; ctl->ext_done = 0; ctl->find_next = 0; }
+    if (threadIdx.x == 0) { ctl->ext_next = 0; ctl->find_next = 0; }
     TL_MAX(23);
   }
   __syncthreads();
@@ -855,52 +911,13 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
     const uint32_t T = __ldcg(&ctl->T);
     const int64_t Kstar = __ldcg(&ctl->Kstar);
     const int ntask = __ldcg(&ctl->ntask);
-    for (int task = gw; task < ntask; task += nw) {
-      const int32_t code = __ldcg(&b.cand[task]);
-      const uint32_t cc = (uint32_t)code >> 27;
-      const int64_t blk = code & ((1 << 27) - 1);
-      const uint32_t* bm = s.bm + (int64_t)cc * s.bm_words;
-      uint32_t w[4];
-      int cl = 0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r;
-        uint32_t bits = wi < s.bm_words ? __ldcg(&bm[wi]) : 0u;
-        if (cc == T) {   // keep keys <= K*
-          const int64_t k0 = wi << 5;
-          if (k0 > Kstar) bits = 0;
-          else if (k0 + 31 > Kstar) bits &= (1u << (Kstar - k0 + 1)) - 1u;
-        }
-        w[r] = bits;
-        cl += __popc(bits);
-      }
-      int incl = cl;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      if (!total) continue;
-      int base = 0;
-      if (lane == 31) base = atomicAdd(&ctl->nsel, total);
-      base = __shfl_sync(0xffffffffu, base, 31);
-      int pos = base + incl - cl;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        uint32_t bits = w[r];
-        const int64_t kb = ((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r) << 5;
-        while (bits) {
-          b.vsel[pos++] = kb + (__ffs(bits) - 1);
-          bits &= bits - 1;
-        }
-      }
-    }
+    if (!__ldcg(&ctl->ext_done))
+      for (int task = gw; task < ntask; task += nw) extract_task(s, b, task, T, Kstar, lane);
   }
   TL_MAX(19);
   // ---- phase 2 (LFU bitmap path): every update done; evict, warp per victim
   if (emode == 1) {
-    grid.sync();
+    if (!__ldcg(&ctl->ext_done)) grid.sync();   // uniform: ext_done was set before the first grid sync
     TL_MAX(20);
     const int nsel = ctl->nsel;
     for (int i = gw; i < nsel; i += nw) {

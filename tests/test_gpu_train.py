@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_train_wdl_learns():
-    cmd = [sys.executable, os.path.join(ROOT, "examples", "train_wdl.py"), "--s", "10", "--steps", "300",
+    cmd = [sys.executable, os.path.join(ROOT, "examples", "train_wdl.py"), "--staleness", "10", "--steps", "300",
            "--rows", "200000"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

@@ -1,6 +1,7 @@
 """SURVEY §8(f) NEXT-2 / NEXT-3 measurements on the production kernels.
 
   python tools/next_sweeps.py miss            # NEXT-2, one GPU
+  python tools/next_sweeps.py light           # NEXT-2 light-LFU vs LFU, one GPU
   torchrun --nproc-per-node N tools/next_sweeps.py comm   # NEXT-3, N GPUs
 
 miss: Criteo-shaped WDL keys (BASELINE configs[1] shape), cache size 3/5/10/15 %
@@ -63,6 +64,40 @@ def miss_sweep():
                               "cold_miss_rate": d["misses"] / d["unique"], "unique_per_step": d["unique"] / meas,
                               "evictions_per_step": d["evictions"] / meas, "wall_s": round(time.time() - t0, 1)}),
                   flush=True)
+            c.close()
+
+
+def light_sweep():
+    """Light-LFU (R27) against exact LFU on the WDL-shaped stream:
+    miss rate (the paper: "similar miss rate") and the device time of a
+    lookup+update step (the paper: "significantly small run-time cost"),
+    CUDA events around MEAS stream-launched steps after WARM warm-up steps."""
+    dev = torch.device("cuda", 0)
+    warm, meas = int(os.environ.get("WARM", 6000)), int(os.environ.get("MEAS", 1000))
+    g = gen.grads(0, 0, N_KEYS, D, device=dev)
+    for frac in (0.03, 0.10):
+        for pol, name in ((het.HET_LFU, "LFU"), (het.HET_LIGHT_LFU, "light-LFU(64)")):
+            c = het.HetCache(R, D, frac, 100, pol, max_keys_per_call=N_KEYS, pin_threshold=64)
+            keys = gen.criteo_keys(0, 0, warm + meas, B, CARDS, 0.7, device=dev)
+            for t in range(warm):
+                c.lookup(keys[t], het.HET_CLOCK_AUTO)
+                c.update(keys[t], g, 0.01)
+            torch.cuda.synchronize()
+            s0 = c.stats()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for t in range(warm, warm + meas):
+                c.lookup(keys[t], het.HET_CLOCK_AUTO)
+                c.update(keys[t], g, 0.01)
+            e1.record()
+            torch.cuda.synchronize()
+            s1 = c.stats()
+            d = {k: s1[k] - s0[k] for k in ("unique", "hits", "exp1", "exp2", "misses", "evictions")}
+            print(json.dumps({"sweep": "NEXT-2 light-LFU", "cache_frac": frac, "policy": name, "s": 100,
+                              "warm_steps": warm, "measured_steps": meas,
+                              "miss_rate": (d["misses"] + d["exp1"] + d["exp2"]) / d["unique"],
+                              "pinned": s1["pinned"], "capacity": s1["capacity"],
+                              "us_per_step_stream": e0.elapsed_time(e1) / meas * 1e3}), flush=True)
             c.close()
 
 
@@ -130,4 +165,4 @@ def comm_sweep():
 
 
 if __name__ == "__main__":
-    {"miss": miss_sweep, "comm": comm_sweep}[sys.argv[1]]()
+    {"miss": miss_sweep, "light": light_sweep, "comm": comm_sweep}[sys.argv[1]]()
