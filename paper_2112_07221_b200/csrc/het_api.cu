@@ -674,7 +674,14 @@ het_status_t het_dense_allreduce(het_cache_t h, float* buf, uint64_t count, het_
   if (count == 0 || h->d.world == 1) return HET_OK;
   if (!buf || !is_device_ptr(buf)) return fail(h, HET_ERR_ARG, "dense buffer must be device memory");
   Prof p(h, "dense_allreduce", st);
-  het_status_t rc = mgpu_allreduce_sum(h->mg, buf, count, st);
+  int l = 0;
+  het_status_t rc = mgpu_dense_p2p(h->mg, h->d, buf, count, st, &l);   // peer-memory one-shot mean
+  if (rc == HET_OK) {
+    h->launches += l;
+    return HET_OK;
+  }
+  if (rc != HET_ERR_CAPACITY) return fail(h, rc, "peer all-reduce failed");
+  rc = mgpu_allreduce_sum(h->mg, buf, count, st);
   if (rc) return fail(h, rc, "allreduce failed");
   k_scale<<<148 * 4, 256, 0, st>>>(buf, count, 1.0f / (float)h->d.world);
   h->launches += 1;

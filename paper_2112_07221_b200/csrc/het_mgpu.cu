@@ -779,6 +779,13 @@ het_status_t mgpu_flush(MgpuState* m, const Dev& d, cudaStream_t st) {
   return rc;
 }
 
+het_status_t mgpu_dense_p2p(MgpuState* m, const Dev& d, float* buf, uint64_t count, cudaStream_t st,
+                            int* launches) {
+  static const bool nccl_only = getenv("HET_DENSE_NCCL") != nullptr;   // diagnostic: NCCL all-reduce
+  if (!m->p2p || nccl_only) return HET_ERR_CAPACITY;
+  return p2p_dense_allreduce(m->p2p, d, buf, count, m->comm, st, launches);
+}
+
 het_status_t mgpu_allreduce_sum(MgpuState* m, float* buf, uint64_t count, cudaStream_t st) {
   return nccl_ok(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, m->comm, st));
 }

@@ -21,6 +21,9 @@ het_status_t mgpu_flush(MgpuState* mg, const Dev& d, cudaStream_t st);
 // deliver the eviction pushes still waiting for the next exchange round
 het_status_t mgpu_drain(MgpuState* mg, const Dev& d, const Call& c, cudaStream_t st);
 het_status_t mgpu_allreduce_sum(MgpuState* mg, float* buf, uint64_t count, cudaStream_t st);
+// Eq. 2 mean over peer memory (p2p exchange only); HET_ERR_CAPACITY -> use NCCL
+het_status_t mgpu_dense_p2p(MgpuState* mg, const Dev& d, float* buf, uint64_t count, cudaStream_t st,
+                            int* launches);
 void mgpu_bytes(MgpuState* mg, uint64_t* ctx, uint64_t* crx, uint64_t* etx, uint64_t* erx);
 uint64_t mgpu_take_launches(MgpuState* mg);
 

@@ -762,11 +762,101 @@ k_exchange(Dev s, Call c, P2P m, float* __restrict__ out) {
 }
 
 // ---------------------------------------------------------------- host side
+// ---------------------------------------------------------------- dense all-reduce over peer memory
+// Eq. 2: buf <- mean over the N workers.  Every rank stages its
+// buffer in an IPC-exported region (two buffers by epoch parity), publishes
+// an epoch flag into every peer's flag array, and then each rank sums ALL
+// staged buffers itself in rank order (one-shot: every rank computes the same
+// fp32 sums in the same order, so the result is bitwise identical on every
+// rank).  A second flag ("done reading epoch e") guards the reuse of a
+// staging buffer two epochs later.  No grid-wide barrier: last-block
+// election publishes, every block waits for the peers before its share of
+// the sum; the grid (coop_sm_reserve() blocks) fits in the SMs the
+// cooperative hot-path kernels leave free, so a spinning block never starves
+// a peer's kernel.
+struct DenseView {
+  int N, rank;
+  char* const* peer;            // [N] dense-region bases (own included)
+  uint64_t cap;                 // floats per staging buffer
+  unsigned long long* epoch;    // completed all-reduces (device)
+  int32_t* done;                // [2] last-block counters
+};
+__device__ __forceinline__ Flag* dready(const DenseView& v, int r) { return (Flag*)v.peer[r]; }
+__device__ __forceinline__ Flag* ddone(const DenseView& v, int r) { return (Flag*)v.peer[r] + 64; }
+__device__ __forceinline__ float* dbuf(const DenseView& v, int r, int par) {
+  return (float*)(v.peer[r] + 2 * 64 * sizeof(Flag)) + (uint64_t)par * v.cap;
+}
+
+__global__ void __launch_bounds__(512) k_dense_ar(DenseView v, float* __restrict__ buf, uint64_t count,
+                                                  float scale, Ctl* ctl) {
+  __shared__ int s_ok;
+  const unsigned long long e = *v.epoch + 1;
+  const int par = (int)(e & 1);
+  const uint64_t n4 = count / 4;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = (uint64_t)gridDim.x * blockDim.x;
+  // staging buffer `par` is free once every peer finished reading epoch e - 2
+  if (threadIdx.x == 0) s_ok = e <= 2 || wait_flags(ddone(v, v.rank), v.N, e - 2, ctl);
+  __syncthreads();
+  float4* mine = reinterpret_cast<float4*>(dbuf(v, v.rank, par));
+  constexpr int U = 8;   // float4 per thread in flight (peer reads cross NVLink: latency-bound)
+  if (s_ok) {
+    const float4* b4 = reinterpret_cast<const float4*>(buf);
+    for (uint64_t i0 = tid; i0 < n4; i0 += U * nth) {
+      float4 t[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) if (i0 + k * nth < n4) t[k] = b4[i0 + k * nth];
+#pragma unroll
+      for (int k = 0; k < U; ++k) if (i0 + k * nth < n4) mine[i0 + k * nth] = t[k];
+    }
+    for (uint64_t i = n4 * 4 + tid; i < count; i += nth) ((float*)mine)[i] = buf[i];
+  }
+  if (last_block(&v.done[0]) && threadIdx.x < v.N) {   // fence.sys done by last_block
+    st_release(&dready(v, threadIdx.x)[v.rank].epoch, e);
+    if (threadIdx.x == 0) v.done[0] = 0;
+  }
+  if (threadIdx.x == 0) s_ok = s_ok && wait_flags(dready(v, v.rank), v.N, e, ctl);
+  __syncthreads();
+  if (s_ok) {
+    for (uint64_t i0 = tid; i0 < n4; i0 += U * nth) {
+      float4 a[U];
+      const float4* s0 = reinterpret_cast<const float4*>(dbuf(v, 0, par));
+#pragma unroll
+      for (int k = 0; k < U; ++k) if (i0 + k * nth < n4) a[k] = s0[i0 + k * nth];
+      for (int r = 1; r < v.N; ++r) {              // rank order: the same sums on every rank
+        const float4* sr = reinterpret_cast<const float4*>(dbuf(v, r, par));
+        float4 x[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) if (i0 + k * nth < n4) x[k] = sr[i0 + k * nth];
+#pragma unroll
+        for (int k = 0; k < U; ++k) a[k] = f4add_p(a[k], x[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (i0 + k * nth < n4)
+          reinterpret_cast<float4*>(buf)[i0 + k * nth] = make_float4(
+              __fmul_rn(a[k].x, scale), __fmul_rn(a[k].y, scale), __fmul_rn(a[k].z, scale), __fmul_rn(a[k].w, scale));
+    }
+    for (uint64_t i = n4 * 4 + tid; i < count; i += nth) {
+      float a = dbuf(v, 0, par)[i];
+      for (int r = 1; r < v.N; ++r) a = __fadd_rn(a, dbuf(v, r, par)[i]);
+      buf[i] = __fmul_rn(a, scale);
+    }
+  }
+  if (last_block(&v.done[1])) {
+    if (threadIdx.x < v.N) st_release(&ddone(v, threadIdx.x)[v.rank].epoch, e);
+    if (threadIdx.x == 0) { v.done[1] = 0; *v.epoch = e; }
+  }
+}
+
 struct P2PState {
   P2P v{};
   char* inbox = nullptr;
   std::vector<char*> mapped;     // opened peer bases (to close)
   std::vector<void*> allocs;
+  // dense all-reduce staging (set up by the first call)
+  char* dense = nullptr;
+  DenseView dv{};
+  bool dense_failed = false;
 };
 
 template <typename T>
@@ -842,7 +932,72 @@ void p2p_destroy(P2PState* p) {
   for (char* q : p->mapped) cudaIpcCloseMemHandle(q);
   for (void* q : p->allocs) cudaFree(q);
   if (p->inbox) cudaFree(p->inbox);
+  if (p->dense) cudaFree(p->dense);
   delete p;
+}
+
+// IPC export of one allocation, import of every peer's (collective over comm)
+static het_status_t exchange_bases(P2PState* p, char* mine_base, int N, int rank, ncclComm_t comm,
+                                   cudaStream_t st, char*** dbases_out) {
+  cudaIpcMemHandle_t mine;
+  if (cudaIpcGetMemHandle(&mine, mine_base) != cudaSuccess) return HET_ERR_CUDA;
+  char* dh;
+  if (cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * N) != cudaSuccess) return HET_ERR_OOM;
+  cudaMemcpyAsync(dh + sizeof(cudaIpcMemHandle_t) * rank, &mine, sizeof(mine), cudaMemcpyHostToDevice, st);
+  if (ncclAllGather(dh + sizeof(cudaIpcMemHandle_t) * rank, dh, sizeof(cudaIpcMemHandle_t), ncclChar, comm, st) !=
+      ncclSuccess)
+    return HET_ERR_NCCL;
+  std::vector<cudaIpcMemHandle_t> all(N);
+  cudaMemcpyAsync(all.data(), dh, sizeof(cudaIpcMemHandle_t) * N, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
+  cudaFree(dh);
+  std::vector<char*> bases(N);
+  for (int r = 0; r < N; ++r) {
+    if (r == rank) { bases[r] = mine_base; continue; }
+    void* q = nullptr;
+    if (cudaIpcOpenMemHandle(&q, all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return HET_ERR_CUDA;
+    bases[r] = (char*)q;
+    p->mapped.push_back((char*)q);
+  }
+  char** dbases;
+  if (!p_alloc(p, &dbases, N)) return HET_ERR_OOM;
+  cudaMemcpyAsync(dbases, bases.data(), sizeof(char*) * N, cudaMemcpyHostToDevice, st);
+  *dbases_out = dbases;
+  return HET_OK;
+}
+
+het_status_t p2p_dense_allreduce(P2PState* p, const Dev& d, float* buf, uint64_t count, ncclComm_t comm,
+                                 cudaStream_t st, int* launches) {
+  if (!p->dense) {
+    if (p->dense_failed) return HET_ERR_CAPACITY;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return HET_ERR_CAPACITY;   // set up outside capture only
+    const int N = d.world;
+    const uint64_t cap = (count + 3) & ~3ull;
+    const size_t flags = 2 * 64 * sizeof(Flag);
+    if (N > 64 || cudaMalloc(&p->dense, flags + 2 * cap * sizeof(float)) != cudaSuccess) {
+      p->dense_failed = true;
+      return HET_ERR_CAPACITY;
+    }
+    cudaMemsetAsync(p->dense, 0, flags, st);
+    char** dbases = nullptr;
+    het_status_t rc = exchange_bases(p, p->dense, N, d.rank, comm, st, &dbases);
+    if (rc) return rc;
+    DenseView& v = p->dv;
+    v.N = N; v.rank = d.rank; v.peer = dbases; v.cap = cap;
+    if (!p_alloc(p, &v.epoch, 1) || !p_alloc(p, &v.done, 2)) return HET_ERR_OOM;
+    cudaMemsetAsync(v.epoch, 0, 8, st);
+    cudaMemsetAsync(v.done, 0, 8, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
+    // every rank's flags are zero before any rank's first epoch
+    if (ncclAllReduce(v.epoch, v.epoch, 1, ncclUint64, ncclMax, comm, st) != ncclSuccess) return HET_ERR_NCCL;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
+  }
+  if (count > p->dv.cap) return HET_ERR_CAPACITY;
+  k_dense_ar<<<coop_sm_reserve(), 512, 0, st>>>(p->dv, buf, count, 1.0f / (float)d.world, d.ctl);
+  *launches += 1;
+  return HET_OK;
 }
 
 static int grid_p(int64_t units_warps) {

@@ -21,5 +21,11 @@ struct P2P;
 P2P* p2p_view_ptr(P2PState* p);
 // eviction pushes of the current update (sent with the next round)
 int p2p_pushes(P2PState* p, const Dev& d, void* evbuf, cudaStream_t st);
+// Eq. 2 dense all-reduce (mean) over peer memory; HET_ERR_CAPACITY when
+// count exceeds the staging set up by the first call (the caller falls back
+// to NCCL).  The first call allocates and exchanges the staging (collective,
+// outside graph capture).
+het_status_t p2p_dense_allreduce(P2PState* p, const Dev& d, float* buf, uint64_t count, ncclComm_t comm,
+                                 cudaStream_t st, int* launches);
 
 }  // namespace het

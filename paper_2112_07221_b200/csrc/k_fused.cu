@@ -1007,7 +1007,7 @@ int coop_sm_reserve() {
   static int r = -1;
   if (r < 0) {
     const char* e = getenv("HET_NCCL_CTAS");
-    r = e ? std::max(1, atoi(e)) : 32;
+    r = e ? std::max(1, atoi(e)) : 16;   // dense all-reduce blocks (peer memory or NCCL CTAs)
   }
   return r;
 }

@@ -78,10 +78,14 @@ def main():
     assert np.array_equal(gcg, ocg)
     np.testing.assert_allclose(gr, orows, rtol=1e-6, atol=1e-30)
     # dense all-reduce (Eq. 2): mean over workers
-    x = torch.full((1000,), float(rank + 1), device="cuda")
-    het.het_dense_allreduce(g.h, x, x.numel())
-    torch.cuda.synchronize()
-    assert torch.allclose(x, torch.full_like(x, (world + 1) / 2.0))
+    # (peer-memory one-shot mean; epochs reuse the two staging buffers; a
+    # shorter call exercises the scalar tail; a longer one falls back to NCCL)
+    for k, cnt in enumerate([1000, 1000, 998, 1000, 4096]):
+        x = torch.arange(cnt, device="cuda", dtype=torch.float32) * (rank + 1) + k
+        het.het_dense_allreduce(g.h, x, x.numel())
+        torch.cuda.synchronize()
+        want = torch.arange(cnt, device="cuda", dtype=torch.float32) * ((world + 1) / 2.0) + k
+        assert torch.allclose(x, want, rtol=1e-6, atol=1e-6), (k, cnt)
     g.close()
     dist.barrier()
     if rank == 0:
