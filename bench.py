@@ -352,7 +352,9 @@ def run_gpu(args):
     tot = sum(v["ms_per_launch"] * v["launches"] for v in kern.values()) or 1.0
     for v in kern.values():
         v["share"] = v["ms_per_launch"] * v["launches"] / tot
-    dom = max(kern, key=lambda k: kern[k]["share"]) if kern else None
+    # dominant kernel of the sparse path (the dense all-reduce runs overlapped on a side stream)
+    cand = [k for k in kern if k != "dense_allreduce"]
+    dom = max(cand, key=lambda k: kern[k]["share"]) if cand else None
     roof = None
     if dom:
         a = kern[dom]["achieved_gbs"]
@@ -442,12 +444,15 @@ def nvlink_fraction(kern, wire, world, device):
         torch.distributed.all_to_all_single(b, a)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(10):
-        torch.distributed.all_to_all_single(b, a)
-    e1.record()
-    torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / 10 * 1e-3
+    t = float("inf")
+    for _ in range(3):                                 # best of 3 trials of 10 (max over ranks)
+        torch.distributed.barrier()
+        e0.record()
+        for _ in range(10):
+            torch.distributed.all_to_all_single(b, a)
+        e1.record()
+        torch.cuda.synchronize()
+        t = min(t, max_over_ranks(e0.elapsed_time(e1) / 10 * 1e-3, world, device))
     peak = n * (world - 1) / world / t / 1e9
     sent = wire["bytes_clock_tx"] + wire["bytes_emb_tx"]
     ach = sent / (ex["ms_per_launch"] * 1e-3) / 1e9

@@ -796,8 +796,6 @@ __device__ __forceinline__ void extract_task(const Dev& s, const EvBuf& b, int t
   }
 }
 
-constexpr int EXT_IN_PLAN = UPD_WARPS;   // block 0 extracts the victims itself up to one listed block per warp
-
 __global__ void __launch_bounds__(UPD_THREADS)
 k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, int stage_rows, P2P pm, int push) {
   const P2P* pp = push ? &pm : nullptr;
@@ -816,6 +814,9 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   __syncthreads();
   const bool abort = ctl->abort;
   const int U = abort ? 0 : ctl->U;
+  // this update's plan epoch (read by every block before any grid sync;
+  // block 0 advances upd_epoch after the last one)
+  const uint32_t ep = __ldcg(&ctl->upd_epoch) + 1;
   // ---- block 0: this step's eviction plan (need, mode, LFU threshold T / K*,
   // hash maintenance), in parallel with the segment reduce of the other blocks
   if (blockIdx.x == 0) {
@@ -866,18 +867,18 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
         }
       }
       __syncthreads();
-      if (threadIdx.x == 0) { ctl->ntask = s_nt; ctl->ext_done = s_nt <= EXT_IN_PLAN; }
-      // few listed blocks (the common steady state): block 0 extracts the
-      // victim keys now, in parallel with the segment reduce, so the grid
-      // skips the extraction phase and its grid sync
-      if (s_nt <= EXT_IN_PLAN)
-        for (int task = threadIdx.x >> 5; task < s_nt; task += UPD_WARPS)
-          extract_task(s, b, task, T, ctl->Kstar, threadIdx.x & 31);
+      if (threadIdx.x == 0) ctl->ntask = s_nt;
     } else if (threadIdx.x == 0) {
       ctl->ntask = 0;
-      ctl->ext_done = 0;
     }
-    if (threadIdx.x == 0) { ctl->ext_next = 0; ctl->find_next = 0; }
+    // publish the plan: warps that finish their segment reduce extract the
+    // victim keys from a work queue while the heavier keys are still reduced
+    if (threadIdx.x == 0) {
+      ctl->ext_next = 0;
+      ctl->find_next = 0;
+      __threadfence();
+      st_release_gpu(&ctl->plan_seq, ep);
+    }
     TL_MAX(23);
   }
   __syncthreads();
@@ -898,26 +899,42 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
       for (int it = rw; it < U * S; it += nrw) segreduce_slice(s, c, G4, lr, it / S, it % S, lane);
   }
   TL_MAX(18);
-  // ---- every update done and block 0's plan + task list visible
+  // ---- the plan is out: extraction of the victim keys (LFU bitmap path),
+  // one listed bitmap block per grab of the work queue
+  {
+    if (lane == 0) {
+      const unsigned long long t0 = gtime();
+      while (ld_acquire_gpu(&ctl->plan_seq) != ep) {
+        if (gtime() - t0 > WAIT_NS) { raise_err(ctl, 6 /*HET_ERR_CUDA: plan never published*/); break; }
+        __nanosleep(32);
+      }
+    }
+    __syncwarp();
+    if (!abort && __ldcg(&ctl->emode) == 1) {
+      const uint32_t T = __ldcg(&ctl->T);
+      const int64_t Kstar = __ldcg(&ctl->Kstar);
+      const int ntask = __ldcg(&ctl->ntask);
+      for (;;) {
+        int task = 0;
+        if (lane == 0) task = atomicAdd(&ctl->ext_next, 1);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (task >= ntask) break;
+        extract_task(s, b, task, T, Kstar, lane);
+      }
+    }
+  }
+  TL_MAX(19);
+  // ---- every update done, every victim key listed
   grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->upd_epoch = ep;   // every block read it at entry
   if (S > 1) {                                  // Cache.Clock once per key, after every slice
     for (int u = gw * 32 + lane; u < U; u += nw * 32) s.cc[c.uentry[u]] += 1;
     grid.sync();
   }
   const int emode = abort ? 0 : __ldcg(&ctl->emode);
   const bool rebuild = __ldcg(&ctl->rebuild_req);
+  // ---- phase 2 (LFU bitmap path): evict, warp per victim
   if (emode == 1) {
-    // extraction of the victim keys, one listed bitmap block per warp
-    const uint32_t T = __ldcg(&ctl->T);
-    const int64_t Kstar = __ldcg(&ctl->Kstar);
-    const int ntask = __ldcg(&ctl->ntask);
-    if (!__ldcg(&ctl->ext_done))
-      for (int task = gw; task < ntask; task += nw) extract_task(s, b, task, T, Kstar, lane);
-  }
-  TL_MAX(19);
-  // ---- phase 2 (LFU bitmap path): every update done; evict, warp per victim
-  if (emode == 1) {
-    if (!__ldcg(&ctl->ext_done)) grid.sync();   // uniform: ext_done was set before the first grid sync
     TL_MAX(20);
     const int nsel = ctl->nsel;
     for (int i = gw; i < nsel; i += nw) {
