@@ -83,7 +83,7 @@ struct Ctl {
   int32_t nbucket[32];
   // light-LFU (R27): promotion candidates of the current lookup, pinned entries
   int32_t npin_cand;
-  uint32_t upd_epoch;   // fused update: completed updates (plan_seq == upd_epoch + 1 once the plan is out)
+  int32_t pad7_;
   int64_t npinned;
 };
 
@@ -174,10 +174,10 @@ __device__ __forceinline__ int32_t warp_find(const Dev& s, int64_t key, int lane
   for (int it = 0; it < (1 << 20); ++it) {
     uint64_t slot = (w + lane) & s.hmask;
     int64_t hk = s.hkey[slot];
-    int32_t val = s.hval[slot];   // issued with the key load: no dependent round trip on a hit
     unsigned m = __ballot_sync(0xffffffffu, hk == key);
     if (m) {
       int src = __ffs(m) - 1;
+      int32_t val = s.hval[slot];
       return __shfl_sync(0xffffffffu, val, src);
     }
     if (__ballot_sync(0xffffffffu, hk == HK_EMPTY)) return -1;
@@ -192,10 +192,10 @@ __device__ __forceinline__ int32_t warp_find_slot(const Dev& s, int64_t key, int
   for (int it = 0; it < (1 << 20); ++it) {
     uint64_t slot = (w + lane) & s.hmask;
     int64_t hk = s.hkey[slot];
-    int32_t val = s.hval[slot];   // issued with the key load
     unsigned m = __ballot_sync(0xffffffffu, hk == key);
     if (m) {
       int src = __ffs(m) - 1;
+      int32_t val = s.hval[slot];
       *slot_out = __shfl_sync(0xffffffffu, slot, src);
       return __shfl_sync(0xffffffffu, val, src);
     }

@@ -749,53 +749,6 @@ __device__ __forceinline__ void segreduce_slice(const Dev& s, const Call& c, con
   }
 }
 
-// Victim keys of one listed count-bitmap block (task = (count << 27) | block):
-// all set bits for counts < T, bits of keys <= K* for count T; appended to
-// b.vsel at a warp-aggregated cursor (ctl->nsel).
-__device__ __forceinline__ void extract_task(const Dev& s, const EvBuf& b, int task, uint32_t T, int64_t Kstar,
-                                             int lane) {
-  Ctl* ctl = s.ctl;
-  const int32_t code = __ldcg(&b.cand[task]);
-  const uint32_t cc = (uint32_t)code >> 27;
-  const int64_t blk = code & ((1 << 27) - 1);
-  const uint32_t* bm = s.bm + (int64_t)cc * s.bm_words;
-  uint32_t w[4];
-  int cl = 0;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r;
-    uint32_t bits = wi < s.bm_words ? __ldcg(&bm[wi]) : 0u;
-    if (cc == T) {   // keep keys <= K*
-      const int64_t k0 = wi << 5;
-      if (k0 > Kstar) bits = 0;
-      else if (k0 + 31 > Kstar) bits &= (1u << (Kstar - k0 + 1)) - 1u;
-    }
-    w[r] = bits;
-    cl += __popc(bits);
-  }
-  int incl = cl;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  if (!total) return;
-  int base = 0;
-  if (lane == 31) base = atomicAdd(&ctl->nsel, total);
-  base = __shfl_sync(0xffffffffu, base, 31);
-  int pos = base + incl - cl;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    uint32_t bits = w[r];
-    const int64_t kb = ((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r) << 5;
-    while (bits) {
-      b.vsel[pos++] = kb + (__ffs(bits) - 1);
-      bits &= bits - 1;
-    }
-  }
-}
-
 __global__ void __launch_bounds__(UPD_THREADS)
 k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, int stage_rows, P2P pm, int push) {
   const P2P* pp = push ? &pm : nullptr;
@@ -814,9 +767,6 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   __syncthreads();
   const bool abort = ctl->abort;
   const int U = abort ? 0 : ctl->U;
-  // this update's plan epoch (read by every block before any grid sync;
-  // block 0 advances upd_epoch after the last one)
-  const uint32_t ep = __ldcg(&ctl->upd_epoch) + 1;
   // ---- block 0: this step's eviction plan (need, mode, LFU threshold T / K*,
   // hash maintenance), in parallel with the segment reduce of the other blocks
   if (blockIdx.x == 0) {
@@ -871,14 +821,7 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
     } else if (threadIdx.x == 0) {
       ctl->ntask = 0;
     }
-    // publish the plan: warps that finish their segment reduce extract the
-    // victim keys from a work queue while the heavier keys are still reduced
-    if (threadIdx.x == 0) {
-      ctl->ext_next = 0;
-      ctl->find_next = 0;
-      __threadfence();
-      st_release_gpu(&ctl->plan_seq, ep);
-    }
+    if (threadIdx.x == 0) { ctl->ext_next = 0; ctl->ext_done = 0; ctl->find_next = 0; }
     TL_MAX(23);
   }
   __syncthreads();
@@ -899,42 +842,65 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
       for (int it = rw; it < U * S; it += nrw) segreduce_slice(s, c, G4, lr, it / S, it % S, lane);
   }
   TL_MAX(18);
-  // ---- the plan is out: extraction of the victim keys (LFU bitmap path),
-  // one listed bitmap block per grab of the work queue
-  {
-    if (lane == 0) {
-      const unsigned long long t0 = gtime();
-      while (ld_acquire_gpu(&ctl->plan_seq) != ep) {
-        if (gtime() - t0 > WAIT_NS) { raise_err(ctl, 6 /*HET_ERR_CUDA: plan never published*/); break; }
-        __nanosleep(32);
-      }
-    }
-    __syncwarp();
-    if (!abort && __ldcg(&ctl->emode) == 1) {
-      const uint32_t T = __ldcg(&ctl->T);
-      const int64_t Kstar = __ldcg(&ctl->Kstar);
-      const int ntask = __ldcg(&ctl->ntask);
-      for (;;) {
-        int task = 0;
-        if (lane == 0) task = atomicAdd(&ctl->ext_next, 1);
-        task = __shfl_sync(0xffffffffu, task, 0);
-        if (task >= ntask) break;
-        extract_task(s, b, task, T, Kstar, lane);
-      }
-    }
-  }
-  TL_MAX(19);
-  // ---- every update done, every victim key listed
+  // ---- every update done and block 0's plan + task list visible
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->upd_epoch = ep;   // every block read it at entry
   if (S > 1) {                                  // Cache.Clock once per key, after every slice
     for (int u = gw * 32 + lane; u < U; u += nw * 32) s.cc[c.uentry[u]] += 1;
     grid.sync();
   }
   const int emode = abort ? 0 : __ldcg(&ctl->emode);
   const bool rebuild = __ldcg(&ctl->rebuild_req);
-  // ---- phase 2 (LFU bitmap path): evict, warp per victim
   if (emode == 1) {
+    // extraction of the victim keys, one listed bitmap block per warp
+    const uint32_t T = __ldcg(&ctl->T);
+    const int64_t Kstar = __ldcg(&ctl->Kstar);
+    const int ntask = __ldcg(&ctl->ntask);
+    for (int task = gw; task < ntask; task += nw) {
+      const int32_t code = __ldcg(&b.cand[task]);
+      const uint32_t cc = (uint32_t)code >> 27;
+      const int64_t blk = code & ((1 << 27) - 1);
+      const uint32_t* bm = s.bm + (int64_t)cc * s.bm_words;
+      uint32_t w[4];
+      int cl = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r;
+        uint32_t bits = wi < s.bm_words ? __ldcg(&bm[wi]) : 0u;
+        if (cc == T) {   // keep keys <= K*
+          const int64_t k0 = wi << 5;
+          if (k0 > Kstar) bits = 0;
+          else if (k0 + 31 > Kstar) bits &= (1u << (Kstar - k0 + 1)) - 1u;
+        }
+        w[r] = bits;
+        cl += __popc(bits);
+      }
+      int incl = cl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (!total) continue;
+      int base = 0;
+      if (lane == 31) base = atomicAdd(&ctl->nsel, total);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      int pos = base + incl - cl;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        uint32_t bits = w[r];
+        const int64_t kb = ((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r) << 5;
+        while (bits) {
+          b.vsel[pos++] = kb + (__ffs(bits) - 1);
+          bits &= bits - 1;
+        }
+      }
+    }
+  }
+  TL_MAX(19);
+  // ---- phase 2 (LFU bitmap path): every update done; evict, warp per victim
+  if (emode == 1) {
+    grid.sync();
     TL_MAX(20);
     const int nsel = ctl->nsel;
     for (int i = gw; i < nsel; i += nw) {
