@@ -427,15 +427,7 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
   // the peer-memory exchange for every n; the dedup kernel follows n
   h->fused = !getenv("HET_NO_FUSED") && (d.world == 1 ? (int)n <= FUSED_LOOKUP_MAX : mgpu_p2p(h->mg) != nullptr);
   if (h->fused) {
-    // dedup: multi-CTA rank count (n <= 8192) or the one-CTA radix sort
-    // (n <= 16384; HET_DD=radix / rank forces one of them where both apply)
-    const char* dd_env = getenv("HET_DD");
-    const bool radix = dd_radix_ok((int)n) &&
-                       (dd_env ? std::strcmp(dd_env, "radix") == 0 : !fused_ok(d, (int)n));
-    if (radix) {
-      Prof p(h, "dedup", st);
-      h->launches += launch_dd_radix(d, c, (int)n, clock_t, 1, st);
-    } else if (fused_ok(d, (int)n)) {
+    if (fused_ok(d, (int)n)) {
       Prof p(h, "dedup", st);
       h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st);
     } else {

@@ -367,8 +367,6 @@ void launch_hash_rebuild(const Dev& s, cudaStream_t st);
 // fused single-GPU step (k_fused.cu)
 bool fused_ok(const Dev& s, int n);
 int launch_pin_apply(const Dev& s, cudaStream_t st);
-bool dd_radix_ok(int n);
-int launch_dd_radix(const Dev& s, const Call& c, int n, uint64_t t, int lookup, cudaStream_t st);
 constexpr int FUSED_LOOKUP_MAX = 16384;   // N = 1: fused lookup/update up to this n
 int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st);
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st);

@@ -106,14 +106,12 @@ def toy_keys(t, B=128, i=0):
     (LRU, 100, 1, 0.3),
     (LFU, 10, 1, 0.0),       # no cache: HET Hybrid mode (R10)
 ])
-@pytest.mark.parametrize("fused", [True, False, "radix"])
+@pytest.mark.parametrize("fused", [True, False])
 def test_toy_full_parity(policy, s, persist, frac, fused, monkeypatch):
-    """fused: the 3-kernel single-GPU step (radix: with the one-CTA radix
-    dedup); unfused: the per-phase kernels (the multi-GPU / large-batch path)."""
+    """fused: the 3-kernel single-GPU step; unfused: the per-phase kernels
+    (the multi-GPU / large-batch path)."""
     if not fused:
         monkeypatch.setenv("HET_NO_FUSED", "1")
-    if fused == "radix":
-        monkeypatch.setenv("HET_DD", "radix")
     R, D, T = 1000, 8, 200
     p = Pair(R, D, frac, s, policy, persist)
     p.g_policy = policy
@@ -193,19 +191,16 @@ def test_ragged_and_degenerate_calls():
     p.finish()
 
 
-@pytest.mark.parametrize("dd", ["radix", "rank"])
-def test_dedup_paths_sizes(dd, monkeypatch):
-    """Both fused-path dedup kernels (one-CTA radix sort, multi-CTA rank count)
-    at sizes around their item/tile boundaries, with duplicates, keys 0 and
-    R-1 and ragged tails: unique/inverse/perm/seg_off bit-exact vs the oracle."""
-    monkeypatch.setenv("HET_DD", dd)
+def test_dedup_paths_sizes():
+    """The fused path's dedup kernels (multi-CTA rank count up to 8192, the
+    cluster bitonic sort beyond) at sizes around their tile boundaries, with
+    duplicates, keys 0 and R-1 and ragged tails: unique/inverse/perm/seg_off
+    bit-exact vs the oracle."""
     R, D = 1 << 20, 4
     p = Pair(R, D, 0.01, 10, LFU, n_max=16384)
     p.g_policy = LFU
     rng = np.random.default_rng(7)
     sizes = [1, 2, 31, 32, 33, 1023, 4095, 4096, 4097, 8191, 8192, 8193, 12000, 16383, 16384]
-    if dd == "rank":
-        sizes = [s for s in sizes if s <= 8192]
     for t, n in enumerate(sizes):
         keys = rng.integers(0, R, size=n).astype(np.int64)
         keys[rng.integers(0, n, size=max(1, n // 4))] = keys[0]           # a heavy duplicate
