@@ -427,7 +427,7 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
   // the peer-memory exchange for every n; the dedup kernel follows n
   h->fused = !getenv("HET_NO_FUSED") && (d.world == 1 ? (int)n <= FUSED_LOOKUP_MAX : mgpu_p2p(h->mg) != nullptr);
   if (h->fused) {
-    if (fused_dd_ok((int)n) && !getenv("HET_DD_CLUSTER")) {   // HET_DD_CLUSTER: the cluster bitonic dedup
+    if (fused_ok(d, (int)n)) {
       Prof p(h, "dedup", st);
       h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st);
     } else {

@@ -368,7 +368,6 @@ void launch_hash_rebuild(const Dev& s, cudaStream_t st);
 bool fused_ok(const Dev& s, int n);
 int launch_pin_apply(const Dev& s, cudaStream_t st);
 constexpr int FUSED_LOOKUP_MAX = 16384;   // N = 1: fused lookup/update up to this n
-bool fused_dd_ok(int n);   // k_dd_fused / k_dd_fused_l cover n (<= 16384)
 int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st);
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st);
 // SMs left free by the cooperative kernels for NCCL's blocks at N > 1

@@ -210,148 +210,6 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
   TL_MAX(4);
 }
 
-// ------------------------------------------------------------------ K_dd, 8192 < n <= 16384
-// The same rank-count dedup for the Reddit-shaped batches (14,208 ids):
-// 1024-thread blocks, one wave of at most 148 blocks, block b ranks the
-// contiguous positions [b*E, (b+1)*E) (up to DL_MINE per lane) against all n
-// composites in shared memory (n*8 B <= 128 KB), 32 warps splitting the
-// compares; the last block finishes with 16 items per thread.
-constexpr int DL_THREADS = 1024;
-constexpr int DL_WARPS = DL_THREADS / 32;
-constexpr int DL_ITEMS = 16;      // 16 x 1024 = 16384
-constexpr int DL_MINE = 4;        // positions per lane: E <= 128 per block
-constexpr int DL_MAX = DL_THREADS * DL_ITEMS;
-
-__global__ void __launch_bounds__(DL_THREADS)
-k_dd_fused_l(const int64_t* __restrict__ keys, int n, int E, int pbits, Dev s, Call c, uint64_t t, int lookup) {
-  extern __shared__ uint64_t comp[];
-  int* part = reinterpret_cast<int*>(comp + DL_MAX);   // [DL_WARPS][DL_MINE * 32]
-  __shared__ int warp_sums[32];
-  __shared__ int s_last;
-  Ctl* ctl = s.ctl;
-  int bad = 0;
-  {
-    int64_t kk[DL_ITEMS];
-#pragma unroll
-    for (int i = 0; i < DL_ITEMS; ++i) {
-      const int q = threadIdx.x + i * DL_THREADS;
-      kk[i] = q < n ? __ldg(&keys[q]) : 0;
-    }
-#pragma unroll
-    for (int i = 0; i < DL_ITEMS; ++i) {
-      const int q = threadIdx.x + i * DL_THREADS;
-      if (q < n) {
-        if (kk[i] < 0 || kk[i] >= s.R) bad = 1;
-        comp[q] = ((uint64_t)kk[i] << pbits) | (uint64_t)q;
-      }
-    }
-  }
-  bad = __syncthreads_or(bad);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {   // per-call begin
-    if (lookup) {
-      if (t == CLOCK_AUTO) { t = ctl->t_auto; ctl->t_auto = t + 1; }
-      ctl->t_cur = t;
-      ctl->lk_seq = ctl->lk_seq + 1;
-      s.cnt[C_LOOKUPS] += 1;
-      s.cnt[C_KEYS] += (unsigned long long)n;
-    }
-    ctl->abort = 0;
-    if (bad) { raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/); ctl->U = 0; c.seg_off[0] = 0; }
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int p0 = blockIdx.x * E, p1 = min(n, p0 + E);
-  if (!bad) {
-    uint64_t mine[DL_MINE];
-    int cnt[DL_MINE];
-#pragma unroll
-    for (int m = 0; m < DL_MINE; ++m) {
-      const int p = p0 + m * 32 + lane;
-      mine[m] = p < p1 ? comp[p] : ~0ull;
-      cnt[m] = 0;
-    }
-    const int per = (n + DL_WARPS - 1) / DL_WARPS;
-    const int q0 = wid * per, q1 = min(n, q0 + per);
-    const int nm = (p1 - p0 + 31) >> 5;           // live position groups of this block (uniform)
-    if (nm <= 1) {
-#pragma unroll 8
-      for (int q = q0; q < q1; ++q) cnt[0] += comp[q] < mine[0];
-    } else if (nm == 2) {
-#pragma unroll 4
-      for (int q = q0; q < q1; ++q) { const uint64_t x = comp[q]; cnt[0] += x < mine[0]; cnt[1] += x < mine[1]; }
-    } else {
-#pragma unroll 4
-      for (int q = q0; q < q1; ++q) {
-        const uint64_t x = comp[q];
-#pragma unroll
-        for (int m = 0; m < DL_MINE; ++m) cnt[m] += x < mine[m];
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < DL_MINE; ++m) part[wid * DL_MINE * 32 + m * 32 + lane] = cnt[m];
-    __syncthreads();
-    if (wid < DL_MINE) {
-      const int p = p0 + wid * 32 + lane;
-      if (p < p1) {
-        int r = 0;
-        for (int w = 0; w < DL_WARPS; ++w) r += part[w * DL_MINE * 32 + wid * 32 + lane];
-        c.sortbuf0[r] = comp[p];
-        c.perm[r] = p;
-      }
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&ctl->dd_done, 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  if (threadIdx.x == 0) ctl->dd_done = 0;
-  if (bad) return;
-  // ---- last block: head flags / scan / outputs (warp w owns a contiguous segment)
-  const uint64_t* sorted = c.sortbuf0;
-  const int seg = ((n + DL_WARPS - 1) / DL_WARPS + 31) & ~31;
-  const int s0 = wid * seg, s1 = min(n, s0 + seg);
-  uint64_t x[DL_ITEMS];
-  unsigned hm[DL_ITEMS];
-  uint64_t prevlast = (s0 > 0 && s0 <= n) ? __ldcg(&sorted[s0 - 1]) : ~0ull;
-#pragma unroll
-  for (int i = 0; i < DL_ITEMS; ++i) {
-    const int j = s0 + i * 32 + lane;
-    x[i] = j < s1 ? __ldcg(&sorted[j]) : ~0ull;
-  }
-  int wcnt = 0;
-#pragma unroll
-  for (int i = 0; i < DL_ITEMS; ++i) {
-    const int j = s0 + i * 32 + lane;
-    uint64_t prev = __shfl_up_sync(0xffffffffu, x[i], 1);
-    if (lane == 0) prev = prevlast;
-    const bool head = j < s1 && (j == 0 || (x[i] >> pbits) != (prev >> pbits));
-    hm[i] = __ballot_sync(0xffffffffu, head);
-    wcnt += __popc(hm[i]);
-    prevlast = __shfl_sync(0xffffffffu, x[i], 31);
-  }
-  if (lane == 0) warp_sums[wid] = wcnt;
-  __syncthreads();
-  int base = 0, tot = 0;
-  for (int w = 0; w < DL_WARPS; ++w) {
-    const int v = warp_sums[w];
-    if (w < wid) base += v;
-    tot += v;
-  }
-  int run = base - 1;
-#pragma unroll
-  for (int i = 0; i < DL_ITEMS; ++i) {
-    const int j = s0 + i * 32 + lane;
-    const int u = run + __popc(hm[i] & ((2u << lane) - 1u));
-    if (j < s1 && ((hm[i] >> lane) & 1u)) {
-      c.uniq[u] = (int64_t)(x[i] >> pbits);
-      c.seg_off[u] = j;
-    }
-    run += __popc(hm[i]);
-  }
-  if (threadIdx.x == 0) { c.seg_off[tot] = n; ctl->U = tot; }
-}
-
 // ------------------------------------------------------------------ K_look
 // LFU threshold (T, K*) for this step, one CTA (the last block of k_lookup_fused):
 // T = the smallest count whose cumulative population reaches `need`, K* = the
@@ -1102,27 +960,12 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
 constexpr int FUSED_MAX = 8192;
 
 bool fused_ok(const Dev& s, int n) { return n <= FUSED_MAX; }
-bool fused_dd_ok(int n) { return n <= DL_MAX; }
 
 int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_dd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, FUSED_MAX * 8);
-    cudaFuncSetAttribute(k_dd_fused_l, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         DL_MAX * 8 + DL_WARPS * DL_MINE * 32 * 4);
     attr = true;
-  }
-  if (n > FUSED_MAX) {   // 8192 < n <= 16384: one wave of 1024-thread blocks
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int E = (n + sms - 1) / sms;
-    E = (E + 31) & ~31;
-    if (E > DL_MINE * 32) E = DL_MINE * 32;
-    const int blocks = (n + E - 1) / E;
-    k_dd_fused_l<<<blocks, DL_THREADS, (size_t)DL_MAX * 8 + DL_WARPS * DL_MINE * 32 * 4, st>>>(c.keys, n, E, pbits,
-                                                                                               s, c, t, lookup);
-    return 1;
   }
   int blocks = std::max(1, (n + 31) / 32);
   k_dd_fused<<<blocks, DDF_THREADS, (size_t)std::max(n, 1) * 8, st>>>(c.keys, n, pbits, s, c, t, lookup);
