@@ -571,9 +571,11 @@ k_probe_build(Dev s, Call c, P2P m) {
 // install + gather for one unique key (warp): finish the status of a
 // clock-checked hit from the owner's answer, install a fetched row, scatter
 // the key's row to its occurrences (Cache.Get)
+// mnext: this warp's next index into its block's free-stack reservation
+// (misses in u order, descending); nullptr: one atomic pop per miss
 __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, const P2P& m, int u, int lane,
                                                    float* __restrict__ out, unsigned* bc, int* dpop,
-                                                   unsigned long long* sb) {
+                                                   unsigned long long* sb, int* mnext = nullptr) {
   Ctl* ctl = s.ctl;
   const int D4 = s.D >> 2;
   uint8_t st = c.status[u];
@@ -596,8 +598,12 @@ __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, 
     if (!(st == ST_NEEDQ && valid)) {
       if (st == ST_MISS) {
         int32_t idx = 0;
-        if (lane == 0) idx = atomicSub(&ctl->ftop, 1) - 1;
-        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (mnext) {
+          idx = (*mnext)--;                   // warp-uniform: the block reserved these entries
+        } else {
+          if (lane == 0) idx = atomicSub(&ctl->ftop, 1) - 1;
+          idx = __shfl_sync(0xffffffffu, idx, 0);
+        }
         if (idx < 0) {
           if (lane == 0) raise_err(ctl, 4);
           ok = false;
@@ -752,7 +758,26 @@ k_exchange(Dev s, Call c, P2P m, float* __restrict__ out) {
   __syncthreads();
   PTL(10);
   const int U2 = (s_ok && !ctl->abort) ? ctl->U : 0;
-  for (int u = gw; u < U2; u += nw) install_gather_key(s, c, m, u, lane, out, bc, dpop, sb);
+  {
+    // the block's misses take one free-stack reservation (one atomic per
+    // block instead of one per miss: the Reddit-shaped batches miss ~7K keys)
+    __shared__ int s_mcount, s_mbase;
+    if (threadIdx.x == 0) s_mcount = 0;
+    __syncthreads();
+    int my = 0;
+    for (int i0 = 0; gw + i0 * nw < U2; i0 += 32) {
+      const int uu = gw + (i0 + lane) * nw;
+      my += __popc(__ballot_sync(0xffffffffu, uu < U2 && c.status[uu] == ST_MISS));
+    }
+    int woff = 0;
+    if (lane == 0 && my) woff = atomicAdd(&s_mcount, my);
+    woff = __shfl_sync(0xffffffffu, woff, 0);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_mcount) s_mbase = atomicSub(&ctl->ftop, s_mcount);
+    __syncthreads();
+    int mnext = s_mbase - 1 - woff;
+    for (int u = gw; u < U2; u += nw) install_gather_key(s, c, m, u, lane, out, bc, dpop, sb, &mnext);
+  }
   PTL(11);
   __syncthreads();
   install_gather_flush(s, bc, dpop, sb);

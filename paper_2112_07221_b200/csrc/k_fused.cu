@@ -323,13 +323,13 @@ __device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_su
 }
 
 __global__ void __launch_bounds__(LK_WARPS * 32)
-k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
+k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
   __shared__ unsigned bc[4];
   __shared__ int dpop[LFU_CB_MAX];
-  __shared__ int s_last;
-  __shared__ int warp_sums_i[32];
-  __shared__ long long warp_sums[32];
+  __shared__ int s_nmiss, s_base;
+  __shared__ uint32_t s_minp;
   if (threadIdx.x < 4) bc[threadIdx.x] = 0;
+  if (threadIdx.x == 0) { s_nmiss = 0; s_minp = 0xFFFFFFFFu; }
   dpop_init(dpop);
   TL_MIN(8); TL_MAX(9);
   __syncthreads();
@@ -338,19 +338,26 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
   const int u = blockIdx.x * LK_WARPS + (threadIdx.x >> 5);
   const int U = ctl->U;
   const int D4 = s.D >> 2;
-  if (!ctl->abort && u < U) {
-    const int64_t key = c.uniq[u];
-    const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
-    const int cnt = j1 - j0;
-    const int pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
-    uint32_t cntk = 0, gpre = 0;
+  const bool live = !ctl->abort && u < U;
+  // ---- phase A (warp per unique key): Find, CheckValid, touch; with agg (large
+  // n: thousands of misses) a miss takes a slot of the block's free-entry
+  // reservation -- one atomic per block between the phases instead of one per miss
+  int64_t key = 0;
+  int j0 = 0, cnt = 0, pos_lane = 0, moff = 0;
+  int32_t e = -1;
+  uint8_t st = ST_HIT;
+  uint32_t ecs = 0, ecc = 0, cntk = 0, gpre = 0, mprim = 0;
+  if (live) {
+    key = c.uniq[u];
+    j0 = c.seg_off[u];
+    cnt = c.seg_off[u + 1] - j0;
+    pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
     if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
     if (lane == 1 && s.s != S_INF) gpre = s.cg[key];
-    int32_t e = warp_find(s, key, lane);
+    e = warp_find(s, key, lane);
     gpre = __shfl_sync(0xffffffffu, gpre, 1);
     TL_MAX(13);
-    uint8_t st = ST_MISS;
-    uint32_t ecs = 0, ecc = 0;
+    st = ST_MISS;
     if (e >= 0) { ecs = s.cs[e]; ecc = s.cc[e]; }
     if (lane == 0) {
       // light-LFU: a pinned entry skips the frequency maintenance
@@ -371,11 +378,32 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
         } else {
           s.eprim[e] = (uint32_t)ctl->t_cur;
         }
+      } else {
+        mprim = s.policy == 0 ? (s.lfu_persist ? cntk : 1u) : (uint32_t)ctl->t_cur;
+        if (agg) {
+          moff = atomicAdd(&s_nmiss, 1);
+          atomicMin(&s_minp, mprim);
+        } else {
+          moff = atomicSub(&ctl->ftop, 1) - 1;      // the entry's free-stack index
+          atomicMin(&ctl->min_install, mprim);
+        }
       }
       c.status[u] = st;
       atomicAdd(&bc[st == ST_HIT ? 0 : st == ST_EXP1 ? 1 : st == ST_EXP2 ? 2 : 3], 1u);
     }
     st = __shfl_sync(0xffffffffu, st, 0);
+    moff = __shfl_sync(0xffffffffu, moff, 0);
+  }
+  if (agg) {                                 // uniform per launch
+    __syncthreads();
+    if (threadIdx.x == 0 && s_nmiss) {       // the block's misses: one free-stack pop, one min_install
+      s_base = atomicSub(&ctl->ftop, s_nmiss);
+      atomicMin(&ctl->min_install, s_minp);
+    }
+    __syncthreads();
+  }
+  // ---- phase B: sync push / fetch / install, Get scatter
+  if (live) {
     float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
     if (st != ST_HIT) {
       uint32_t g = gpre;
@@ -387,10 +415,8 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
           g = g > ecc ? g : ecc;
           if (lane == 0) s.cg[key] = g;
         }
-      } else {          // miss: free entry + hash insert
-        int32_t idx = 0;
-        if (lane == 0) idx = atomicSub(&ctl->ftop, 1) - 1;
-        idx = __shfl_sync(0xffffffffu, idx, 0);
+      } else {          // miss: the reserved free entry + hash insert
+        const int idx = agg ? s_base - 1 - moff : moff;
         if (idx < 0) {
           if (lane == 0) raise_err(ctl, 4 /*HET_ERR_CAPACITY*/);
           e = -1;
@@ -399,10 +425,8 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out) {
           warp_insert(s, key, e, lane);
           if (lane == 0) {
             s.ekey[e] = key;
-            uint32_t prim = s.policy == 0 ? (s.lfu_persist ? cntk : 1u) : (uint32_t)ctl->t_cur;
-            s.eprim[e] = prim;
-            if (s.policy == 0) { lfu_move(s, key, EP_FREE, prim, dpop); pin_candidate(s, key, e, prim); }
-            atomicMin(&ctl->min_install, prim);
+            s.eprim[e] = mprim;
+            if (s.policy == 0) { lfu_move(s, key, EP_FREE, mprim, dpop); pin_candidate(s, key, e, mprim); }
           }
         }
       }
@@ -582,9 +606,12 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
 // Evict push of one resident entry at N = 1 (warp-cooperative) + delete + free
 // push != nullptr (N > 1): the Evict push goes to the owner's inbox, carried
 // by the next exchange round; otherwise the local server applies it now
+// vi: the victim's export index; fpos: the free-stack slot its entry goes to
+// (the caller reserved [ftop, ftop + victims) once: no per-victim atomics on
+// the shared cursors; tombstones are counted per block in *s_tomb)
 __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_t e, int64_t key, uint64_t slot,
                                             int lane, int* dpop, unsigned* s_dirty, unsigned* s_ev,
-                                            const P2P* push = nullptr) {
+                                            unsigned* s_tomb, int vi, int64_t fpos, const P2P* push = nullptr) {
   Ctl* ctl = s.ctl;
   const uint32_t ecs = s.cs[e], ecc = s.cc[e], prim = s.eprim[e];
   const bool dirty = ecc > ecs;
@@ -606,15 +633,14 @@ __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_
     if (push && dirty) atomicAdd(&s.cnt[C_BEMB_TX], 16ull + 4ull * s.D);
     if (dirty && !push) { uint32_t g = s.cg[key]; s.cg[key] = g > ecc ? g : ecc; }
     s.hkey[slot] = HK_TOMB;
-    atomicAdd(&ctl->n_tomb, 1);
-    int vi = atomicAdd(&ctl->nvict, 1);
+    atomicAdd(s_tomb, 1u);
     b.vkeys[vi] = key;
     b.vdirty[vi] = dirty ? 1 : 0;
     if (s.policy == 0) lfu_move(s, key, prim, EP_FREE, dpop);
     unpin_count(s, prim);
     s.eprim[e] = EP_FREE;
     s.ekey[e] = -1;
-    s.fstack[atomicAdd(&ctl->ftop, 1)] = e;
+    s.fstack[fpos] = e;
     atomicAdd(s_ev, 1u);
     if (dirty) atomicAdd(s_dirty, 1u);
   }
@@ -756,11 +782,11 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   __shared__ uint32_t h[NBIN];
   __shared__ uint64_t bars[UPD_WARPS];
   __shared__ int dpop[LFU_CB_MAX];
-  __shared__ unsigned s_dirty, s_ev;
+  __shared__ unsigned s_dirty, s_ev, s_tomb;
   cg::grid_group grid = cg::this_grid();
   Ctl* ctl = s.ctl;
   dpop_init(dpop);
-  if (threadIdx.x == 0) { s_dirty = 0; s_ev = 0; }
+  if (threadIdx.x == 0) { s_dirty = 0; s_ev = 0; s_tomb = 0; }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) { mbar_init(&bars[wid], 1); fence_mbar_init(); }
   TL_MIN(16); TL_MAX(17);
@@ -900,14 +926,17 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   TL_MAX(19);
   // ---- phase 2 (LFU bitmap path): every update done; evict, warp per victim
   if (emode == 1) {
+    const int64_t ftop0 = __ldcg(&ctl->ftop);   // stable during the update; read before the grid sync
     grid.sync();
     TL_MAX(20);
     const int nsel = ctl->nsel;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->ftop = (int32_t)(ftop0 + nsel); ctl->nvict = nsel; }
     for (int i = gw; i < nsel; i += nw) {
       const int64_t key = __ldcg(&b.vsel[i]);
       uint64_t slot = 0;
       const int32_t e = warp_find_slot(s, key, lane, &slot);
-      if (e >= 0) evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev, pp);
+      if (e >= 0) evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev, &s_tomb, i, ftop0 + i, pp);
+      else if (lane == 0) raise_err(ctl, 3 /*HET_ERR_PROTOCOL: a listed victim is not resident*/);
     }
   }
   // ---- generic selection (LRU, LFU fallback, evict-all) after all updates
@@ -915,16 +944,15 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
     generic_select(s, b, reinterpret_cast<uint64_t*>(dyn), h, grid);
     grid.sync();
     const int nv = ctl->nvict;
-    // nvict is reused as the export cursor by evict_entry: reset once, grid-wide
+    const int64_t ftop0 = __ldcg(&ctl->ftop);
     grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->nvict = 0;
-    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->ftop = (int32_t)(ftop0 + nv);
     for (int i = gw; i < nv; i += nw) {
       const int32_t e0 = b.victims[i];
       const int64_t key = s.ekey[e0];
       uint64_t slot = 0;
       int32_t e = warp_find_slot(s, key, lane, &slot);
-      evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev, pp);
+      evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev, &s_tomb, i, ftop0 + i, pp);
     }
   }
   TL_MAX(21);
@@ -933,6 +961,7 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   if (threadIdx.x == 0) {
     if (s_ev) atomicAdd(&s.cnt[C_EVICTIONS], (unsigned long long)s_ev);
     if (s_dirty) atomicAdd(&s.cnt[C_DIRTY_PUSHES], (unsigned long long)s_dirty);
+    if (s_tomb) atomicAdd(&ctl->n_tomb, (int)s_tomb);
   }
   // ---- hash maintenance (rare): rebuild from the resident entries
   if (rebuild) {
@@ -957,6 +986,7 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
 }
 
 // ------------------------------------------------------------------ launchers
+constexpr int FUSED_MAX_DD_RANK = 8192;
 constexpr int FUSED_MAX = 8192;
 
 bool fused_ok(const Dev& s, int n) { return n <= FUSED_MAX; }
@@ -982,7 +1012,8 @@ int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st
     return 1;
   }
   int blocks = std::max(1, (c.n + LK_WARPS - 1) / LK_WARPS);
-  k_lookup_fused<<<blocks, LK_WARPS * 32, 0, st>>>(s, c, out);
+  const int agg = c.n > FUSED_MAX_DD_RANK;   // many misses: block-aggregated free-stack pops
+  k_lookup_fused<<<blocks, LK_WARPS * 32, 0, st>>>(s, c, out, agg);
   return 1;
 }
 
