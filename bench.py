@@ -86,7 +86,10 @@ def ncu_traffic(phase, world):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
     phase's kernel from the committed `ncu --set full` capture of this workload
     (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), else None.
-    Cold-cache, replayed launches: compare with `achieved`'s algorithmic bytes."""
+    Cold-cache, replayed launches: compare with `achieved`'s algorithmic bytes.
+    The capture is of the default workload (WDL at N = 1) only."""
+    if CFG.get("name") not in ("WDL", "DCN"):
+        return None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
