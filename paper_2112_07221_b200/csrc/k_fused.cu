@@ -60,6 +60,13 @@ extern "C" int het_debug_timeline(unsigned long long* out, int marks, int warps)
 #define TL_MAX(i) do {} while (0)
 #endif
 
+// Programmatic dependent launch (PDL): the next kernel of the step is
+// launched while this one still runs (its blocks park in griddepcontrol.wait
+// until this grid has completed and its writes are visible), hiding the
+// launch gap between the three kernels.  HET_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 constexpr int DDF_THREADS = 512;
 constexpr int DDF_WARPS = DDF_THREADS / 32;
 constexpr int DDF_ITEMS = 16;   // FUSED_MAX / DDF_THREADS (elements per lane in the finish)
@@ -96,6 +103,7 @@ __device__ __forceinline__ int block_scan_int(int x, int* warp_sums, int* tot) {
 // ------------------------------------------------------------------ K_dd
 __global__ void __launch_bounds__(DDF_THREADS)
 k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, uint64_t t, int lookup) {
+  pdl_trigger();
   extern __shared__ uint64_t comp[];
   __shared__ int part[DDF_WARPS][32];
   __shared__ int warp_sums[32];
@@ -324,6 +332,8 @@ __device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_su
 
 __global__ void __launch_bounds__(LK_WARPS * 32)
 k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned bc[4];
   __shared__ int dpop[LFU_CB_MAX];
   __shared__ int s_nmiss, s_base;
@@ -480,6 +490,8 @@ struct LkMeta { int64_t key; int32_t e; int32_t j0; int32_t cnt; uint32_t g; uin
 
 __global__ void __launch_bounds__(LK_WARPS * 32)
 k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned bc[4];
   __shared__ int dpop[LFU_CB_MAX];
   __shared__ LkMeta meta[LK_WARPS];
@@ -777,6 +789,7 @@ __device__ __forceinline__ void segreduce_slice(const Dev& s, const Call& c, con
 
 __global__ void __launch_bounds__(UPD_THREADS)
 k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, int stage_rows, P2P pm, int push) {
+  pdl_wait();
   const P2P* pp = push ? &pm : nullptr;
   extern __shared__ float4 dyn[];
   __shared__ uint32_t h[NBIN];
@@ -1002,18 +1015,53 @@ int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, i
   return 1;
 }
 
+// HET_PDL: 0 off, 1 dedup -> lookup (default), 2 also lookup -> cooperative update
+static int pdl_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("HET_PDL");
+    m = e ? atoi(e) : 1;
+  }
+  return m;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), int blocks, int threads, size_t smem, cudaStream_t st, bool pdl, bool coop,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (coop) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st) {
   const int D4 = (int)s.D / 4;
   if (D4 >= 256 && D4 % 128 == 0) {            // wide rows: G warps per key (a power of two)
     int G = 1;
     while (G * 2 <= std::min(LK_WARPS, D4 / 128)) G *= 2;
     const int blocks = std::max(1, (c.n + LK_WARPS / G - 1) / (LK_WARPS / G));
-    k_lookup_wide<<<blocks, LK_WARPS * 32, 0, st>>>(s, c, out, G);
+    launch_pdl(k_lookup_wide, blocks, LK_WARPS * 32, 0, st, pdl_mode() >= 1, false, s, c, out, G);
     return 1;
   }
   int blocks = std::max(1, (c.n + LK_WARPS - 1) / LK_WARPS);
   const int agg = c.n > FUSED_MAX_DD_RANK;   // many misses: block-aggregated free-stack pops
-  k_lookup_fused<<<blocks, LK_WARPS * 32, 0, st>>>(s, c, out, agg);
+  launch_pdl(k_lookup_fused, blocks, LK_WARPS * 32, 0, st, pdl_mode() >= 1, false, s, c, out, agg);
   return 1;
 }
 
@@ -1055,7 +1103,10 @@ int launch_update_fused(const Dev& s, const Call& c, const float* grads, float l
   int push = 0;
   if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
   void* args[] = {(void*)&sd, (void*)&cd, (void*)&grads, (void*)&lr, (void*)&b, (void*)&sr, (void*)&pm, (void*)&push};
-  cudaLaunchCooperativeKernel((void*)k_update_fused, dim3(coop_blocks), dim3(UPD_THREADS), args, smem, st);
+  if (pdl_mode() >= 2)
+    launch_pdl(k_update_fused, coop_blocks, UPD_THREADS, smem, st, true, true, sd, cd, grads, lr, b, sr, pm, push);
+  else
+    cudaLaunchCooperativeKernel((void*)k_update_fused, dim3(coop_blocks), dim3(UPD_THREADS), args, smem, st);
   return 1;
 }
 
