@@ -31,6 +31,15 @@
  * Collectives: with N > 1, het_lookup, het_update, het_evict, het_sync,
  * het_read_global and het_dense_allreduce are collective — every rank calls
  * them in the same order with the same clock (n may differ, including 0).
+ *
+ * Loopback group (het_group_*): N workers in ONE process on ONE device, with
+ * the same per-worker state, kernels and peer-memory exchange records as N
+ * processes on N GPUs, but the inboxes are plain device allocations shared by
+ * pointer (no CUDA IPC, no NCCL) and each collective call is driven phase by
+ * phase over the members -- phase k of every worker before phase k+1 of any --
+ * so no kernel ever waits for a flag another kernel has not yet set.  Used to
+ * test the N-worker protocol (CheckValid condition (2), owner-side sync/fetch,
+ * carried eviction pushes, Eq. 2) on a single GPU.
  */
 #ifndef HET_H
 #define HET_H
@@ -79,6 +88,8 @@ typedef struct {
   int lfu_persist;             /* 1 (default): LFU counts persist across evictions (R7); 0: reset */
   int debug_log;               /* reserved */
   uint32_t pin_threshold;      /* HET_LIGHT_LFU promotion count; 0 = default 64 */
+  uint64_t dense_max;          /* N > 1: floats of the peer-memory dense all-reduce staging, set up at
+                                  create (0 = default 2^22); larger het_dense_allreduce calls take NCCL */
 } het_opts_t;
 
 typedef struct {
@@ -118,7 +129,13 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
                         float* out, het_stream_t stream);
 
 /* Het.Write (Alg. 3) for the keys of the immediately preceding
- * het_lookup (same n; the lookup's dedup is reused): per unique key
+ * het_lookup (a write of keys the read did not return is a
+ * protocol violation).  n != the lookup's n: HET_ERR_PROTOCOL, returned at
+ * once.  `keys` is the lookup's pointer: accepted as is (the library reads it
+ * no further).  Any other buffer is compared on the device with the lookup's
+ * dedup, position by position; a mismatch latches HET_ERR_PROTOCOL (sticky,
+ * reported by het_check / het_sync) and the update is skipped entirely (no
+ * partial mutation).  The lookup's dedup is reused: per unique key
  * acc = sum of grads[pos] in ascending position (R11), delta = -lr * acc,
  * v += delta, pending += delta, c_c += 1; then the
  * overflow Evict() (R9).  grads: float32[n][D]. */
@@ -169,6 +186,39 @@ het_status_t het_profile_enable(het_cache_t h, int on);
 /* Fills up to cap (name, total ms, launches) records; returns count in *k. */
 het_status_t het_profile_read(het_cache_t h, char (*names)[32], double* ms, uint64_t* launches,
                               uint32_t cap, uint32_t* k);
+
+/* ---- loopback group (see "Loopback group" above) ----
+ * het_group_create: N (2..16) workers rank 0..N-1 on the current device, all
+ * with the given arguments; out[N] receives the handles in rank order.  The
+ * handles are used with het_group_* (every member, rank order, in `hs`) and
+ * with the non-collective calls (het_stats, het_check, het_read_global of
+ * owned keys, het_debug_*); het_lookup / het_update / het_evict / het_sync /
+ * het_dense_allreduce on a member return HET_ERR_PROTOCOL.  Destroy every
+ * member with het_cache_destroy.  keys[i], n[i], out[i], grads[i], bufs[i]
+ * are worker i's arguments of the corresponding single-worker call. */
+het_status_t het_group_create(uint32_t N, uint64_t rows, uint32_t D, double cache_frac, uint32_t s,
+                              het_policy_t policy, const het_opts_t* opt, het_stream_t stream,
+                              het_cache_t* out);
+/* Alg. 2 for every worker: dedup; probe + request build; owner
+ * link; owner process (U4 of the previous update, CheckValid condition (2)
+ * P:448, sync pushes P:442-443, responses P:439); install + Get. */
+het_status_t het_group_lookup(const het_cache_t* hs, uint32_t N, const int64_t* const* keys,
+                              const uint32_t* n, uint64_t clock_t, float* const* out,
+                              het_stream_t stream);
+/* Alg. 3 for every worker; eviction pushes go to the owners'
+ * inboxes and are applied by the next round (U4 precedes the next L3). */
+het_status_t het_group_update(const het_cache_t* hs, uint32_t N, const int64_t* const* keys,
+                              const uint32_t* n, const float* const* grads, float lr,
+                              het_stream_t stream);
+/* Cache.Evict for every worker; keys == NULL: overflow Evict(). */
+het_status_t het_group_evict(const het_cache_t* hs, uint32_t N, const int64_t* const* keys,
+                             const uint32_t* n, het_stream_t stream);
+/* End-of-run flush (R16) of every worker; synchronises `stream`. */
+het_status_t het_group_sync(const het_cache_t* hs, uint32_t N, het_stream_t stream);
+/* Eq. 2: bufs[i][0..count) <- mean over the workers, bitwise equal
+ * on every worker; count must fit the staging (opts.dense_max). */
+het_status_t het_group_dense_allreduce(const het_cache_t* hs, uint32_t N, float* const* bufs,
+                                       uint64_t count, het_stream_t stream);
 
 het_status_t het_cache_destroy(het_cache_t h);
 const char* het_last_error(het_cache_t h);

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <memory>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -31,6 +32,14 @@ struct ProfRec {
   cudaEvent_t a, b;
 };
 
+struct het_cache;
+// Loopback group (het_group_create): N workers of one process on one device,
+// their inboxes shared by plain device pointers; every collective call is
+// driven phase by phase across the members (no NCCL, no spinning wait).
+struct het_group {
+  std::vector<het_cache*> m;   // members in rank order
+};
+
 struct het_cache {
   Dev d{};
   uint64_t R = 0;
@@ -51,8 +60,11 @@ struct het_cache {
   float* stage_out = nullptr;
   // protocol state
   bool have_lookup = false;
-  bool fused = false;          // the last lookup ran the fused single-GPU kernels
+  bool fused = false;          // the last lookup ran the fused kernels
   uint32_t last_n = 0;
+  const int64_t* last_keys = nullptr;  // the lookup's keys as passed by the caller
+  bool no_fused = false;       // env HET_NO_FUSED (read once at create)
+  std::shared_ptr<het_group> group;    // loopback member (nullptr: one process per GPU)
   int64_t overflow_bound = 0;  // worst-case residents above C since the last eviction
   uint64_t lookups = 0, keys = 0, updates = 0, launches = 0;
   // multi-GPU
@@ -240,23 +252,19 @@ het_status_t het_get_unique_id(void* out128) {
   return HET_OK;
 }
 
-het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint32_t s,
-                              het_policy_t policy, const het_dist_t* dist, const het_opts_t* opt,
-                              het_stream_t stream_, het_cache_t* out) {
-  cudaStream_t stream = (cudaStream_t)stream_;
-  if (!out) return HET_ERR_ARG;
+static constexpr uint64_t DENSE_DEFAULT = 1ull << 22;   // floats of dense all-reduce staging by default
+
+// one worker; world > 1 with uid == nullptr: a loopback member (het_group_create)
+static het_status_t create_impl(uint64_t rows, uint32_t D, double cache_frac, uint32_t s, het_policy_t policy,
+                                int rank, int world, const void* uid, const het_opts_t* opt, cudaStream_t stream,
+                                het_cache_t* out) {
   *out = nullptr;
   if (rows == 0 || rows > (1ull << 32) || D == 0 || (D % 4) != 0 || D > (1u << 16)) return HET_ERR_ARG;
   if (!(cache_frac >= 0.0 && cache_frac <= 1.0)) return HET_ERR_ARG;
   if (policy != HET_LFU && policy != HET_LRU && policy != HET_LIGHT_LFU) return HET_ERR_ARG;
-  int rank = 0, world = 1;
-  if (dist) {
-    rank = dist->rank;
-    world = dist->world;
-    if (world < 1 || rank < 0 || rank >= world) return HET_ERR_ARG;
-    if (world > 1 && !dist->nccl_unique_id) return HET_ERR_ARG;
-  }
+  if (world < 1 || rank < 0 || rank >= world) return HET_ERR_ARG;
   het_cache* h = new het_cache();
+  h->no_fused = std::getenv("HET_NO_FUSED") != nullptr;
   h->R = rows;
   h->D = D;
   h->C = (int64_t)std::floor(cache_frac * (double)rows);  // R10
@@ -378,7 +386,7 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
   cudaMemsetAsync(d.pop, 0, LFU_CB_MAX * 4, stream);
   launch_reset_cache(d, stream);
   if (world > 1) {
-    rc = mgpu_create(h->mg, d, h->n_max, dist->nccl_unique_id, stream);
+    rc = mgpu_create(h->mg, d, h->n_max, uid, (opt && opt->dense_max) ? opt->dense_max : DENSE_DEFAULT, stream);
     if (rc != HET_OK) goto oom;
   }
   if (cudaStreamSynchronize(stream) != cudaSuccess) { rc = HET_ERR_CUDA; goto oom; }
@@ -393,6 +401,50 @@ oom:
   return rc;
 }
 
+het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint32_t s,
+                              het_policy_t policy, const het_dist_t* dist, const het_opts_t* opt,
+                              het_stream_t stream_, het_cache_t* out) {
+  if (!out) return HET_ERR_ARG;
+  *out = nullptr;
+  int rank = 0, world = 1;
+  const void* uid = nullptr;
+  if (dist) {
+    rank = dist->rank;
+    world = dist->world;
+    uid = dist->nccl_unique_id;
+    if (world > 1 && !uid) return HET_ERR_ARG;
+  }
+  return create_impl(rows, D, cache_frac, s, policy, rank, world, uid, opt, (cudaStream_t)stream_, out);
+}
+
+het_status_t het_group_create(uint32_t N, uint64_t rows, uint32_t D, double cache_frac, uint32_t s,
+                              het_policy_t policy, const het_opts_t* opt, het_stream_t stream_,
+                              het_cache_t* out) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!out || N < 2 || N > 16) return HET_ERR_ARG;
+  for (uint32_t r = 0; r < N; ++r) out[r] = nullptr;
+  auto g = std::make_shared<het_group>();
+  het_status_t rc = HET_OK;
+  for (uint32_t r = 0; r < N && rc == HET_OK; ++r) {
+    rc = create_impl(rows, D, cache_frac, s, policy, (int)r, (int)N, nullptr, opt, st, &out[r]);
+    if (rc == HET_OK) g->m.push_back(out[r]);
+  }
+  if (rc == HET_OK) {
+    std::vector<P2PState*> ps(N);
+    for (uint32_t r = 0; r < N; ++r) ps[r] = mgpu_p2p(out[r]->mg);
+    rc = p2p_loopback_connect(ps.data(), (int)N, st);
+  }
+  if (rc != HET_OK) {
+    for (uint32_t r = 0; r < N; ++r) {
+      if (out[r]) het_cache_destroy(out[r]);
+      out[r] = nullptr;
+    }
+    return rc;
+  }
+  for (uint32_t r = 0; r < N; ++r) out[r]->group = g;
+  return HET_OK;
+}
+
 static het_status_t stage_keys(het_cache* h, const int64_t*& keys, uint32_t n, cudaStream_t st) {
   if (n == 0 || is_device_ptr(keys)) return HET_OK;
   if (!h->stage_keys) CUDA_TRY(h, (dalloc(h, &h->stage_keys, h->n_max)));
@@ -401,77 +453,146 @@ static het_status_t stage_keys(het_cache* h, const int64_t*& keys, uint32_t n, c
   return HET_OK;
 }
 
-het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t clock_t, float* out,
-                        het_stream_t stream_) {
-  cudaStream_t st = (cudaStream_t)stream_;
-  if (!h) return HET_ERR_ARG;
+// ---------------------------------------------------------------- members of a collective call
+// One process per GPU: the call drives its own worker, every phase back to
+// back (peers are other processes).  Loopback group: the call drives all N
+// workers, phase k of every worker before phase k+1 of any.
+struct Members {
+  het_cache* const* hs;
+  int n;
+};
+static P2PState* p2p_of(het_cache* h) { return mgpu_p2p(h->mg); }
+
+static het_status_t check_members(het_cache* const* hs, uint32_t N) {
+  if (!hs || N < 2 || !hs[0] || !hs[0]->group) return HET_ERR_ARG;
+  const auto& m = hs[0]->group->m;
+  if (m.size() != N) return HET_ERR_ARG;
+  for (uint32_t i = 0; i < N; ++i)
+    if (hs[i] != m[i]) return HET_ERR_ARG;   // every member, in rank order
+  return HET_OK;
+}
+
+// a round of the peer-memory exchange carrying only the pending pushes
+static void drain_round(Members g, cudaStream_t st) {
+  for (int ph = 0; ph < RP_NUM; ++ph)
+    for (int i = 0; i < g.n; ++i) {
+      het_cache* h = g.hs[i];
+      Prof p(h, "drain", st);
+      h->launches += p2p_round_phase(p2p_of(h), h->d, h->call, 1, ph, st);
+    }
+}
+
+// ---------------------------------------------------------------- lookup
+struct LkCtx {
+  float* out = nullptr;    // caller's
+  float* dout = nullptr;   // device destination
+  bool out_host = false;
+};
+
+// argument checks, staging, dedup (K1) and the per-call begin
+static het_status_t lookup_pre(het_cache* h, const int64_t* keys, uint32_t n, uint64_t clock_t, float* out,
+                               LkCtx& x, cudaStream_t st) {
   if (n > h->n_max) return fail(h, HET_ERR_CAPACITY, "n exceeds max_keys_per_call");
   if (n && (!keys || !out)) return fail(h, HET_ERR_ARG, "null keys/out");
   if (h->overflow_bound + (int64_t)n > 2 * (int64_t)h->n_max)
     return fail(h, HET_ERR_CAPACITY, "too many lookups without eviction");
+  const int64_t* ukeys = keys;
   het_status_t rc = stage_keys(h, keys, n, st);
   if (rc) return rc;
-  bool out_host = n && !is_device_ptr(out);
-  float* dout = out;
-  if (out_host) {
+  x.out = out;
+  x.out_host = n && !is_device_ptr(out);
+  x.dout = out;
+  if (x.out_host) {
     if (!h->stage_out) CUDA_TRY(h, (dalloc(h, &h->stage_out, (size_t)h->n_max * h->D)));
-    dout = h->stage_out;
+    x.dout = h->stage_out;
   }
   Call& c = h->call;
   c.n = (int)n;
   c.t = clock_t;
   c.keys = keys;
+  h->last_keys = ukeys;
   Dev& d = h->d;
   // fused path: N = 1 up to FUSED_LOOKUP_MAX keys (beyond, the large-batch
   // per-phase kernels with the sliced heavy-key segment reduce), N > 1 over
   // the peer-memory exchange for every n; the dedup kernel follows n
-  h->fused = !getenv("HET_NO_FUSED") && (d.world == 1 ? (int)n <= FUSED_LOOKUP_MAX : mgpu_p2p(h->mg) != nullptr);
-  if (h->fused) {
-    if (fused_ok(d, (int)n)) {
-      Prof p(h, "dedup", st);
-      h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st);
-    } else {
-      launch_begin(d, clock_t, (int)n, st);
-      Prof p(h, "dedup", st);
-      h->launches += 1 + launch_dedup(c, (int)n, d.R, h->pbits, d.ctl, st);
-    }
-    if (d.world == 1) {
-      Prof p(h, "lookup_fused", st);
-      h->launches += launch_lookup_fused(d, c, dout, st);
-    } else {
-      Prof p(h, "exchange_fused", st);
-      h->launches += p2p_round_fused(mgpu_p2p(h->mg), d, c, dout, st);
-    }
+  h->fused = !h->no_fused && (d.world == 1 ? (int)n <= FUSED_LOOKUP_MAX : mgpu_p2p(h->mg) != nullptr);
+  if (h->fused && fused_ok(d, (int)n)) {
+    Prof p(h, "dedup", st);
+    h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st);
   } else {
     launch_begin(d, clock_t, (int)n, st);
-    h->launches += 1;
-    {
-      Prof p(h, "dedup", st);
-      h->launches += launch_dedup(c, (int)n, d.R, h->pbits, d.ctl, st);
-    }
-    if (d.world == 1) {
-      {
-        Prof p(h, "probe", st);
-        launch_probe(d, c, (int)n, st);
-      }
-      {
-        Prof p(h, "sync_fetch", st);
-        launch_sync_fetch_install_local(d, c, (int)n, st);
-      }
-      h->launches += 2;
-    } else {
-      rc = mgpu_lookup(h->mg, d, c, h->prof ? (void*)h : nullptr, st);
-      if (rc) return fail(h, rc, "multi-GPU lookup failed");
-      h->launches += mgpu_take_launches(h->mg);
-    }
-    {
-      Prof p(h, "gather", st);
-      launch_gather(d, c, dout, st);
-      h->launches += 1;
-    }
+    Prof p(h, "dedup", st);
+    h->launches += 1 + launch_dedup(c, (int)n, d.R, h->pbits, d.ctl, st);
   }
+  return HET_OK;
+}
+
+// one process per GPU: the rest of Alg. 2 (probe, CheckValid, sync/fetch, Get)
+static het_status_t lookup_body(het_cache* h, LkCtx& x, cudaStream_t st) {
+  Dev& d = h->d;
+  Call& c = h->call;
+  if (h->fused) {
+    if (d.world == 1) {
+      Prof p(h, "lookup_fused", st);
+      h->launches += launch_lookup_fused(d, c, x.dout, st);
+    } else {
+      Prof p(h, "exchange_fused", st);
+      h->launches += p2p_round_fused(p2p_of(h), d, c, x.dout, st);
+    }
+    return HET_OK;
+  }
+  if (d.world == 1) {
+    {
+      Prof p(h, "probe", st);
+      launch_probe(d, c, c.n, st);
+    }
+    {
+      Prof p(h, "sync_fetch", st);
+      launch_sync_fetch_install_local(d, c, c.n, st);
+    }
+    h->launches += 2;
+  } else {
+    het_status_t rc = mgpu_lookup(h->mg, d, c, h->prof ? (void*)h : nullptr, st);
+    if (rc) return fail(h, rc, "multi-GPU lookup failed");
+    h->launches += mgpu_take_launches(h->mg);
+  }
+  Prof p(h, "gather", st);
+  launch_gather(d, c, x.dout, st);
+  h->launches += 1;
+  return HET_OK;
+}
+
+// loopback: phase `ph` of the exchange round of one member
+static void lookup_phase(het_cache* h, LkCtx& x, int ph, cudaStream_t st) {
+  Dev& d = h->d;
+  Call& c = h->call;
+  P2PState* p = p2p_of(h);
+  if (h->fused) {
+    Prof pr(h, "exchange_fused", st);
+    h->launches += p2p_lookup_phase(p, d, c, x.dout, ph, st);
+    return;
+  }
+  if (ph == RP_BUILD) {
+    Prof pr(h, "probe", st);
+    launch_probe(d, c, c.n, st);
+    h->launches += 1;
+  }
+  {
+    Prof pr(h, "exchange", st);
+    h->launches += p2p_round_phase(p, d, c, 0, ph, st);
+  }
+  if (ph == RP_INSTALL) {
+    Prof pr(h, "gather", st);
+    launch_gather(d, c, x.dout, st);
+    h->launches += 1;
+  }
+}
+
+static het_status_t lookup_post(het_cache* h, LkCtx& x, cudaStream_t st) {
+  Dev& d = h->d;
+  const uint32_t n = (uint32_t)h->call.n;
   if (d.pin_thr) h->launches += launch_pin_apply(d, st);   // light-LFU promotions of this lookup
-  if (out_host) CUDA_TRY(h, cudaMemcpyAsync(out, dout, (size_t)n * h->D * 4, cudaMemcpyDeviceToHost, st));
+  if (x.out_host) CUDA_TRY(h, cudaMemcpyAsync(x.out, x.dout, (size_t)n * h->D * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaGetLastError());
   h->have_lookup = true;
   h->last_n = n;
@@ -479,6 +600,40 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
   return HET_OK;
 }
 
+het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t clock_t, float* out,
+                        het_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!h) return HET_ERR_ARG;
+  if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_lookup");
+  LkCtx x;
+  het_status_t rc = lookup_pre(h, keys, n, clock_t, out, x, st);
+  if (rc == HET_OK) rc = lookup_body(h, x, st);
+  if (rc == HET_OK) rc = lookup_post(h, x, st);
+  return rc;
+}
+
+het_status_t het_group_lookup(const het_cache_t* hs, uint32_t N, const int64_t* const* keys, const uint32_t* n,
+                              uint64_t clock_t, float* const* out, het_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (check_members(hs, N) || !keys || !n || !out) return HET_ERR_ARG;
+  std::vector<LkCtx> x(N);
+  for (uint32_t i = 0; i < N; ++i)
+    if (n[i] > hs[i]->n_max || hs[i]->overflow_bound + (int64_t)n[i] > 2 * (int64_t)hs[i]->n_max)
+      return fail(hs[i], HET_ERR_CAPACITY, "n exceeds max_keys_per_call / too many lookups without eviction");
+  for (uint32_t i = 0; i < N; ++i) {
+    het_status_t rc = lookup_pre(hs[i], keys[i], n[i], clock_t, out[i], x[i], st);
+    if (rc) return rc;
+  }
+  for (int ph = 0; ph < RP_NUM; ++ph)
+    for (uint32_t i = 0; i < N; ++i) lookup_phase(hs[i], x[i], ph, st);
+  for (uint32_t i = 0; i < N; ++i) {
+    het_status_t rc = lookup_post(hs[i], x[i], st);
+    if (rc) return rc;
+  }
+  return HET_OK;
+}
+
+// ---------------------------------------------------------------- update
 static het_status_t evict_overflow(het_cache* h, cudaStream_t st) {
   Dev& d = h->d;
   if (d.world == 1) {
@@ -489,6 +644,7 @@ static het_status_t evict_overflow(het_cache* h, cudaStream_t st) {
     Prof p(h, "evict_apply", st);
     h->launches += launch_evict_apply_local(d, h->evbuf_host, st);
   } else {
+    // select + PUSH records into the owners' inboxes (carried by the next round: no wait)
     het_status_t rc = mgpu_evict_overflow(h->mg, d, h->evbuf_host, h->prof ? (void*)h : nullptr, st);
     if (rc) return rc;
     h->launches += mgpu_take_launches(h->mg);
@@ -503,23 +659,37 @@ static het_status_t evict_overflow(het_cache* h, cudaStream_t st) {
   return HET_OK;
 }
 
-het_status_t het_update(het_cache_t h, const int64_t* keys, uint32_t n, const float* grads, float lr,
-                        het_stream_t stream_) {
-  cudaStream_t st = (cudaStream_t)stream_;
-  if (!h) return HET_ERR_ARG;
-  (void)keys;
+// Alg. 3 writes the keys Alg. 2 read: same n, and a buffer other
+// than the lookup's is compared on the device, position by position, with the
+// lookup's dedup (keys[pos] == unique[inverse[pos]]); a mismatch latches
+// HET_ERR_PROTOCOL and aborts the update before it touches the cache.
+__global__ void k_check_keys(const int64_t* __restrict__ keys, int n, Call c, Ctl* ctl) {
+  int bad = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    bad |= keys[i] != c.uniq[c.inverse[i]];
+  if (__syncthreads_or(bad) && threadIdx.x == 0) raise_err(ctl, 3 /*HET_ERR_PROTOCOL*/);
+}
+
+static het_status_t update_impl(het_cache* h, const int64_t* keys, uint32_t n, const float* grads, float lr,
+                                cudaStream_t st) {
   if (!h->have_lookup || n != h->last_n) return fail(h, HET_ERR_PROTOCOL, "write without matching read");
-  if (n && !grads) return fail(h, HET_ERR_ARG, "null grads");
+  if (n && (!grads || !keys)) return fail(h, HET_ERR_ARG, "null keys/grads");
+  Dev& d = h->d;
+  if (n && keys != h->last_keys) {
+    het_status_t rc = stage_keys(h, keys, n, st);
+    if (rc) return rc;
+    k_check_keys<<<std::min<int>(148, (n + 255) / 256), 256, 0, st>>>(keys, (int)n, h->call, d.ctl);
+    h->launches += 1;
+  }
   if (n && !is_device_ptr(grads)) {
     if (!h->stage_rows) CUDA_TRY(h, (dalloc(h, &h->stage_rows, (size_t)h->n_max * h->D)));
     CUDA_TRY(h, cudaMemcpyAsync(h->stage_rows, grads, (size_t)n * h->D * 4, cudaMemcpyHostToDevice, st));
     grads = h->stage_rows;
   }
-  Dev& d = h->d;
   if (h->fused) {
     Prof p(h, "update_fused", st);
     h->launches += launch_update_fused(d, h->call, grads, lr, h->evbuf_host, st,
-                                       d.world > 1 ? (const void*)p2p_view_ptr(mgpu_p2p(h->mg)) : nullptr);
+                                       d.world > 1 ? (const void*)p2p_view_ptr(p2p_of(h)) : nullptr);
     h->overflow_bound = 0;
   } else {
     {
@@ -534,70 +704,189 @@ het_status_t het_update(het_cache_t h, const int64_t* keys, uint32_t n, const fl
   return HET_OK;
 }
 
-het_status_t het_evict(het_cache_t h, const int64_t* keys, uint32_t n, het_stream_t stream_) {
-  cudaStream_t st = (cudaStream_t)stream_;
+het_status_t het_update(het_cache_t h, const int64_t* keys, uint32_t n, const float* grads, float lr,
+                        het_stream_t stream_) {
   if (!h) return HET_ERR_ARG;
-  Dev& d = h->d;
-  if (!keys) {
-    het_status_t rc = evict_overflow(h, st);
-    if (rc) return fail(h, rc, "evict failed");
-    return HET_OK;
+  if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_update");
+  return update_impl(h, keys, n, grads, lr, (cudaStream_t)stream_);
+}
+
+het_status_t het_group_update(const het_cache_t* hs, uint32_t N, const int64_t* const* keys, const uint32_t* n,
+                              const float* const* grads, float lr, het_stream_t stream_) {
+  if (check_members(hs, N) || !keys || !n || !grads) return HET_ERR_ARG;
+  for (uint32_t i = 0; i < N; ++i)   // no partial group update on a synchronous error
+    if (!hs[i]->have_lookup || n[i] != hs[i]->last_n)
+      return fail(hs[i], HET_ERR_PROTOCOL, "write without matching read");
+  for (uint32_t i = 0; i < N; ++i) {   // pushes go to the owners' inboxes: no cross-worker wait
+    het_status_t rc = update_impl(hs[i], keys[i], n[i], grads[i], lr, (cudaStream_t)stream_);
+    if (rc) return rc;
   }
+  return HET_OK;
+}
+
+// ---------------------------------------------------------------- evict
+static het_status_t evict_keys_pre(het_cache* h, const int64_t* keys, uint32_t n, cudaStream_t st) {
   if (n > h->n_max) return fail(h, HET_ERR_CAPACITY, "n exceeds max_keys_per_call");
   het_status_t rc = stage_keys(h, keys, n, st);
   if (rc) return rc;
   Call& c = h->call;
   c.n = (int)n;
   c.keys = keys;
-  cudaMemsetAsync(&d.ctl->abort, 0, 4, st);
-  h->launches += launch_dedup(c, (int)n, d.R, h->pbits, d.ctl, st);
-  if (d.world == 1) {
-    int blocks = std::max(1, ((int)n + 7) / 8);
-    k_evict_keys_local<<<blocks, 256, 0, st>>>(d, c);
-    h->launches += 1;
-  } else {
-    rc = mgpu_evict_keys(h->mg, d, c, st);
-    if (rc) return fail(h, rc, "multi-GPU evict failed");
-    h->launches += mgpu_take_launches(h->mg);
-  }
-  h->have_lookup = false;
-  CUDA_TRY(h, cudaGetLastError());
+  cudaMemsetAsync(&h->d.ctl->abort, 0, 4, st);
+  h->launches += launch_dedup(c, (int)n, h->d.R, h->pbits, h->d.ctl, st);
   return HET_OK;
 }
 
+// keys == nullptr: overflow Evict() (no cross-worker wait); else Cache.Evict(key)
+static het_status_t evict_members(Members g, const int64_t* const* keys, const uint32_t* n, cudaStream_t st) {
+  if (!keys) {
+    for (int i = 0; i < g.n; ++i) {
+      het_status_t rc = evict_overflow(g.hs[i], st);
+      if (rc) return fail(g.hs[i], rc, "evict failed");
+    }
+    return HET_OK;
+  }
+  het_cache* h0 = g.hs[0];
+  if (h0->d.world == 1) {
+    het_status_t rc = evict_keys_pre(h0, keys[0], n[0], st);
+    if (rc) return rc;
+    k_evict_keys_local<<<std::max(1, ((int)n[0] + 7) / 8), 256, 0, st>>>(h0->d, h0->call);
+    h0->launches += 1;
+  } else if (!p2p_of(h0)) {   // NCCL exchange (HET_P2P=0)
+    het_status_t rc = evict_keys_pre(h0, keys[0], n[0], st);
+    if (rc) return rc;
+    rc = mgpu_evict_keys(h0->mg, h0->d, h0->call, st);
+    if (rc) return fail(h0, rc, "multi-GPU evict failed");
+    h0->launches += mgpu_take_launches(h0->mg);
+  } else {
+    drain_round(g, st);   // the pushes of the last update precede (U4 before this Evict)
+    for (int i = 0; i < g.n; ++i) {
+      het_status_t rc = evict_keys_pre(g.hs[i], keys[i], n[i], st);
+      if (rc) return rc;
+      g.hs[i]->launches += p2p_evict_keys(p2p_of(g.hs[i]), g.hs[i]->d, g.hs[i]->call, st);
+    }
+    drain_round(g, st);
+  }
+  for (int i = 0; i < g.n; ++i) {
+    g.hs[i]->have_lookup = false;
+    CUDA_TRY(g.hs[i], cudaGetLastError());
+  }
+  return HET_OK;
+}
+
+het_status_t het_evict(het_cache_t h, const int64_t* keys, uint32_t n, het_stream_t stream_) {
+  if (!h) return HET_ERR_ARG;
+  if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_evict");
+  het_cache* one[1] = {h};
+  const int64_t* k1[1] = {keys};
+  return evict_members(Members{one, 1}, keys ? k1 : nullptr, &n, (cudaStream_t)stream_);
+}
+
+het_status_t het_group_evict(const het_cache_t* hs, uint32_t N, const int64_t* const* keys, const uint32_t* n,
+                             het_stream_t stream_) {
+  if (check_members(hs, N) || (keys && !n)) return HET_ERR_ARG;
+  if (keys)
+    for (uint32_t i = 0; i < N; ++i)
+      if (n[i] > hs[i]->n_max) return fail(hs[i], HET_ERR_CAPACITY, "n exceeds max_keys_per_call");
+  return evict_members(Members{hs, (int)N}, keys, n, (cudaStream_t)stream_);
+}
+
+// ---------------------------------------------------------------- sync (flush)
 static het_status_t sticky(het_cache* h, cudaStream_t st) {
   Ctl ctl;
   CUDA_TRY(h, cudaMemcpyAsync(&ctl, h->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaStreamSynchronize(st));
   if (ctl.err) return fail(h, (het_status_t)ctl.err, "sticky device error");
+  if (h->mg && mgpu_comm_error(h->mg)) return fail(h, HET_ERR_NCCL, "NCCL asynchronous error");
   return HET_OK;
 }
 
-het_status_t het_sync(het_cache_t h, het_stream_t stream_) {
-  cudaStream_t st = (cudaStream_t)stream_;
-  if (!h) return HET_ERR_ARG;
-  Dev& d = h->d;
-  if (d.world == 1) {
-    k_flush_local<<<148 * 4, 256, 0, st>>>(d);
-    h->launches += 1;
-  } else {
-    het_status_t rc = mgpu_drain(h->mg, d, h->call, st);
-    if (rc == HET_OK) rc = mgpu_flush(h->mg, d, st);
-    if (rc) return fail(h, rc, "multi-GPU flush failed");
+// het_sync over the peer-memory exchange: dirty entries of key range [k0, k1)
+// in rounds of whole key bins (a key's pushes from every worker meet at the
+// owner in one round, applied in source-rank order, R1), each round at most
+// CAPS records per source; a bin too large for one round is split again.
+static het_status_t flush_range(Members g, int64_t k0, int64_t k1, cudaStream_t st) {
+  std::vector<int32_t> bins(FBINS, 0), mine(FBINS);
+  for (int i = 0; i < g.n; ++i) {
+    het_cache* h = g.hs[i];
+    het_status_t rc = mgpu_flush_hist(h->mg, h->d, k0, k1, mine.data(), st);
+    if (rc) return fail(h, rc, "flush histogram failed");
     h->launches += mgpu_take_launches(h->mg);
+    for (int b = 0; b < FBINS; ++b) bins[b] = std::max(bins[b], mine[b]);
   }
-  launch_reset_cache(d, st);
-  h->launches += 1;
-  if (d.lfu_cb) {
-    cudaMemsetAsync(d.bm, 0, (size_t)d.lfu_cb * d.bm_words * 4, st);
-    cudaMemsetAsync(d.bcnt, 0, (size_t)d.lfu_cb * d.nbk * 4, st);
-    cudaMemsetAsync(d.bcnt2, 0, (size_t)d.lfu_cb * d.nbk2 * 4, st);
+  if (g.n == 1) {   // one process per GPU: the max over the ranks
+    het_status_t rc = mgpu_allreduce_max_host(g.hs[0]->mg, bins.data(), FBINS, st);
+    if (rc) return fail(g.hs[0], rc, "flush histogram all-reduce failed");
   }
-  cudaMemsetAsync(d.pop, 0, LFU_CB_MAX * 4, st);
-  h->have_lookup = false;
-  h->overflow_bound = 0;
-  CUDA_TRY(h, cudaGetLastError());
-  return sticky(h, st);
+  const int64_t caps = p2p_caps(p2p_of(g.hs[0]));
+  const int64_t W = k1 - k0;
+  auto kb = [&](int b) { return k0 + ((int64_t)b * W + FBINS - 1) / FBINS; };   // first key of bin b
+  int b0 = 0;
+  while (b0 < FBINS) {
+    if (bins[b0] > caps) {   // one bin over capacity: split it (its keys >= its dirty count per worker)
+      het_status_t rc = flush_range(g, kb(b0), kb(b0 + 1), st);
+      if (rc) return rc;
+      ++b0;
+      continue;
+    }
+    int64_t acc = 0;
+    int b1 = b0;
+    while (b1 < FBINS && bins[b1] <= caps && acc + bins[b1] <= caps) acc += bins[b1++];
+    if (acc > 0) {
+      for (int i = 0; i < g.n; ++i)
+        g.hs[i]->launches += p2p_flush_build(p2p_of(g.hs[i]), g.hs[i]->d, kb(b0), kb(b1), st);
+      drain_round(g, st);
+    }
+    b0 = b1;
+  }
+  return HET_OK;
+}
+
+static het_status_t sync_members(Members g, cudaStream_t st) {
+  het_cache* h0 = g.hs[0];
+  if (h0->d.world == 1) {
+    k_flush_local<<<148 * 4, 256, 0, st>>>(h0->d);
+    h0->launches += 1;
+  } else if (!p2p_of(h0)) {   // NCCL exchange (HET_P2P=0)
+    het_status_t rc = mgpu_flush(h0->mg, h0->d, st);
+    if (rc) return fail(h0, rc, "multi-GPU flush failed");
+    h0->launches += mgpu_take_launches(h0->mg);
+  } else {
+    drain_round(g, st);   // U4 of the last update precedes the flush
+    het_status_t rc = flush_range(g, 0, (int64_t)h0->R, st);
+    if (rc) return rc;
+  }
+  het_status_t first = HET_OK;
+  for (int i = 0; i < g.n; ++i) {
+    het_cache* h = g.hs[i];
+    Dev& d = h->d;
+    launch_reset_cache(d, st);
+    h->launches += 1;
+    if (d.lfu_cb) {
+      cudaMemsetAsync(d.bm, 0, (size_t)d.lfu_cb * d.bm_words * 4, st);
+      cudaMemsetAsync(d.bcnt, 0, (size_t)d.lfu_cb * d.nbk * 4, st);
+      cudaMemsetAsync(d.bcnt2, 0, (size_t)d.lfu_cb * d.nbk2 * 4, st);
+    }
+    cudaMemsetAsync(d.pop, 0, LFU_CB_MAX * 4, st);
+    h->have_lookup = false;
+    h->overflow_bound = 0;
+    CUDA_TRY(h, cudaGetLastError());
+    het_status_t rc = sticky(h, st);
+    if (rc && !first) first = rc;
+  }
+  return first;
+}
+
+het_status_t het_sync(het_cache_t h, het_stream_t stream_) {
+  if (!h) return HET_ERR_ARG;
+  if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_sync");
+  het_cache* one[1] = {h};
+  return sync_members(Members{one, 1}, (cudaStream_t)stream_);
+}
+
+het_status_t het_group_sync(const het_cache_t* hs, uint32_t N, het_stream_t stream_) {
+  if (check_members(hs, N)) return HET_ERR_ARG;
+  return sync_members(Members{hs, (int)N}, (cudaStream_t)stream_);
 }
 
 het_status_t het_check(het_cache_t h) {
@@ -630,7 +919,7 @@ het_status_t het_stats(het_cache_t h, het_stats_t* out) {
   out->launches = h->launches;
   out->resident = (uint32_t)(h->d.Ecap - ctl.ftop);
   out->capacity = (uint32_t)h->C;
-  out->sticky_error = ctl.err;
+  out->sticky_error = ctl.err ? ctl.err : (h->mg && mgpu_comm_error(h->mg) ? HET_ERR_NCCL : 0);
   out->pinned = (uint32_t)ctl.npinned;
   return HET_OK;
 }
@@ -668,23 +957,43 @@ het_status_t het_read_global(het_cache_t h, const int64_t* keys, uint32_t n, flo
   return HET_OK;
 }
 
+// ---------------------------------------------------------------- dense all-reduce (Eq. 2)
 het_status_t het_dense_allreduce(het_cache_t h, float* buf, uint64_t count, het_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!h) return HET_ERR_ARG;
+  if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_dense_allreduce");
   if (count == 0 || h->d.world == 1) return HET_OK;
   if (!buf || !is_device_ptr(buf)) return fail(h, HET_ERR_ARG, "dense buffer must be device memory");
   Prof p(h, "dense_allreduce", st);
   int l = 0;
-  het_status_t rc = mgpu_dense_p2p(h->mg, h->d, buf, count, st, &l);   // peer-memory one-shot mean
+  het_status_t rc = mgpu_dense_p2p(h->mg, h->d, buf, count, 0, st, &l);   // peer-memory one-shot mean
   if (rc == HET_OK) {
     h->launches += l;
     return HET_OK;
   }
   if (rc != HET_ERR_CAPACITY) return fail(h, rc, "peer all-reduce failed");
-  rc = mgpu_allreduce_sum(h->mg, buf, count, st);
+  rc = mgpu_allreduce_sum(h->mg, buf, count, st);   // count is collective: every rank falls back together
   if (rc) return fail(h, rc, "allreduce failed");
   k_scale<<<148 * 4, 256, 0, st>>>(buf, count, 1.0f / (float)h->d.world);
   h->launches += 1;
+  return HET_OK;
+}
+
+het_status_t het_group_dense_allreduce(const het_cache_t* hs, uint32_t N, float* const* bufs, uint64_t count,
+                                       het_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (check_members(hs, N) || !bufs) return HET_ERR_ARG;
+  if (count == 0) return HET_OK;
+  for (uint32_t i = 0; i < N; ++i)
+    if (!bufs[i] || !is_device_ptr(bufs[i])) return fail(hs[i], HET_ERR_ARG, "dense buffer must be device memory");
+  for (int ph = 1; ph <= 2; ++ph)
+    for (uint32_t i = 0; i < N; ++i) {
+      int l = 0;
+      Prof p(hs[i], "dense_allreduce", st);
+      het_status_t rc = mgpu_dense_p2p(hs[i]->mg, hs[i]->d, bufs[i], count, ph, st, &l);
+      if (rc) return fail(hs[i], rc, "loopback dense all-reduce: count exceeds the staging (opts.dense_max)");
+      hs[i]->launches += l;
+    }
   return HET_OK;
 }
 

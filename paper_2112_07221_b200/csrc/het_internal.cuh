@@ -371,7 +371,7 @@ constexpr int FUSED_LOOKUP_MAX = 16384;   // N = 1: fused lookup/update up to th
 int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st);
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st);
 // SMs left free by the cooperative kernels for NCCL's blocks at N > 1
-// (= NCCL's maxCTAs; env HET_NCCL_CTAS, default 32)
+// (= NCCL's maxCTAs and the peer-memory dense all-reduce grid; env HET_NCCL_CTAS, default 16)
 int coop_sm_reserve();
 int launch_update_fused(const Dev& s, const Call& c, const float* grads, float lr, void* evbuf, cudaStream_t st,
                         const void* p2pview = nullptr);

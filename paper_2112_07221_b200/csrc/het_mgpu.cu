@@ -490,7 +490,8 @@ static void owner_group(MgpuState* m, const Dev& d, int total, int kind, cudaStr
 }
 
 // ---------------------------------------------------------------- API
-het_status_t mgpu_create(MgpuState*& mg, const Dev& d, uint32_t n_max, const void* uid, cudaStream_t st) {
+het_status_t mgpu_create(MgpuState*& mg, const Dev& d, uint32_t n_max, const void* uid, uint64_t dense_cap,
+                         cudaStream_t st) {
   MgpuState* m = new MgpuState();
   mg = m;
   m->N = d.world;
@@ -498,17 +499,26 @@ het_status_t mgpu_create(MgpuState*& mg, const Dev& d, uint32_t n_max, const voi
   m->D = d.D;
   m->CAPS = 3 * (int64_t)n_max;
   m->REC = 4 + d.D;
-  ncclUniqueId id;
-  std::memcpy(&id, uid, sizeof(id));
-  // NCCL's kernels (the dense all-reduce, overlapped on a side stream) are
-  // capped at NCCL_CTAS blocks, and the cooperative hot-path kernels leave that
-  // many SMs free (het::coop_sm_reserve), so neither waits for the other's SMs.
-  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
-  if (!getenv("HET_NCCL_DEFAULT")) {   // diagnostic: NCCL's own CTA choice
-    cfg.maxCTAs = coop_sm_reserve();
-    cfg.minCTAs = std::min(4, cfg.maxCTAs);
+  const char* env = std::getenv("HET_P2P");
+  const bool loopback = uid == nullptr;   // N workers on this device, driven by het_group_* (no NCCL)
+  const bool p2p = loopback || !(env && env[0] == '0');
+  if (p2p && d.world > P2P_MAX_WORLD) return HET_ERR_ARG;
+  if (!loopback) {
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    // NCCL's kernels (the dense all-reduce fallback, overlapped on a side
+    // stream) are capped at NCCL_CTAS blocks, and the cooperative hot-path
+    // kernels leave that many SMs free (het::coop_sm_reserve), so neither
+    // waits for the other's SMs.
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    if (!getenv("HET_NCCL_DEFAULT")) {   // diagnostic: NCCL's own CTA choice
+      cfg.maxCTAs = coop_sm_reserve();
+      cfg.minCTAs = std::min(4, cfg.maxCTAs);
+    }
+    if (ncclCommInitRankConfig(&m->comm, d.world, id, d.rank, &cfg) != ncclSuccess) return HET_ERR_NCCL;
   }
-  if (ncclCommInitRankConfig(&m->comm, d.world, id, d.rank, &cfg) != ncclSuccess) return HET_ERR_NCCL;
+  if (p2p) return p2p_create(m->p2p, d, n_max, m->comm, dense_cap, st);
+  // the NCCL send/recv exchange (HET_P2P=0): its staging regions
   const int64_t NC = (int64_t)m->N * m->CAPS;
   bool ok = mg_alloc(m, &m->qkeys, NC) && mg_alloc(m, &m->qidx, NC) && mg_alloc(m, &m->rqkeys, NC) &&
             mg_alloc(m, &m->ans, NC) && mg_alloc(m, &m->ansr, NC) && mg_alloc(m, &m->hdr, NC) &&
@@ -528,11 +538,6 @@ het_status_t mgpu_create(MgpuState*& mg, const Dev& d, uint32_t n_max, const voi
   m->opbits = std::max(1, bits_for((uint64_t)NC - 1));
   cudaMemsetAsync(m->octl, 0, sizeof(Ctl), st);
   cudaMemsetAsync(m->scnt, 0, sizeof(int32_t) * 2 * m->N, st);
-  const char* env = std::getenv("HET_P2P");
-  if (!(env && env[0] == '0')) {
-    het_status_t rc = p2p_create(m->p2p, d, n_max, m->comm, st);
-    if (rc != HET_OK) return rc;
-  }
   return HET_OK;
 }
 
@@ -652,8 +657,7 @@ het_status_t mgpu_evict_overflow(MgpuState* m, const Dev& d, void* evbuf, void* 
   return rc;
 }
 
-het_status_t mgpu_evict_keys(MgpuState* m, const Dev& d, const Call& c, cudaStream_t st) {
-  if (m->p2p) m->launches += p2p_round(m->p2p, d, c, 1, st);   // deliver pending pushes first
+het_status_t mgpu_evict_keys(MgpuState* m, const Dev& d, const Call& c, cudaStream_t st) {   // NCCL exchange only
   cudaMemsetAsync(m->scnt, 0, sizeof(int32_t) * 2 * m->N, st);
   k_build_pushes<<<grid_for(std::max(c.n, 1), 8), MG_TPB, 0, st>>>(d, c, *m, nullptr, nullptr, nullptr, nullptr, 1,
                                                                      0, 0);
@@ -667,12 +671,12 @@ het_status_t mgpu_evict_keys(MgpuState* m, const Dev& d, const Call& c, cudaStre
 // histogram of dirty entries over FBINS key bins is max-reduced across the
 // workers and the host groups consecutive bins into rounds whose per-worker
 // count fits the (temporary) flush buffers.
-constexpr int FBINS = 1024;
 
-__global__ void k_flush_hist(Dev s, int32_t* bins) {
+// dirty resident entries of keys [k0, k1) per bin: bin(key) = (key - k0) * FBINS / (k1 - k0)
+__global__ void k_flush_hist(Dev s, int32_t* bins, int64_t k0, int64_t k1) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < s.Ecap; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t key = s.ekey[e];
-    if (key >= 0 && s.cc[e] > s.cs[e]) atomicAdd(&bins[(int)((key * FBINS) / s.R)], 1);
+    if (key >= k0 && key < k1 && s.cc[e] > s.cs[e]) atomicAdd(&bins[(int)(((key - k0) * FBINS) / (k1 - k0))], 1);
   }
 }
 
@@ -709,8 +713,35 @@ __global__ void k_flush_build(Dev s, MgpuState m_, int64_t k0, int64_t k1) {
   }
 }
 
-het_status_t mgpu_drain(MgpuState* m, const Dev& d, const Call& c, cudaStream_t st) {
-  if (m->p2p) m->launches += p2p_round(m->p2p, d, c, 1, st);
+het_status_t mgpu_flush_hist(MgpuState* m, const Dev& d, int64_t k0, int64_t k1, int32_t* bins_host,
+                             cudaStream_t st) {
+  int32_t* dbins;
+  if (cudaMallocAsync((void**)&dbins, FBINS * 4, st) != cudaSuccess) return HET_ERR_OOM;
+  cudaMemsetAsync(dbins, 0, FBINS * 4, st);
+  k_flush_hist<<<148 * 4, 256, 0, st>>>(d, dbins, k0, k1);
+  m->launches += 1;
+  cudaMemcpyAsync(bins_host, dbins, FBINS * 4, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dbins, st);
+  return cudaStreamSynchronize(st) == cudaSuccess ? HET_OK : HET_ERR_CUDA;
+}
+
+het_status_t mgpu_allreduce_max_host(MgpuState* m, int32_t* x, int count, cudaStream_t st) {
+  if (!m->comm) return HET_ERR_ARG;
+  int32_t* dx;
+  if (cudaMallocAsync((void**)&dx, (size_t)count * 4, st) != cudaSuccess) return HET_ERR_OOM;
+  cudaMemcpyAsync(dx, x, (size_t)count * 4, cudaMemcpyHostToDevice, st);
+  if (ncclAllReduce(dx, dx, count, ncclInt32, ncclMax, m->comm, st) != ncclSuccess) return HET_ERR_NCCL;
+  cudaMemcpyAsync(x, dx, (size_t)count * 4, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dx, st);
+  return cudaStreamSynchronize(st) == cudaSuccess ? HET_OK : HET_ERR_CUDA;
+}
+
+bool mgpu_loopback(MgpuState* m) { return m && m->p2p && p2p_loopback(m->p2p); }
+
+het_status_t mgpu_comm_error(MgpuState* m) {
+  if (!m || !m->comm) return HET_OK;
+  ncclResult_t r = ncclSuccess;
+  if (ncclCommGetAsyncError(m->comm, &r) != ncclSuccess || r != ncclSuccess) return HET_ERR_NCCL;
   return HET_OK;
 }
 
@@ -720,7 +751,7 @@ het_status_t mgpu_flush(MgpuState* m, const Dev& d, cudaStream_t st) {
   if (cudaMallocAsync((void**)&dbins, FBINS * 4, st) || cudaMallocAsync((void**)&rbins, FBINS * 4, st))
     return HET_ERR_OOM;
   cudaMemsetAsync(dbins, 0, FBINS * 4, st);
-  k_flush_hist<<<148 * 4, 256, 0, st>>>(d, dbins);
+  k_flush_hist<<<148 * 4, 256, 0, st>>>(d, dbins, 0, d.R);
   if (ncclAllReduce(dbins, rbins, FBINS, ncclInt32, ncclMax, m->comm, st) != ncclSuccess) return HET_ERR_NCCL;
   std::vector<int32_t> bins(FBINS);
   cudaMemcpyAsync(bins.data(), rbins, FBINS * 4, cudaMemcpyDeviceToHost, st);
@@ -779,14 +810,15 @@ het_status_t mgpu_flush(MgpuState* m, const Dev& d, cudaStream_t st) {
   return rc;
 }
 
-het_status_t mgpu_dense_p2p(MgpuState* m, const Dev& d, float* buf, uint64_t count, cudaStream_t st,
+het_status_t mgpu_dense_p2p(MgpuState* m, const Dev& d, float* buf, uint64_t count, int phase, cudaStream_t st,
                             int* launches) {
   static const bool nccl_only = getenv("HET_DENSE_NCCL") != nullptr;   // diagnostic: NCCL all-reduce
-  if (!m->p2p || nccl_only) return HET_ERR_CAPACITY;
-  return p2p_dense_allreduce(m->p2p, d, buf, count, m->comm, st, launches);
+  if (!m->p2p || (nccl_only && m->comm)) return HET_ERR_CAPACITY;
+  return p2p_dense_allreduce(m->p2p, d, buf, count, phase, st, launches);
 }
 
 het_status_t mgpu_allreduce_sum(MgpuState* m, float* buf, uint64_t count, cudaStream_t st) {
+  if (!m->comm) return HET_ERR_CAPACITY;   // loopback: no NCCL
   return nccl_ok(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, m->comm, st));
 }
 

@@ -812,32 +812,41 @@ __device__ __forceinline__ float* dbuf(const DenseView& v, int r, int par) {
   return (float*)(v.peer[r] + 2 * 64 * sizeof(Flag)) + (uint64_t)par * v.cap;
 }
 
+// phase 0: the whole all-reduce (one process per GPU: every wait is for
+// another GPU's kernel); phase 1: stage + publish only; phase 2: wait + sum
+// only.  The loopback driver (one GPU, N workers) runs phase 1 of every
+// worker before phase 2 of any, so no wait ever spins.
 __global__ void __launch_bounds__(512) k_dense_ar(DenseView v, float* __restrict__ buf, uint64_t count,
-                                                  float scale, Ctl* ctl) {
+                                                  float scale, Ctl* ctl, int phase) {
   __shared__ int s_ok;
   const unsigned long long e = *v.epoch + 1;
   const int par = (int)(e & 1);
   const uint64_t n4 = count / 4;
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = (uint64_t)gridDim.x * blockDim.x;
-  // staging buffer `par` is free once every peer finished reading epoch e - 2
-  if (threadIdx.x == 0) s_ok = e <= 2 || wait_flags(ddone(v, v.rank), v.N, e - 2, ctl);
-  __syncthreads();
-  float4* mine = reinterpret_cast<float4*>(dbuf(v, v.rank, par));
   constexpr int U = 8;   // float4 per thread in flight (peer reads cross NVLink: latency-bound)
-  if (s_ok) {
-    const float4* b4 = reinterpret_cast<const float4*>(buf);
-    for (uint64_t i0 = tid; i0 < n4; i0 += U * nth) {
-      float4 t[U];
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  if (phase != 2) {
+    // staging buffer `par` is free once every peer finished reading epoch e - 2
+    if (threadIdx.x == 0) s_ok = e <= 2 || wait_flags(ddone(v, v.rank), v.N, e - 2, ctl);
+    __syncthreads();
+    float4* mine = reinterpret_cast<float4*>(dbuf(v, v.rank, par));
+    if (s_ok) {
+      const float4* b4 = reinterpret_cast<const float4*>(buf);
+      for (uint64_t i0 = tid; i0 < n4; i0 += U * nth) {
+        float4 t[U];
 #pragma unroll
-      for (int k = 0; k < U; ++k) if (i0 + k * nth < n4) t[k] = b4[i0 + k * nth];
+        for (int k = 0; k < U; ++k) if (i0 + k * nth < n4) t[k] = b4[i0 + k * nth];
 #pragma unroll
-      for (int k = 0; k < U; ++k) if (i0 + k * nth < n4) mine[i0 + k * nth] = t[k];
+        for (int k = 0; k < U; ++k) if (i0 + k * nth < n4) mine[i0 + k * nth] = t[k];
+      }
+      for (uint64_t i = n4 * 4 + tid; i < count; i += nth) ((float*)mine)[i] = buf[i];
     }
-    for (uint64_t i = n4 * 4 + tid; i < count; i += nth) ((float*)mine)[i] = buf[i];
-  }
-  if (last_block(&v.done[0]) && threadIdx.x < v.N) {   // fence.sys done by last_block
-    st_release(&dready(v, threadIdx.x)[v.rank].epoch, e);
-    if (threadIdx.x == 0) v.done[0] = 0;
+    if (last_block(&v.done[0]) && threadIdx.x < v.N) {   // fence.sys done by last_block
+      st_release(&dready(v, threadIdx.x)[v.rank].epoch, e);
+      if (threadIdx.x == 0) v.done[0] = 0;
+    }
+    if (phase == 1) return;
   }
   if (threadIdx.x == 0) s_ok = s_ok && wait_flags(dready(v, v.rank), v.N, e, ctl);
   __syncthreads();
@@ -873,15 +882,90 @@ __global__ void __launch_bounds__(512) k_dense_ar(DenseView v, float* __restrict
   }
 }
 
+// ---------------------------------------------------------------- flush / explicit evict (pushes only)
+// het_sync (R16): every dirty resident entry with key in [k0, k1)
+// sends a PUSH record {key, c_c} + its pending row to the owner's inbox at the
+// source's push cursor; the next drain round applies them (per row in source
+// rank order, so the key ranges keep every worker's push of a key in one round).
+__global__ void k_p2p_flush_build(Dev s, P2P m, int64_t k0, int64_t k1) {
+  __shared__ unsigned long long sb[4];
+  bytes_init(sb);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t e0 = (int64_t)w * 32; e0 < s.Ecap; e0 += (int64_t)nw * 32) {
+    const int64_t e = e0 + lane;
+    const int64_t key = e < s.Ecap ? s.ekey[e] : -1;
+    const bool pick = key >= k0 && key < k1 && s.cc[e] > s.cs[e];
+    unsigned mk = __ballot_sync(0xffffffffu, pick);
+    while (mk) {
+      const int src = __ffs(mk) - 1;
+      mk &= mk - 1;
+      const int64_t k = __shfl_sync(0xffffffffu, key, src);
+      const int32_t ee = (int32_t)(e0 + src);
+      push_record(s, m, ee, k, s.cc[ee], lane);
+      if (lane == 0) atomicAdd(&sb[2], 16ull + 4ull * s.D);
+    }
+  }
+  __syncthreads();
+  bytes_flush(s, sb);
+}
+
+// Cache.Evict(key) of the call's unique keys at N > 1: a resident
+// dirty entry sends its PUSH record (delivered by the next drain round), then
+// delete + free.  Warp per unique key.
+__global__ void k_p2p_evict_keys(Dev s, Call c, P2P m) {
+  __shared__ unsigned long long sb[4];
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ unsigned s_dirty, s_ev;
+  bytes_init(sb);
+  dpop_init(dpop);
+  if (threadIdx.x == 0) { s_dirty = 0; s_ev = 0; }
+  __syncthreads();
+  Ctl* ctl = s.ctl;
+  const int lane = threadIdx.x & 31;
+  const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (!ctl->abort && u < ctl->U) {
+    const int64_t key = c.uniq[u];
+    uint64_t slot = 0;
+    const int32_t e = warp_find_slot(s, key, lane, &slot);
+    if (e >= 0) {
+      const uint32_t ecc = s.cc[e], ecs = s.cs[e], prim = s.eprim[e];
+      const bool dirty = ecc > ecs;
+      if (dirty) push_record(s, m, e, key, ecc, lane);
+      if (lane == 0) {
+        if (dirty) atomicAdd(&sb[2], 16ull + 4ull * s.D);
+        s.hkey[slot] = HK_TOMB;
+        atomicAdd(&ctl->n_tomb, 1);
+        if (s.policy == 0) lfu_move(s, key, prim, EP_FREE, dpop);
+        unpin_count(s, prim);
+        s.eprim[e] = EP_FREE;
+        s.ekey[e] = -1;
+        s.fstack[atomicAdd(&ctl->ftop, 1)] = e;
+        atomicAdd(&s_ev, 1u);
+        if (dirty) atomicAdd(&s_dirty, 1u);
+      }
+    }
+  }
+  __syncthreads();
+  dpop_flush(s, dpop);
+  bytes_flush(s, sb);
+  if (threadIdx.x == 0) {
+    if (s_ev) atomicAdd(&s.cnt[C_EVICTIONS], (unsigned long long)s_ev);
+    if (s_dirty) atomicAdd(&s.cnt[C_DIRTY_PUSHES], (unsigned long long)s_dirty);
+  }
+}
+
 struct P2PState {
   P2P v{};
   char* inbox = nullptr;
   std::vector<char*> mapped;     // opened peer bases (to close)
   std::vector<void*> allocs;
-  // dense all-reduce staging (set up by the first call)
+  bool loopback = false;         // N workers on one device: plain pointers, no IPC
+  // dense all-reduce staging (allocated at create; nullptr = NCCL fallback)
   char* dense = nullptr;
   DenseView dv{};
-  bool dense_failed = false;
 };
 
 template <typename T>
@@ -893,77 +977,9 @@ static bool p_alloc(P2PState* p, T** q, size_t count) {
   return true;
 }
 
-het_status_t p2p_create(P2PState*& out, const Dev& d, uint32_t n_max, ncclComm_t comm, cudaStream_t st) {
-  P2PState* p = new P2PState();
-  out = p;
-  P2P& v = p->v;
-  v.N = d.world;
-  v.rank = d.rank;
-  v.CAPS = 3 * (int64_t)n_max;
-  v.REC = 4 + d.D;
-  v.D = d.D;
-  const int N = v.N;
-  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  size_t off = 0;
-  v.off_reqflag = off; off = al(off + sizeof(Flag) * N);
-  v.off_respflag = off; off = al(off + sizeof(Flag) * N);
-  v.off_req = off; off = al(off + sizeof(Rec) * N * v.CAPS);
-  v.off_rows = off; off = al(off + sizeof(float) * N * v.CAPS * d.D);
-  v.off_resp = off; off = al(off + sizeof(float) * N * v.CAPS * v.REC);
-  if (cudaMalloc(&p->inbox, off) != cudaSuccess) return HET_ERR_OOM;
-  cudaMemsetAsync(p->inbox, 0, v.off_req, st);                      // flags: epoch 0
-  cudaIpcMemHandle_t mine;
-  if (cudaIpcGetMemHandle(&mine, p->inbox) != cudaSuccess) return HET_ERR_CUDA;
-  char* dh;
-  if (cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * N) != cudaSuccess) return HET_ERR_OOM;
-  cudaMemcpyAsync(dh + sizeof(cudaIpcMemHandle_t) * d.rank, &mine, sizeof(mine), cudaMemcpyHostToDevice, st);
-  if (ncclAllGather(dh + sizeof(cudaIpcMemHandle_t) * d.rank, dh, sizeof(cudaIpcMemHandle_t), ncclChar, comm, st) !=
-      ncclSuccess)
-    return HET_ERR_NCCL;
-  std::vector<cudaIpcMemHandle_t> all(N);
-  cudaMemcpyAsync(all.data(), dh, sizeof(cudaIpcMemHandle_t) * N, cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
-  cudaFree(dh);
-  std::vector<char*> bases(N);
-  for (int r = 0; r < N; ++r) {
-    if (r == d.rank) { bases[r] = p->inbox; continue; }
-    void* q = nullptr;
-    if (cudaIpcOpenMemHandle(&q, all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return HET_ERR_CUDA;
-    bases[r] = (char*)q;
-    p->mapped.push_back((char*)q);
-  }
-  char** dbases;
-  if (!p_alloc(p, &dbases, N)) return HET_ERR_OOM;
-  cudaMemcpyAsync(dbases, bases.data(), sizeof(char*) * N, cudaMemcpyHostToDevice, st);
-  v.peer = dbases;
-  const int64_t NC = (int64_t)N * v.CAPS;
-  bool ok = p_alloc(p, &v.lcnt, N) && p_alloc(p, &v.c3cnt, N) && p_alloc(p, &v.ridx, NC) &&
-            p_alloc(p, &v.head, d.rows_local) && p_alloc(p, &v.next, NC) && p_alloc(p, &v.leaders, NC) &&
-            p_alloc(p, &v.nlead, 1) && p_alloc(p, &v.done, 4) && p_alloc(p, &v.epoch, 1) &&
-            p_alloc(p, &v.qtot, N) && p_alloc(p, &v.qpush, N) && p_alloc(p, &v.uslot, n_max);
-  if (!ok) return HET_ERR_OOM;
-  cudaMemsetAsync(v.lcnt, 0, 4 * N, st);
-  cudaMemsetAsync(v.c3cnt, 0, 4 * N, st);
-  cudaMemsetAsync(v.head, 0xFF, 4 * d.rows_local, st);
-  cudaMemsetAsync(v.nlead, 0, 4, st);
-  cudaMemsetAsync(v.done, 0, 16, st);
-  cudaMemsetAsync(v.epoch, 0, 8, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
-  return HET_OK;
-}
-
-void p2p_destroy(P2PState* p) {
-  if (!p) return;
-  for (char* q : p->mapped) cudaIpcCloseMemHandle(q);
-  for (void* q : p->allocs) cudaFree(q);
-  if (p->inbox) cudaFree(p->inbox);
-  if (p->dense) cudaFree(p->dense);
-  delete p;
-}
-
 // IPC export of one allocation, import of every peer's (collective over comm)
 static het_status_t exchange_bases(P2PState* p, char* mine_base, int N, int rank, ncclComm_t comm,
-                                   cudaStream_t st, char*** dbases_out) {
+                                   cudaStream_t st, char** dbases) {
   cudaIpcMemHandle_t mine;
   if (cudaIpcGetMemHandle(&mine, mine_base) != cudaSuccess) return HET_ERR_CUDA;
   char* dh;
@@ -984,43 +1000,125 @@ static het_status_t exchange_bases(P2PState* p, char* mine_base, int N, int rank
     bases[r] = (char*)q;
     p->mapped.push_back((char*)q);
   }
-  char** dbases;
-  if (!p_alloc(p, &dbases, N)) return HET_ERR_OOM;
   cudaMemcpyAsync(dbases, bases.data(), sizeof(char*) * N, cudaMemcpyHostToDevice, st);
-  *dbases_out = dbases;
   return HET_OK;
 }
 
-het_status_t p2p_dense_allreduce(P2PState* p, const Dev& d, float* buf, uint64_t count, ncclComm_t comm,
-                                 cudaStream_t st, int* launches) {
-  if (!p->dense) {
-    if (p->dense_failed) return HET_ERR_CAPACITY;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cs);
-    if (cs != cudaStreamCaptureStatusNone) return HET_ERR_CAPACITY;   // set up outside capture only
-    const int N = d.world;
-    const uint64_t cap = (count + 3) & ~3ull;
-    const size_t flags = 2 * 64 * sizeof(Flag);
-    if (N > 64 || cudaMalloc(&p->dense, flags + 2 * cap * sizeof(float)) != cudaSuccess) {
-      p->dense_failed = true;
-      return HET_ERR_CAPACITY;
-    }
-    cudaMemsetAsync(p->dense, 0, flags, st);
-    char** dbases = nullptr;
-    het_status_t rc = exchange_bases(p, p->dense, N, d.rank, comm, st, &dbases);
+// comm == nullptr: loopback worker (p2p_loopback_connect fills the peer tables)
+het_status_t p2p_create(P2PState*& out, const Dev& d, uint32_t n_max, ncclComm_t comm, uint64_t dense_cap,
+                        cudaStream_t st) {
+  P2PState* p = new P2PState();
+  out = p;
+  p->loopback = comm == nullptr;
+  P2P& v = p->v;
+  v.N = d.world;
+  v.rank = d.rank;
+  v.CAPS = 3 * (int64_t)n_max;
+  v.REC = 4 + d.D;
+  v.D = d.D;
+  const int N = v.N;
+  if (N > P2P_MAX_WORLD) return HET_ERR_ARG;   // per-row record lists hold <= 32 records (2 per source)
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t off = 0;
+  v.off_reqflag = off; off = al(off + sizeof(Flag) * N);
+  v.off_respflag = off; off = al(off + sizeof(Flag) * N);
+  v.off_req = off; off = al(off + sizeof(Rec) * N * v.CAPS);
+  v.off_rows = off; off = al(off + sizeof(float) * N * v.CAPS * d.D);
+  v.off_resp = off; off = al(off + sizeof(float) * N * v.CAPS * v.REC);
+  if (cudaMalloc(&p->inbox, off) != cudaSuccess) return HET_ERR_OOM;
+  cudaMemsetAsync(p->inbox, 0, v.off_req, st);                      // flags: epoch 0
+  char** dbases;
+  if (!p_alloc(p, &dbases, N)) return HET_ERR_OOM;
+  v.peer = dbases;
+  if (!p->loopback) {
+    het_status_t rc = exchange_bases(p, p->inbox, N, d.rank, comm, st, dbases);
     if (rc) return rc;
-    DenseView& v = p->dv;
-    v.N = N; v.rank = d.rank; v.peer = dbases; v.cap = cap;
-    if (!p_alloc(p, &v.epoch, 1) || !p_alloc(p, &v.done, 2)) return HET_ERR_OOM;
-    cudaMemsetAsync(v.epoch, 0, 8, st);
-    cudaMemsetAsync(v.done, 0, 8, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
-    // every rank's flags are zero before any rank's first epoch
-    if (ncclAllReduce(v.epoch, v.epoch, 1, ncclUint64, ncclMax, comm, st) != ncclSuccess) return HET_ERR_NCCL;
-    if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
   }
-  if (count > p->dv.cap) return HET_ERR_CAPACITY;
-  k_dense_ar<<<coop_sm_reserve(), 512, 0, st>>>(p->dv, buf, count, 1.0f / (float)d.world, d.ctl);
+  const int64_t NC = (int64_t)N * v.CAPS;
+  bool ok = p_alloc(p, &v.lcnt, N) && p_alloc(p, &v.c3cnt, N) && p_alloc(p, &v.ridx, NC) &&
+            p_alloc(p, &v.head, d.rows_local) && p_alloc(p, &v.next, NC) && p_alloc(p, &v.leaders, NC) &&
+            p_alloc(p, &v.nlead, 1) && p_alloc(p, &v.done, 4) && p_alloc(p, &v.epoch, 1) &&
+            p_alloc(p, &v.qtot, N) && p_alloc(p, &v.qpush, N) && p_alloc(p, &v.uslot, n_max);
+  if (!ok) return HET_ERR_OOM;
+  cudaMemsetAsync(v.lcnt, 0, 4 * N, st);
+  cudaMemsetAsync(v.c3cnt, 0, 4 * N, st);
+  cudaMemsetAsync(v.head, 0xFF, 4 * d.rows_local, st);
+  cudaMemsetAsync(v.nlead, 0, 4, st);
+  cudaMemsetAsync(v.done, 0, 16, st);
+  cudaMemsetAsync(v.epoch, 0, 8, st);
+  // dense all-reduce staging (Eq. 2), set up here -- outside any graph capture,
+  // and agreed by every rank: a rank whose allocation failed makes all of
+  // them use the NCCL all-reduce (no rank-local path choice)
+  const uint64_t cap = (std::max<uint64_t>(dense_cap, 4) + 3) & ~3ull;
+  const size_t flags = 2 * 64 * sizeof(Flag);
+  int ok_dense = cudaMalloc(&p->dense, flags + 2 * cap * sizeof(float)) == cudaSuccess ? 1 : 0;
+  if (!ok_dense) { cudaGetLastError(); p->dense = nullptr; }
+  if (p->dense) cudaMemsetAsync(p->dense, 0, flags, st);
+  DenseView& dv = p->dv;
+  dv.N = N; dv.rank = d.rank; dv.cap = cap;
+  char** dd;
+  if (!p_alloc(p, &dd, N) || !p_alloc(p, &dv.epoch, 1) || !p_alloc(p, &dv.done, 2)) return HET_ERR_OOM;
+  dv.peer = dd;
+  cudaMemsetAsync(dv.epoch, 0, 8, st);
+  cudaMemsetAsync(dv.done, 0, 8, st);
+  if (!p->loopback) {
+    int32_t* dok;
+    if (!p_alloc(p, &dok, 1)) return HET_ERR_OOM;
+    cudaMemcpyAsync(dok, &ok_dense, 4, cudaMemcpyHostToDevice, st);
+    if (ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, comm, st) != ncclSuccess) return HET_ERR_NCCL;
+    cudaMemcpyAsync(&ok_dense, dok, 4, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
+    if (ok_dense) {
+      het_status_t rc = exchange_bases(p, p->dense, N, d.rank, comm, st, dd);
+      if (rc) return rc;
+    } else if (p->dense) {
+      cudaFree(p->dense);
+      p->dense = nullptr;
+    }
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) return HET_ERR_CUDA;
+  return HET_OK;
+}
+
+het_status_t p2p_loopback_connect(P2PState* const* ps, int N, cudaStream_t st) {
+  std::vector<char*> inb(N), den(N);
+  bool dense = true;
+  for (int r = 0; r < N; ++r) {
+    if (!ps[r] || !ps[r]->loopback) return HET_ERR_ARG;
+    inb[r] = ps[r]->inbox;
+    den[r] = ps[r]->dense;
+    dense = dense && ps[r]->dense != nullptr && ps[r]->dv.cap == ps[0]->dv.cap;
+  }
+  for (int r = 0; r < N; ++r) {
+    if (cudaMemcpyAsync((void*)ps[r]->v.peer, inb.data(), sizeof(char*) * N, cudaMemcpyHostToDevice, st) !=
+        cudaSuccess)
+      return HET_ERR_CUDA;
+    if (dense) {
+      cudaMemcpyAsync((void*)ps[r]->dv.peer, den.data(), sizeof(char*) * N, cudaMemcpyHostToDevice, st);
+    } else if (ps[r]->dense) {
+      cudaFree(ps[r]->dense);
+      ps[r]->dense = nullptr;
+    }
+  }
+  return cudaStreamSynchronize(st) == cudaSuccess ? HET_OK : HET_ERR_CUDA;
+}
+
+void p2p_destroy(P2PState* p) {
+  if (!p) return;
+  for (char* q : p->mapped) cudaIpcCloseMemHandle(q);
+  for (void* q : p->allocs) cudaFree(q);
+  if (p->inbox) cudaFree(p->inbox);
+  if (p->dense) cudaFree(p->dense);
+  delete p;
+}
+
+bool p2p_loopback(const P2PState* p) { return p && p->loopback; }
+int64_t p2p_caps(const P2PState* p) { return p->v.CAPS; }
+
+het_status_t p2p_dense_allreduce(P2PState* p, const Dev& d, float* buf, uint64_t count, int phase, cudaStream_t st,
+                                 int* launches) {
+  if (!p->dense || count > p->dv.cap) return HET_ERR_CAPACITY;   // the caller falls back to NCCL
+  k_dense_ar<<<coop_sm_reserve(), 512, 0, st>>>(p->dv, buf, count, 1.0f / (float)d.world, d.ctl, phase);
   *launches += 1;
   return HET_OK;
 }
@@ -1030,20 +1128,44 @@ static int grid_p(int64_t units_warps) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 4));
 }
 
-// one exchange round (after probe); drain = no requests, only pending pushes
-int p2p_round(P2PState* p, const Dev& d, const Call& c, int drain, cudaStream_t st) {
+// one phase of a drain round (drain = no requests, only the pending pushes)
+// or of the non-fused lookup round (after k_probe)
+int p2p_round_phase(P2PState* p, const Dev& d, const Call& c, int drain, int phase, cudaStream_t st) {
   P2P& v = p->v;
-  cudaMemsetAsync(v.lcnt, 0, 4 * v.N, st);
-  k_p2p_build<<<grid_p(std::max(c.n, 1)), 256, 0, st>>>(d, c, v, drain);
-  k_p2p_link<<<148, 256, 0, st>>>(d, v);
-  k_p2p_process<<<148 * 2, 256, 0, st>>>(d, v);
-  k_p2p_install<<<148 * 2, 256, 0, st>>>(d, c, v);
-  return 4;
+  switch (phase) {
+    case RP_BUILD:
+      cudaMemsetAsync(v.lcnt, 0, 4 * v.N, st);
+      k_p2p_build<<<grid_p(std::max(c.n, 1)), 256, 0, st>>>(d, c, v, drain);
+      return 1;
+    case RP_LINK: k_p2p_link<<<148, 256, 0, st>>>(d, v); return 1;
+    case RP_PROCESS: k_p2p_process<<<148 * 2, 256, 0, st>>>(d, v); return 1;
+    default: k_p2p_install<<<148 * 2, 256, 0, st>>>(d, c, v); return 1;
+  }
 }
 
-// fused round: probe+build, owner link, owner process, install+gather
-int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaStream_t st) {
+int p2p_round(P2PState* p, const Dev& d, const Call& c, int drain, cudaStream_t st) {
+  int l = 0;
+  for (int ph = 0; ph < RP_NUM; ++ph) l += p2p_round_phase(p, d, c, drain, ph, st);
+  return l;
+}
+
+// one phase of the fused lookup round (after the dedup): probe+build, link,
+// process, install+gather -- the device functions k_exchange runs between its
+// grid syncs
+int p2p_lookup_phase(P2PState* p, const Dev& d, const Call& c, float* out, int phase, cudaStream_t st) {
   P2P& v = p->v;   // lcnt is zero here: the previous round's publish reset it
+  const int blocks = std::max(1, (c.n + 7) / 8);
+  switch (phase) {
+    case RP_BUILD: k_probe_build<<<blocks, 256, 0, st>>>(d, c, v); return 1;
+    case RP_LINK: k_p2p_link<<<148, 256, 0, st>>>(d, v); return 1;
+    case RP_PROCESS: k_p2p_process<<<148 * 2, 256, 0, st>>>(d, v); return 1;
+    default: k_install_gather<<<blocks, 256, 0, st>>>(d, c, v, out); return 1;
+  }
+}
+
+// fused round as ONE cooperative kernel (one process per GPU)
+int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaStream_t st) {
+  P2P& v = p->v;
   static const bool split = getenv("HET_P2P_SPLIT") != nullptr;   // diagnostic: the four-kernel round
   if (!split) {
     int dev = 0, nsm = 0;
@@ -1059,12 +1181,9 @@ int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaSt
       return 1;
     cudaGetLastError();   // fall through to the split round
   }
-  const int blocks = std::max(1, (c.n + 7) / 8);
-  k_probe_build<<<blocks, 256, 0, st>>>(d, c, v);
-  k_p2p_link<<<148, 256, 0, st>>>(d, v);
-  k_p2p_process<<<148 * 2, 256, 0, st>>>(d, v);
-  k_install_gather<<<blocks, 256, 0, st>>>(d, c, v, out);
-  return 4;
+  int l = 0;
+  for (int ph = 0; ph < RP_NUM; ++ph) l += p2p_lookup_phase(p, d, c, out, ph, st);
+  return l;
 }
 
 P2P* p2p_view_ptr(P2PState* p) { return &p->v; }
@@ -1072,6 +1191,16 @@ P2P* p2p_view_ptr(P2PState* p) { return &p->v; }
 int p2p_pushes(P2PState* p, const Dev& d, void* evbuf, cudaStream_t st) {
   EvView b = *reinterpret_cast<EvView*>(evbuf);
   k_p2p_pushes<<<148 * 2, 256, 0, st>>>(d, p->v, b);
+  return 1;
+}
+
+int p2p_flush_build(P2PState* p, const Dev& d, int64_t k0, int64_t k1, cudaStream_t st) {
+  k_p2p_flush_build<<<148 * 4, 256, 0, st>>>(d, p->v, k0, k1);
+  return 1;
+}
+
+int p2p_evict_keys(P2PState* p, const Dev& d, const Call& c, cudaStream_t st) {
+  k_p2p_evict_keys<<<std::max(1, (c.n + 7) / 8), 256, 0, st>>>(d, c, p->v);
   return 1;
 }
 

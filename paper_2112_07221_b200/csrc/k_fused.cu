@@ -8,21 +8,23 @@
 //  k_lookup_fused  warp per unique key: Cache.Find, CheckValid cond (1)+(2),
 //                  LFU/LRU touch, fused Evict(k)+Fetch(k) / miss install, and
 //                  Cache.Get scattered to every occurrence of the key (K2,
-//                  K4/K5, K6).  The last
-//                  block derives this step's eviction threshold: with LFU
-//                  count bitmaps the victims are exactly {count < T} plus the
-//                  keys <= K* among count T (R9).
+//                  K4/K5, K6).
 //  k_update_fused  cooperative: warp per unique key does the ordered segment
 //                  reduce + SGD + pending + clock (K7/K8)
-//                  while other warps extract the victim keys from the count
-//                  bitmaps (4096-key blocks); after one grid sync every victim
-//                  is evicted by its own warp (Evict push W += p, c_g = max,
-//                  delete, free; K9).  LRU / LFU fallback: generic
-//                  selection then apply.  Hash rebuild, when requested.
+//                  while block 0 derives this step's eviction threshold (with
+//                  LFU count bitmaps the victims are exactly {count < T} plus
+//                  the keys <= K* among count T; R9) and lists the
+//                  bitmap blocks holding victims; after a grid sync the warps
+//                  extract the victim keys (4096-key blocks), after another
+//                  every victim is evicted by its own warp (Evict push W += p,
+//                  c_g = max, delete, free; K9).  LRU / LFU
+//                  fallback: generic selection then apply.  Hash rebuild,
+//                  when requested.
 #include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "evict_dev.cuh"
 #include "p2p_dev.cuh"
@@ -1005,10 +1007,12 @@ constexpr int FUSED_MAX = 8192;
 bool fused_ok(const Dev& s, int n) { return n <= FUSED_MAX; }
 
 int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_devs = 0;   // devices whose function attribute is set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!((attr_devs >> (dev & 63)) & 1)) {
     cudaFuncSetAttribute(k_dd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, FUSED_MAX * 8);
-    attr = true;
+    attr_devs |= 1ull << (dev & 63);
   }
   int blocks = std::max(1, (n + 31) / 32);
   k_dd_fused<<<blocks, DDF_THREADS, (size_t)std::max(n, 1) * 8, st>>>(c.keys, n, pbits, s, c, t, lookup);
@@ -1074,27 +1078,38 @@ int coop_sm_reserve() {
   return r;
 }
 
+// cooperative launch configuration per (device, N > 1, D): the grid leaves
+// coop_sm_reserve() SMs free at N > 1 and the staging depends on D
+struct UpdCfg { int dev; bool multi; uint32_t D; int blocks; size_t smem; int stage_rows; };
+
 int launch_update_fused(const Dev& s, const Call& c, const float* grads, float lr, void* evbuf, cudaStream_t st,
                         const void* p2pview) {
-  static int coop_blocks = 0;
-  static size_t smem = 0;
-  static int stage_rows = 0;
-  static uint32_t forD = 0;
-  if (!coop_blocks || forD != s.D) {
+  static std::vector<UpdCfg> cfgs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const bool multi = s.world > 1;
+  const UpdCfg* cf = nullptr;
+  for (const UpdCfg& x : cfgs)
+    if (x.dev == dev && x.multi == multi && x.D == s.D) cf = &x;
+  if (!cf) {
+    UpdCfg x{dev, multi, s.D, 0, 0, 0};
     const int rowbytes = (int)s.D * 4;
-    stage_rows = std::min(32, 12288 / rowbytes);
-    if (stage_rows < 4) stage_rows = 0;
-    size_t stg = stage_rows ? (size_t)UPD_WARPS * (stage_rows + 1) * rowbytes : 0;
-    smem = std::max(stg, (size_t)SUBMAX * 8);
-    cudaFuncSetAttribute(k_update_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev, sms, per = 0;
-    cudaGetDevice(&dev);
+    x.stage_rows = std::min(32, 12288 / rowbytes);
+    if (x.stage_rows < 4) x.stage_rows = 0;
+    size_t stg = x.stage_rows ? (size_t)UPD_WARPS * (x.stage_rows + 1) * rowbytes : 0;
+    x.smem = std::max(stg, (size_t)SUBMAX * 8);
+    cudaFuncSetAttribute(k_update_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)x.smem);
+    int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_update_fused, UPD_THREADS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_update_fused, UPD_THREADS, x.smem);
     // N > 1: leave NCCL's SMs free (the overlapped dense all-reduce)
-    coop_blocks = (s.world > 1 ? sms - coop_sm_reserve() : sms) * std::max(per, 1);
-    forD = s.D;
+    x.blocks = (multi ? sms - coop_sm_reserve() : sms) * std::max(per, 1);
+    cfgs.push_back(x);
+    cf = &cfgs.back();
   }
+  const int coop_blocks = cf->blocks;
+  const size_t smem = cf->smem;
+  const int stage_rows = cf->stage_rows;
   EvBuf& b = *reinterpret_cast<EvBuf*>(evbuf);
   Dev sd = s;
   Call cd = c;

@@ -36,7 +36,7 @@ class het_dist_t(ctypes.Structure):
 class het_opts_t(ctypes.Structure):
     _fields_ = [("max_keys_per_call", ctypes.c_uint32), ("init_seed", ctypes.c_uint64),
                 ("lfu_persist", ctypes.c_int), ("debug_log", ctypes.c_int),
-                ("pin_threshold", ctypes.c_uint32)]
+                ("pin_threshold", ctypes.c_uint32), ("dense_max", ctypes.c_uint64)]
 
 
 class het_stats_t(ctypes.Structure):
@@ -53,7 +53,9 @@ class het_stats_t(ctypes.Structure):
 EXPORTS = ["het_get_unique_id", "het_cache_create", "het_lookup", "het_update", "het_evict",
            "het_sync", "het_stats", "het_check", "het_read_global", "het_dense_allreduce",
            "het_debug_lookup_log", "het_debug_victims", "het_debug_dump_cache",
-           "het_profile_enable", "het_profile_read", "het_cache_destroy", "het_last_error"]
+           "het_profile_enable", "het_profile_read", "het_cache_destroy", "het_last_error",
+           "het_group_create", "het_group_lookup", "het_group_update", "het_group_evict",
+           "het_group_sync", "het_group_dense_allreduce"]
 
 _lib = None
 
@@ -84,6 +86,12 @@ def load():
         "het_profile_enable": [P, I],
         "het_profile_read": [P, P, P, P, U32, P],
         "het_cache_destroy": [P],
+        "het_group_create": [U32, U64, U32, D, U32, I, P, P, P],
+        "het_group_lookup": [P, U32, P, P, U64, P, P],
+        "het_group_update": [P, U32, P, P, P, F, P],
+        "het_group_evict": [P, U32, P, P, P],
+        "het_group_sync": [P, U32, P],
+        "het_group_dense_allreduce": [P, U32, P, U64, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -135,14 +143,15 @@ def het_get_unique_id() -> bytes:
 
 
 def het_cache_create(rows, D, cache_frac, s, policy=HET_LFU, rank=0, world=1, unique_id=None,
-                     max_keys_per_call=65536, init_seed=0, lfu_persist=1, stream=None, pin_threshold=0):
+                     max_keys_per_call=65536, init_seed=0, lfu_persist=1, stream=None, pin_threshold=0,
+                     dense_max=0):
     lib = load()
     dist = None
     uid = None
     if world > 1:
         uid = ctypes.create_string_buffer(bytes(unique_id), 128)
         dist = het_dist_t(rank, world, ctypes.cast(uid, ctypes.c_void_p))
-    opts = het_opts_t(max_keys_per_call, init_seed, lfu_persist, 0, pin_threshold)
+    opts = het_opts_t(max_keys_per_call, init_seed, lfu_persist, 0, pin_threshold, dense_max)
     h = ctypes.c_void_p()
     rc = lib.het_cache_create(rows, D, cache_frac, s, policy,
                               ctypes.byref(dist) if dist is not None else None,
@@ -201,6 +210,52 @@ def het_profile_read(h):
     return {bytes(names[i]).split(b"\0")[0].decode(): (float(ms[i]), int(cnt[i])) for i in range(k.value)}
 
 
+def _arr(ctype, xs):
+    return (ctype * len(xs))(*xs)
+
+
+def het_group_create(N, rows, D, cache_frac, s, policy=HET_LFU, max_keys_per_call=65536, init_seed=0,
+                     lfu_persist=1, stream=None, pin_threshold=0, dense_max=0):
+    """Loopback group: N workers on the current device (include/het.h); returns the N handles."""
+    opts = het_opts_t(max_keys_per_call, init_seed, lfu_persist, 0, pin_threshold, dense_max)
+    out = (ctypes.c_void_p * N)()
+    _check(None, load().het_group_create(N, rows, D, cache_frac, s, policy, ctypes.byref(opts),
+                                         _stream(stream), out), "het_group_create")
+    return [out[i] for i in range(N)]
+
+
+def het_group_lookup(hs, keys, n, clock, out, stream=None):
+    N = len(hs)
+    _check(hs[0], load().het_group_lookup(_arr(ctypes.c_void_p, hs), N, _arr(ctypes.c_void_p, [_ptr(k) for k in keys]),
+                                          _arr(ctypes.c_uint32, n), clock,
+                                          _arr(ctypes.c_void_p, [_ptr(o) for o in out]), _stream(stream)),
+           "het_group_lookup")
+
+
+def het_group_update(hs, keys, n, grads, lr, stream=None):
+    N = len(hs)
+    _check(hs[0], load().het_group_update(_arr(ctypes.c_void_p, hs), N, _arr(ctypes.c_void_p, [_ptr(k) for k in keys]),
+                                          _arr(ctypes.c_uint32, n), _arr(ctypes.c_void_p, [_ptr(g) for g in grads]),
+                                          ctypes.c_float(lr), _stream(stream)), "het_group_update")
+
+
+def het_group_evict(hs, keys, n, stream=None):
+    N = len(hs)
+    k = None if keys is None else _arr(ctypes.c_void_p, [_ptr(x) for x in keys])
+    nn = None if keys is None else _arr(ctypes.c_uint32, n)
+    _check(hs[0], load().het_group_evict(_arr(ctypes.c_void_p, hs), N, k, nn, _stream(stream)), "het_group_evict")
+
+
+def het_group_sync(hs, stream=None):
+    _check(hs[0], load().het_group_sync(_arr(ctypes.c_void_p, hs), len(hs), _stream(stream)), "het_group_sync")
+
+
+def het_group_dense_allreduce(hs, bufs, count, stream=None):
+    _check(hs[0], load().het_group_dense_allreduce(_arr(ctypes.c_void_p, hs), len(hs),
+                                                   _arr(ctypes.c_void_p, [_ptr(b) for b in bufs]), count,
+                                                   _stream(stream)), "het_group_dense_allreduce")
+
+
 def het_cache_destroy(h):
     if h:
         load().het_cache_destroy(h)
@@ -211,13 +266,14 @@ class HetCache:
     """One worker's cache (torch tensors in, torch tensors out)."""
 
     def __init__(self, rows, D, cache_frac, s, policy=HET_LFU, rank=0, world=1, unique_id=None,
-                 max_keys_per_call=65536, init_seed=0, lfu_persist=1, pin_threshold=0):
+                 max_keys_per_call=65536, init_seed=0, lfu_persist=1, pin_threshold=0, dense_max=0):
         import torch
         self.torch = torch
         self.rows, self.D, self.world, self.rank = rows, D, world, rank
         self.n_max = max_keys_per_call
         self.h = het_cache_create(rows, D, cache_frac, s, policy, rank, world, unique_id,
-                                  max_keys_per_call, init_seed, lfu_persist, pin_threshold=pin_threshold)
+                                  max_keys_per_call, init_seed, lfu_persist, pin_threshold=pin_threshold,
+                                  dense_max=dense_max)
 
     def close(self):
         if self.h:
@@ -312,18 +368,82 @@ class HetCache:
         return k[:e.value], d[:e.value]
 
     def dump_cache(self, cap=1 << 20, rows=True):
-        lib = load()
-        m = ctypes.c_uint32()
-        # size query
-        rc = lib.het_debug_dump_cache(self.h, None, None, None, None, None, None, 0, ctypes.byref(m),
-                                      _stream(None))
-        mm = m.value
-        keys = np.zeros(mm, np.int64)
-        v = np.zeros((mm, self.D), np.float32) if rows else None
-        p = np.zeros((mm, self.D), np.float32) if rows else None
-        cs = np.zeros(mm, np.uint32)
-        cc = np.zeros(mm, np.uint32)
-        prim = np.zeros(mm, np.uint32)
-        _check(self.h, lib.het_debug_dump_cache(self.h, _ptr(keys), _ptr(v), _ptr(p), _ptr(cs), _ptr(cc),
-                                                _ptr(prim), mm, ctypes.byref(m), _stream(None)), "dump")
-        return dict(keys=keys, v=v, p=p, cs=cs, cc=cc, prim=prim)
+        return _dump_cache(self.h, self.D, rows)
+
+
+class _Member:
+    """Inspection view of one loopback worker (non-collective calls only)."""
+
+    def __init__(self, h, D, n_max, rank, world):
+        self.h, self.D, self.n_max, self.rank, self.world = h, D, n_max, rank, world
+
+    stats = HetCache.stats
+    read_global = HetCache.read_global
+    lookup_log = HetCache.lookup_log
+    victims = HetCache.victims
+
+    def dump_cache(self, rows=True):
+        return _dump_cache(self.h, self.D, rows)
+
+
+class HetGroup:
+    """N loopback workers on one GPU (het_group_*): every collective call takes
+    per-worker lists and drives the workers phase by phase."""
+
+    def __init__(self, N, rows, D, cache_frac, s, policy=HET_LFU, max_keys_per_call=65536, init_seed=0,
+                 lfu_persist=1, pin_threshold=0, dense_max=0):
+        import torch
+        self.torch = torch
+        self.N, self.rows, self.D, self.n_max = N, rows, D, max_keys_per_call
+        self.hs = het_group_create(N, rows, D, cache_frac, s, policy, max_keys_per_call, init_seed, lfu_persist,
+                                   pin_threshold=pin_threshold, dense_max=dense_max)
+        self.workers = [_Member(h, D, max_keys_per_call, i, N) for i, h in enumerate(self.hs)]
+
+    def close(self):
+        if self.hs:
+            for h in self.hs:
+                het_cache_destroy(h)
+            self.hs = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def lookup(self, keys, t):
+        torch = self.torch
+        outs = [torch.empty((k.numel(), self.D), dtype=torch.float32, device=k.device) for k in keys]
+        het_group_lookup(self.hs, keys, [k.numel() for k in keys], t, outs)
+        return outs
+
+    def update(self, keys, grads, lr):
+        het_group_update(self.hs, keys, [k.numel() for k in keys], grads, lr)
+
+    def evict(self, keys=None):
+        if keys is None:
+            het_group_evict(self.hs, None, None)
+        else:
+            het_group_evict(self.hs, keys, [k.numel() for k in keys])
+
+    def sync(self):
+        het_group_sync(self.hs)
+
+    def dense_allreduce(self, bufs):
+        het_group_dense_allreduce(self.hs, bufs, bufs[0].numel())
+
+
+def _dump_cache(h, D, rows=True):
+    lib = load()
+    m = ctypes.c_uint32()
+    lib.het_debug_dump_cache(h, None, None, None, None, None, None, 0, ctypes.byref(m), _stream(None))  # size query
+    mm = m.value
+    keys = np.zeros(mm, np.int64)
+    v = np.zeros((mm, D), np.float32) if rows else None
+    p = np.zeros((mm, D), np.float32) if rows else None
+    cs = np.zeros(mm, np.uint32)
+    cc = np.zeros(mm, np.uint32)
+    prim = np.zeros(mm, np.uint32)
+    _check(h, lib.het_debug_dump_cache(h, _ptr(keys), _ptr(v), _ptr(p), _ptr(cs), _ptr(cc),
+                                       _ptr(prim), mm, ctypes.byref(m), _stream(None)), "dump")
+    return dict(keys=keys, v=v, p=p, cs=cs, cc=cc, prim=prim)

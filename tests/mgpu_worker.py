@@ -40,7 +40,7 @@ def main():
     else:
         R, D, n_max, cards = 1000, 8, 4096, gen.cards_for("toy")
     g = het.HetCache(R, D, frac, s, policy, rank=rank, world=world, unique_id=obj[0], max_keys_per_call=n_max,
-                     pin_threshold=pin)
+                     pin_threshold=pin, dense_max=2048)
     o = Oracle(R=R, D=D, C=capacity(frac, R), s=s, policy=policy, N=world, pin_threshold=pin)
     for t in range(T):
         if shape == "reddit":
@@ -79,7 +79,7 @@ def main():
     np.testing.assert_allclose(gr, orows, rtol=1e-6, atol=1e-30)
     # dense all-reduce (Eq. 2): mean over workers
     # (peer-memory one-shot mean; epochs reuse the two staging buffers; a
-    # shorter call exercises the scalar tail; a longer one falls back to NCCL)
+    # shorter call exercises the scalar tail; one beyond dense_max falls back to NCCL)
     for k, cnt in enumerate([1000, 1000, 998, 1000, 4096]):
         x = torch.arange(cnt, device="cuda", dtype=torch.float32) * (rank + 1) + k
         het.het_dense_allreduce(g.h, x, x.numel())

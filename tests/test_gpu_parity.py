@@ -306,6 +306,47 @@ def test_errors_are_reported():
         g.lookup(torch.zeros(65, dtype=torch.int64, device="cuda"), 1)  # n > n_max
 
 
+def test_update_keys_must_be_the_lookups():
+    """Alg. 3 writes the keys Alg. 2 read; a write of keys
+    the read did not return is a protocol violation.
+    Another length: HET_ERR_PROTOCOL at once.  The lookup's buffer, or a copy
+    of its keys: accepted, results as the oracle's.  Other keys of the same
+    length: sticky HET_ERR_PROTOCOL and the update is skipped -- no entry of
+    the cache changes."""
+    het = _het()
+    R, D = 1000, 8
+    o = Oracle(R=R, D=D, C=capacity(0.1, R), s=10)
+    g = het.HetCache(R, D, 0.1, 10, max_keys_per_call=4096)
+    for t in range(6):                       # the lookup's pointer / a device copy / a host copy
+        keys = toy_keys(t)
+        grads = gen.grads(0, t, keys.size, D).numpy()
+        kd = torch.from_numpy(keys).cuda()
+        assert_rows(g.lookup(kd, t).cpu().numpy(), o.lookup(t, [keys])[0])
+        upd = [kd, kd.clone(), keys.copy()][t % 3]
+        het.het_update(g.h, upd, keys.size, torch.from_numpy(grads).cuda(), LR)
+        o.update([grads], LR)
+        het.het_check(g.h)
+    keys = toy_keys(6)
+    kd = torch.from_numpy(keys).cuda()
+    g.lookup(kd, 6)
+    with pytest.raises(het.HetError) as e:   # another n
+        g.update(kd[:-1], torch.zeros(keys.size - 1, D, device="cuda"), LR)
+    assert e.value.code == 3
+    before = g.dump_cache()
+    other = kd.clone()
+    other[keys.size // 2] = (other[keys.size // 2] + 1) % R
+    if bool((other == kd).all()):
+        other[0] = (other[0] + 1) % R
+    g.update(other, torch.ones(keys.size, D, device="cuda"), LR)
+    with pytest.raises(het.HetError) as e:
+        het.het_check(g.h)
+    assert e.value.code == 3
+    after = g.dump_cache()
+    for k in ["keys", "v", "p", "cs", "cc", "prim"]:
+        assert np.array_equal(before[k], after[k]), k
+    g.close()
+
+
 def test_host_pointer_path():
     """Host buffers are staged by the library (the e2e path of bench.py)."""
     het = _het()
