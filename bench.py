@@ -58,7 +58,26 @@ def workload_cfg(name, world):
     else:
         raise ValueError(name)
     c["name"] = {"wdl": "WDL", "dcn": "DCN", "reddit": "Reddit-GraphSAGE", "scale": "scale-D4096"}[name]
+    c["key"] = name
     return c
+
+
+DATA = {"criteo": "synthetic (seeded Zipf Criteo-shaped keys, counter-hash fp32 grads)",
+        "scale": "synthetic (seeded Zipf Criteo-shaped keys over fields scaled to the table, counter-hash fp32 grads)",
+        "reddit": "synthetic (seeded Zipf(1.0) Reddit-shaped node ids, all distinct per step; counter-hash fp32 grads)"}
+
+
+def config_dict(world, use_dense):
+    """The workload of a line -- identical in both arms (the driver compares them)."""
+    R = CFG["rows"]
+    return {"workload": CFG["name"], "rows": R, "D": CFG["D"], "batch_per_gpu": CFG["batch"],
+            "keys_per_gpu_step": CFG["n"], "fields": CFG["fields"], "cache_frac": CFG["cache_frac"],
+            "cache_entries_per_gpu": int(math.floor(CFG["cache_frac"] * R)), "s": CFG["s"],
+            "policy": CFG["policy"], "zipf_alpha": CFG["alpha"],
+            "dense_params": CFG["dense_params"] if world > 1 else 0,
+            "parallelism": f"hash-sharded table x{world}, dp{world}",
+            "phase": "steady state: cache filled to C from t = 0 before timing (GPU and oracle alike)",
+            "l2": "flushed between timed steps (256 MB write outside the step events)"}
 
 
 CFG = workload_cfg("wdl", 1)       # mutated by main() for the selected workload
@@ -212,6 +231,7 @@ def run_gpu(args):
     R = CFG["rows"]
     lr = CFG["lr"]
     uid = None
+    cpu_base = CpuBaseline() if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
     if world > 1:
         obj = [het.het_get_unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(obj, src=0)
@@ -370,11 +390,12 @@ def run_gpu(args):
     GH = len(grads_h)
     out_h = torch.empty((n, D), dtype=torch.float32).pin_memory()
     te0, te1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for j in range(W):
-        het.het_lookup(cache.h, keys_h[j], n, AUTO, out_h)
-        het.het_update(cache.h, keys_h[j], n, grads_h[j % GH], lr)
+    for j in range(max(W, 50)):                   # >= 50 warm host-buffer steps (staging buffers, page-in)
+        het.het_lookup(cache.h, keys_h[j % (W + K)], n, AUTO, out_h)
+        het.het_update(cache.h, keys_h[j % (W + K)], n, grads_h[j % GH], lr)
     barrier(world, device)
     e2e_ms = 0.0
+    e2e_all = []
     for j in range(K):
         between_steps(j)
         te0.record(st)
@@ -387,26 +408,20 @@ def run_gpu(args):
             st.wait_stream(side)
         te1.record(st)
         te1.synchronize()
-        e2e_ms += te0.elapsed_time(te1)
+        e2e_all.append(te0.elapsed_time(te1))
+        e2e_ms += e2e_all[-1]
     e2e_ms = max_over_ranks(e2e_ms / K, world, device)
+    e2e_med = max_over_ranks(statistics.median(e2e_all), world, device)
 
     value = n * world / (ms * 1e-3)
-    DATA = {"criteo": "synthetic (seeded Zipf Criteo-shaped keys, counter-hash fp32 grads)",
-            "scale": "synthetic (seeded Zipf Criteo-shaped keys over fields scaled to the table, counter-hash fp32 grads)",
-            "reddit": "synthetic (seeded Zipf(1.0) Reddit-shaped node ids, all distinct per step; counter-hash fp32 grads)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": DATA[CFG["keys"]],
-        "config": {"workload": CFG["name"], "rows": R, "D": D, "batch_per_gpu": B,
-                   "keys_per_gpu_step": n, "fields": F, "cache_frac": CFG["cache_frac"],
-                   "cache_entries_per_gpu": C,
-                   "s": CFG["s"], "policy": CFG["policy"], "zipf_alpha": CFG["alpha"],
-                   "dense_params": CFG["dense_params"] if use_dense else 0,
-                   "parallelism": f"hash-sharded table x{world}, dp{world}",
-                   "l2": "flushed between timed steps (256 MB write outside the step events)"
-                   + ("; ranks re-aligned after the flush by a 1-element all-reduce, outside the events" if world > 1 else ""),
-                   "fill_steps": fill_steps, "fill_s": round(fill_s, 1), "grad_pool": G},
+        "config": config_dict(world, use_dense),
+        "setup": {"fill_steps": fill_steps, "fill_s": round(fill_s, 1), "grad_pool": G,
+                  "rank_alignment": "ranks re-aligned after the L2 flush by a 1-element all-reduce, outside the events"
+                  if world > 1 else None},
         "samples_per_s": B * world / (ms * 1e-3),
         "unique_rows_per_s": sd["unique"] / K * world / (ms * 1e-3),
         "step_counters": {k: v / K for k, v in sd.items()},
@@ -419,6 +434,8 @@ def run_gpu(args):
         "nvlink": nvlink_fraction(kern, wire, world, device) if world > 1 else None,
         "clocks": clocks,
         "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "ms_per_step_median": e2e_med, "value_median": n * world / (e2e_med * 1e-3),
+                "warm_steps": max(W, 50),
                 "h2d_bytes_per_step": n * 8 + n * D * 4, "d2h_bytes_per_step": n * D * 4},
     }
     del graph
@@ -427,8 +444,8 @@ def run_gpu(args):
         line["hbm_sweep"] = run_sweep(het, device)
     barrier(world, device)
     cache.close()
-    if rank == 0 and world == 1:
-        line["cpu_baseline"] = cpu_baseline(args)
+    if cpu_base is not None:
+        line["cpu_baseline"] = cpu_base.result()
     return line, rank, world
 
 
@@ -501,39 +518,83 @@ def run_sweep(het, device):
 
 
 # ----------------------------------------------------------------------------- oracle legs
-def oracle_sample(steps, warmup, world=1, budget_s=15.0):
-    """The CPU oracle (as it stands) on the selected workload from a cold
-    cache, simulating `world` lock-step workers on one core: `warmup` untimed
-    iterations, then up to `steps` timed ones, stopping early once `budget_s`
-    of CPU time is spent (a bounded sample).  Full D rows.  Returns
-    (rows/s, seconds, timed iterations)."""
+ORACLE_CORE = 0          # the oracle runs pinned to one host core (taskset -c 0)
+
+
+def _pin(core):
+    try:
+        os.sched_setaffinity(0, {core})
+        return True
+    except (AttributeError, OSError):
+        return False
+
+
+def oracle_steady(world, warmup, steps, budget_s, fill_budget_s=240.0, mem_budget=16e9, go=None):
+    """The CPU oracle (as it stands) on the selected workload at the SAME
+    protocol phase as the GPU arm: a clocks-only fill (rows not tracked) runs
+    the workload's iterations from t = 0 until every worker's cache holds C
+    entries -- the GPU arm's fill criterion -- then every resident entry gets
+    its row (as at a Fetch) and full-D iterations follow: `warmup` untimed,
+    then up to `steps` timed ones, stopping once `budget_s` is spent.  The
+    N-worker simulation runs all workers in lock step on this one core.
+    `go`: called between the untimed and the timed part (the bench's
+    cpu_baseline waits there until the GPU timing is over).  Returns a dict."""
     from oracle.oracle import Oracle, capacity
     n, D, R = CFG["n"], CFG["D"], CFG["rows"]
-    o = Oracle(R=R, D=D, C=capacity(CFG["cache_frac"], R), s=CFG["s"], N=world)
-    keys = [make_keys(i, 0, warmup + steps, "cpu").numpy() for i in range(world)]
-    G = max(4, min(warmup + steps, int(1e9 // (n * D * 4 * world))))
-    grads = [[gen.grads(i, j, n, D).numpy() for i in range(world)] for j in range(G)]
+    C = capacity(CFG["cache_frac"], R)
+    o = Oracle(R=R, D=D, C=C, s=CFG["s"], N=world, track_div=1 << 62)
+    chunk = 500 if CFG["keys"] != "reddit" else 20
+    t, t0 = 0, time.perf_counter()
+    full = False
+    while time.perf_counter() - t0 < fill_budget_s:
+        keys = [make_keys(i, t, chunk, "cpu").numpy() for i in range(world)]
+        for j in range(chunk):
+            o.lookup(t + j, [keys[i][j] for i in range(world)], want_out=False)
+            o.update(None, CFG["lr"])
+        t += chunk
+        if min(o.cache_size(i) for i in range(world)) >= C:
+            full = True
+            break
+    fill_s = time.perf_counter() - t0
+    resident = sum(o.cache_size(i) for i in range(world))
+    track_div = max(1, math.ceil(resident * 2 * D * 4 / mem_budget))   # rows of v and p in host memory
+    o.set_track_div(track_div)
+    T = warmup + steps
+    keys = [make_keys(i, t, T, "cpu").numpy() for i in range(world)]
+    G = max(2, min(T, int(1e9 // (n * D * 4 * world))))
+    grads = [[gen.grads(i, t + j, n, D).numpy() for i in range(world)] for j in range(G)]
     for j in range(warmup):
-        o.lookup(j, [keys[i][j] for i in range(world)], want_out=False)
+        o.lookup(t + j, [keys[i][j] for i in range(world)])
         o.update(grads[j % G], CFG["lr"])
+    if go is not None:
+        go()
+    s0 = o.stats(0)
     done = 0
-    t0 = time.perf_counter()
-    for j in range(warmup, warmup + steps):
-        o.lookup(j, [keys[i][j] for i in range(world)])
+    t1 = time.perf_counter()
+    for j in range(warmup, T):
+        o.lookup(t + j, [keys[i][j] for i in range(world)])
         o.update(grads[j % G], CFG["lr"])
         done += 1
-        if time.perf_counter() - t0 > budget_s:
+        if time.perf_counter() - t1 > budget_s:
             break
-    dt = time.perf_counter() - t0
-    return n * world * done / dt, dt, done
+    dt = time.perf_counter() - t1
+    s1 = o.stats(0)
+    ev = (s1["evictions"] - s0["evictions"]) / max(done, 1)
+    return {"value": n * world * done / dt, "dt": dt, "done": done, "fill_steps": t, "fill_s": fill_s,
+            "full": full, "resident": resident, "capacity": C * world, "track_div": track_div,
+            "evictions_per_step": ev, "t0": t + warmup}
 
 
-def cpu_baseline(args, steps=300):
-    v, dt, done = oracle_sample(steps, 5)
-    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{CFG['name']} config, iterations 5..{5 + done} from a cold cache (full D={CFG['D']} rows), "
-                      f"single-threaded C++ oracle, {dt:.1f} s; host: {os.cpu_count()} cores, "
-                      f"{_cpu_model()}"}
+def _sample_text(r, world, warmup):
+    state = ("cache full" if r["full"] else
+             f"cache at {r['resident'] / r['capacity']:.0%} of C after the {r['fill_s']:.0f} s fill budget")
+    rows = "full D=%d rows" % CFG["D"] if r["track_div"] == 1 else \
+        f"D={CFG['D']} rows for 1/{r['track_div']} of the keys (host-memory bound)"
+    return (f"{CFG['name']} iterations {r['t0']}..{r['t0'] + r['done']} after a clocks-only fill of "
+            f"{r['fill_steps']} iterations ({state}, {r['evictions_per_step']:.0f} evictions/step of worker 0) "
+            f"and {warmup} untimed full-row iterations; {rows}; {world} worker(s) simulated in lock step; "
+            f"single-threaded C++ oracle pinned to core {ORACLE_CORE} (taskset); {r['dt']:.1f} s timed; "
+            f"host: {os.cpu_count()} cores, {_cpu_model()}")
 
 
 def _cpu_model():
@@ -546,27 +607,67 @@ def _cpu_model():
     return "unknown"
 
 
+def oracle_child_main(args):
+    """`--impl oracle-child`: the cpu_baseline leg as a separate process pinned
+    to ORACLE_CORE, started at the beginning of the GPU bench.  It fills, then
+    prints READY and waits for GO on stdin (sent after the GPU timing), then
+    times its sample and prints one JSON line."""
+    pinned = _pin(ORACLE_CORE)
+
+    def go():
+        print("READY", flush=True)
+        sys.stdin.readline()
+    r = oracle_steady(1, 5, 2000, budget_s=15.0, go=go)
+    r["pinned"] = pinned
+    r["sample"] = _sample_text(r, 1, 5)
+    print(json.dumps(r), flush=True)
+
+
+class CpuBaseline:
+    """cpu_baseline of the N = 1 GPU bench: the oracle child process fills
+    while the GPU arm runs (on other cores), and times its sample after."""
+
+    def __init__(self):
+        self.p = subprocess.Popen([sys.executable, os.path.abspath(__file__), "--impl", "oracle-child",
+                                   "--workload", CFG["key"]], stdin=subprocess.PIPE, stdout=subprocess.PIPE,
+                                  text=True, cwd=ROOT)
+        try:   # the GPU arm stays off the oracle's core
+            os.sched_setaffinity(0, set(os.sched_getaffinity(0)) - {ORACLE_CORE} or {ORACLE_CORE})
+        except (AttributeError, OSError):
+            pass
+
+    def result(self):
+        line = self.p.stdout.readline()          # READY (the fill is over)
+        if line.strip() != "READY":
+            return {"error": "oracle child failed: " + line.strip()}
+        self.p.stdin.write("GO\n")
+        self.p.stdin.flush()
+        out = self.p.stdout.readline()
+        self.p.wait()
+        r = json.loads(out)
+        return {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle", "sample": r["sample"],
+                "steady_state": r["full"], "evictions_per_step": r["evictions_per_step"]}
+
+
 def run_reference(args):
     """The reference arm: the CPU oracle of the paper's protocol (there is no
-    reference code to install), on this arm's workload with
-    `world` simulated workers, rank 0 only."""
+    reference code to install), on this arm's workload and
+    config at the GPU arm's protocol phase (steady state), `world` simulated
+    workers, rank 0 only, pinned to one core."""
     rank, world, _ = dist_env()
     if rank != 0:
         return None
-    v, dt, done = oracle_sample(args.steps, args.warmup, world, budget_s=120.0)
-    ms = dt / done * 1e3
-    sample = (f"{CFG['name']} iterations {args.warmup}..{args.warmup + done} from a cold cache, {world} worker(s) "
-              f"simulated in lock step, single-threaded C++ oracle of the paper's protocol"
-              + (f" (stopped after {done} of {args.steps} steps: 120 s budget)" if done < args.steps else "")
-              + f"; {os.cpu_count()} host cores, {_cpu_model()}")
-    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+    _pin(ORACLE_CORE)
+    r = oracle_steady(world, args.warmup, args.steps, budget_s=120.0)
+    ms = r["dt"] / max(r["done"], 1) * 1e3
+    sample = _sample_text(r, world, args.warmup) + (
+        f" (stopped after {r['done']} of {args.steps} steps: 120 s budget)" if r["done"] < args.steps else "")
+    return {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": CFG["name"], "rows": CFG["rows"], "D": CFG["D"],
-                       "batch_per_gpu": CFG["batch"], "keys_per_gpu_step": CFG["n"],
-                       "cache_frac": CFG["cache_frac"], "s": CFG["s"], "policy": CFG["policy"]},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": DATA[CFG["keys"]],
+            "config": config_dict(world, use_dense=False),
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def main():
@@ -574,13 +675,17 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference", "oracle-child"])
+    ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the oracle's cpu_baseline leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the D=128 n-sweep (HBM regime)")
     ap.add_argument("--workload", default="auto", choices=["auto", "wdl", "dcn", "reddit", "scale"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     CFG.clear()
     CFG.update(workload_cfg(args.workload, dist_env()[1]))
+    if args.impl == "oracle-child":
+        oracle_child_main(args)
+        return
     if args.impl == "reference":
         line = run_reference(args)
         if line is not None:

@@ -357,6 +357,23 @@ void* orc_create(int64_t R, uint32_t D, int64_t C, uint32_t s, int policy, int N
   return o;
 }
 void orc_destroy(void* h) { delete (Oracle*)h; }
+// Bench infrastructure only (bench.py cpu_baseline / --impl reference; no
+// parity test calls it): change which keys carry row values.  A clocks-only
+// fill (track_div huge) brings the cache to steady state fast; switching to
+// full rows then gives every resident entry that had none the server row as
+// at a Fetch (v = W[k], p = 0).  Decisions never depend on row values,
+// so the protocol phase is unchanged; row VALUES after the switch are not the
+// protocol's and must not be compared.
+void orc_set_track_div(void* h, int64_t track_div) {
+  Oracle* o = (Oracle*)h;
+  o->track_div = track_div;
+  for (Worker& wk : o->w)
+    for (auto& kv : wk.cache)
+      if (o->tracked(kv.first) && kv.second.v.size() != o->D) {
+        kv.second.v = o->Wrow(kv.first);
+        kv.second.p.assign(o->D, 0.0f);
+      }
+}
 int orc_lookup(void* h, uint64_t t, const int64_t* keys, const int64_t* n_per, float* out) {
   return ((Oracle*)h)->lookup(t, keys, n_per, out);
 }

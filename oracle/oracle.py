@@ -74,6 +74,7 @@ def _load():
         lib.orc_cache_size.argtypes = [P, I]
         lib.orc_dump_cache.argtypes = [P, I, P, P, P, P, P, P, P]
         lib.orc_read_global.argtypes = [P, P, I64, P, P]
+        lib.orc_set_track_div.argtypes = [P, I64]
         lib.orc_w0.restype = ctypes.c_float
         lib.orc_w0.argtypes = [U64, I64, U32]
         _lib = lib
@@ -190,6 +191,12 @@ class Oracle:
                                 _ptr(d["p"]) if D else None, _ptr(d["cs"]), _ptr(d["cc"]),
                                 _ptr(d["count"]), _ptr(d["tick"]))
         return d
+
+    def set_track_div(self, track_div: int):
+        """Bench only: which keys carry row values from now on (a clocks-only
+        fill, then full rows).  Entries gaining rows get the server row as at
+        a Fetch, so row values after the switch are not the protocol's."""
+        self.lib.orc_set_track_div(self.h, int(track_div))
 
     def read_global(self, keys):
         keys = np.ascontiguousarray(np.asarray(keys, np.int64).reshape(-1))

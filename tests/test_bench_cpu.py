@@ -12,14 +12,20 @@ sys.path.insert(0, ROOT)
 
 def test_reference_arm_json_line():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "3",
-                        "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+                        "--warmup", "1", "--workload", "reddit"], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "config", "cpu_baseline", "e2e"):
         assert k in line, k
-    assert line["impl"] == "reference" and line["value"] > 0 and line["config"]["workload"] == "WDL"
+    assert line["impl"] == "reference" and line["value"] > 0 and line["config"]["workload"] == "Reddit-GraphSAGE"
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] == 1
+    assert "cache full" in line["cpu_baseline"]["sample"]          # the GPU arm's protocol phase
+    import bench
+    bench.CFG.clear()
+    bench.CFG.update(bench.workload_cfg("reddit", 1))
+    assert line["config"] == json.loads(json.dumps(bench.config_dict(1, use_dense=False)))   # same_config
     assert line["e2e"]["h2d_bytes_per_step"] == 0
 
 

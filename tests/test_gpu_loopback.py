@@ -187,3 +187,34 @@ def test_loopback_member_calls_are_rejected():
     with pytest.raises(het.HetError):
         het.het_group_lookup(g.hs[::-1], [k, k], [4, 4], 0, [out, out])   # not in rank order
     g.close()
+
+
+def test_loopback_flush_rounds_split():
+    """het_sync over the exchange when one key bin holds more dirty entries
+    than a round carries (n_max = 32: 96 records per source): the bin is
+    split again; the flushed table equals the oracle's (R16)."""
+    het = _het()
+    N, R, D, n, frac = 2, 400_000, 4, 32, 0.002
+    g = het.HetGroup(N, R, D, frac, 5, LFU, max_keys_per_call=n)
+    o = Oracle(R=R, D=D, C=capacity(frac, R), s=5, N=N)
+    rng = np.random.default_rng(7)
+    for t in range(60):
+        keys = [rng.integers(0, 800, size=n).astype(np.int64) for _ in range(N)]
+        grads = [gen.grads(i, t, n, D).numpy() for i in range(N)]
+        kd = [torch.from_numpy(k).cuda() for k in keys]
+        outs = g.lookup(kd, t)
+        oo = o.lookup(t, keys)
+        for i in range(N):
+            np.testing.assert_allclose(outs[i].cpu().numpy(), oo[i], rtol=1e-6, atol=1e-30)
+        g.update(kd, [torch.from_numpy(x).cuda() for x in grads], LR)
+        o.update(grads, LR)
+    assert min(o.cache_size(i) for i in range(N)) > 3 * n * 2   # more dirty rows in bin 0 than one round carries
+    g.sync()
+    o.flush()
+    for i in range(N):
+        owned = np.arange(i, 1000, N, dtype=np.int64)
+        gr, gcg = g.workers[i].read_global(owned)
+        orows, ocg = o.read_global(owned)
+        assert np.array_equal(gcg, ocg), i
+        np.testing.assert_allclose(gr, orows, rtol=1e-6, atol=1e-30)
+    g.close()
