@@ -522,6 +522,9 @@ ORACLE_CORE = 0          # the oracle runs pinned to one 
 
 
 def _pin(core):
+    """Pin this process to one core; torch's CPU ops (the input generator)
+    then use one thread too, instead of a pool oversubscribing that core."""
+    torch.set_num_threads(1)
     try:
         os.sched_setaffinity(0, {core})
         return True
@@ -636,14 +639,22 @@ class CpuBaseline:
         except (AttributeError, OSError):
             pass
 
-    def result(self):
-        line = self.p.stdout.readline()          # READY (the fill is over)
-        if line.strip() != "READY":
-            return {"error": "oracle child failed: " + line.strip()}
+    def _line(self, timeout):
+        import select
+        r, _, _ = select.select([self.p.stdout], [], [], timeout)
+        return self.p.stdout.readline() if r else None
+
+    def result(self, timeout=400.0):
+        line = self._line(timeout)               # READY (the fill is over)
+        if line is None or line.strip() != "READY":
+            self.p.kill()
+            return {"error": "oracle child failed or timed out: " + str(line).strip()}
         self.p.stdin.write("GO\n")
         self.p.stdin.flush()
-        out = self.p.stdout.readline()
+        out = self._line(timeout)
         self.p.wait()
+        if not out:
+            return {"error": "oracle child timed out"}
         r = json.loads(out)
         return {"value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle", "sample": r["sample"],
                 "steady_state": r["full"], "evictions_per_step": r["evictions_per_step"]}

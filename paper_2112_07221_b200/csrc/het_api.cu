@@ -64,6 +64,8 @@ struct het_cache {
   uint32_t last_n = 0;
   const int64_t* last_keys = nullptr;  // the lookup's keys as passed by the caller
   bool no_fused = false;       // env HET_NO_FUSED (read once at create)
+  bool ev_pending = false;     // a fused update may have left listed victims (evicted by the next call's first kernel)
+  bool ev_captured = false;    // a fused update was captured into a CUDA graph (replays leave victims listed)
   std::shared_ptr<het_group> group;    // loopback member (nullptr: one process per GPU)
   int64_t overflow_bound = 0;  // worst-case residents above C since the last eviction
   uint64_t lookups = 0, keys = 0, updates = 0, launches = 0;
@@ -313,8 +315,7 @@ static het_status_t create_impl(uint64_t rows, uint32_t D, double cache_frac, ui
   A(d.eprim, d.Ecap);
   A(d.estep, d.Ecap);
   A(d.fstack, d.Ecap);
-  A(d.hkey, (size_t)S);
-  A(d.hval, (size_t)S);
+  A(d.hslot, (size_t)S);
   A(d.count_by_key, d.lfu_persist ? rows : 1);
   d.bm_words = ((int64_t)rows + 31) / 32;
   d.nbk = ((int64_t)rows + (1 << LFU_BLK_SHIFT) - 1) >> LFU_BLK_SHIFT;
@@ -348,6 +349,12 @@ static het_status_t create_impl(uint64_t rows, uint32_t D, double cache_frac, ui
     A(c.sortbuf1, nm);
     A(c.blockbuf, nm / 1024 + 2);
     A(c.hlist, nm);
+    A(c.urec, nm);
+    A(c.upos, nm);
+    A(c.dbg_status, nm);
+    A(c.dbg_inverse, nm);
+    A(c.dbg_U, 1);
+    c.pbits = h->pbits;
     A(c.hbuf, (size_t)nm * ((D + 15) / 16) * 16);
     c.hcap = (int)nm;
     uint32_t *hist, *khist;
@@ -462,6 +469,20 @@ struct Members {
   int n;
 };
 static P2PState* p2p_of(het_cache* h) { return mgpu_p2p(h->mg); }
+static const void* p2p_view(het_cache* h) { return h->d.world > 1 ? (const void*)p2p_view_ptr(p2p_of(h)) : nullptr; }
+
+// the overflow eviction the last fused update deferred (its victims are
+// listed): run it before anything that reads or changes the cache
+// (inspection calls -- het_stats, het_check, het_debug_* -- pass count =
+// false: the launch counter reports the hot path's kernels)
+static void flush_evict(het_cache* h, cudaStream_t st, bool count = true) {
+  // after a captured update, any graph replay may have listed victims: the
+  // kernel tests the device flag (cheap when nothing is listed)
+  if (!h->ev_pending && !h->ev_captured) return;
+  const int l = launch_evict_pending(h->d, h->evbuf_host, p2p_view(h), st);
+  if (count) h->launches += l;
+  h->ev_pending = false;
+}
 
 static het_status_t check_members(het_cache* const* hs, uint32_t N) {
   if (!hs || N < 2 || !hs[0] || !hs[0]->group) return HET_ERR_ARG;
@@ -516,10 +537,20 @@ static het_status_t lookup_pre(het_cache* h, const int64_t* keys, uint32_t n, ui
   // per-phase kernels with the sliced heavy-key segment reduce), N > 1 over
   // the peer-memory exchange for every n; the dedup kernel follows n
   h->fused = !h->no_fused && (d.world == 1 ? (int)n <= FUSED_LOOKUP_MAX : mgpu_p2p(h->mg) != nullptr);
-  if (h->fused && fused_ok(d, (int)n)) {
+  // N = 1 after the fused dedup: per-key work indexed by sorted position (no compaction pass)
+  c.rmode = (h->fused && fused_ok(d, (int)n) && d.world == 1) ? 1 : 0;
+  if (h->fused && fused_ok(d, (int)n)) {   // the dedup kernel also runs the deferred eviction
+    // a captured graph replays after its own update: keep the eviction blocks
+    // (they test the device flag and return when nothing is listed)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    const bool ev = h->ev_pending || cap == cudaStreamCaptureStatusActive;
     Prof p(h, "dedup", st);
-    h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st);
+    h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st, h->evbuf_host, p2p_view(h), ev,
+                                   c.rmode ? 0 : 1);
+    h->ev_pending = false;
   } else {
+    flush_evict(h, st);
     launch_begin(d, clock_t, (int)n, st);
     Prof p(h, "dedup", st);
     h->launches += 1 + launch_dedup(c, (int)n, d.R, h->pbits, d.ctl, st);
@@ -666,7 +697,7 @@ static het_status_t evict_overflow(het_cache* h, cudaStream_t st) {
 __global__ void k_check_keys(const int64_t* __restrict__ keys, int n, Call c, Ctl* ctl) {
   int bad = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    bad |= keys[i] != c.uniq[c.inverse[i]];
+    bad |= keys[i] != (c.rmode ? (int64_t)(c.sortbuf0[c.inverse[i]] >> c.pbits) : c.uniq[c.inverse[i]]);
   if (__syncthreads_or(bad) && threadIdx.x == 0) raise_err(ctl, 3 /*HET_ERR_PROTOCOL*/);
 }
 
@@ -688,9 +719,12 @@ static het_status_t update_impl(het_cache* h, const int64_t* keys, uint32_t n, c
   }
   if (h->fused) {
     Prof p(h, "update_fused", st);
-    h->launches += launch_update_fused(d, h->call, grads, lr, h->evbuf_host, st,
-                                       d.world > 1 ? (const void*)p2p_view_ptr(p2p_of(h)) : nullptr);
+    h->launches += launch_update_fused(d, h->call, grads, lr, h->evbuf_host, st, p2p_view(h));
     h->overflow_bound = 0;
+    h->ev_pending = true;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    if (cap == cudaStreamCaptureStatusActive) h->ev_captured = true;
   } else {
     {
       Prof p(h, "segreduce_apply", st);
@@ -732,6 +766,7 @@ static het_status_t evict_keys_pre(het_cache* h, const int64_t* keys, uint32_t n
   Call& c = h->call;
   c.n = (int)n;
   c.keys = keys;
+  c.rmode = 0;
   cudaMemsetAsync(&h->d.ctl->abort, 0, 4, st);
   h->launches += launch_dedup(c, (int)n, h->d.R, h->pbits, h->d.ctl, st);
   return HET_OK;
@@ -739,6 +774,7 @@ static het_status_t evict_keys_pre(het_cache* h, const int64_t* keys, uint32_t n
 
 // keys == nullptr: overflow Evict() (no cross-worker wait); else Cache.Evict(key)
 static het_status_t evict_members(Members g, const int64_t* const* keys, const uint32_t* n, cudaStream_t st) {
+  for (int i = 0; i < g.n; ++i) flush_evict(g.hs[i], st);
   if (!keys) {
     for (int i = 0; i < g.n; ++i) {
       het_status_t rc = evict_overflow(g.hs[i], st);
@@ -843,6 +879,7 @@ static het_status_t flush_range(Members g, int64_t k0, int64_t k1, cudaStream_t 
 }
 
 static het_status_t sync_members(Members g, cudaStream_t st) {
+  for (int i = 0; i < g.n; ++i) flush_evict(g.hs[i], st);
   het_cache* h0 = g.hs[0];
   if (h0->d.world == 1) {
     k_flush_local<<<148 * 4, 256, 0, st>>>(h0->d);
@@ -891,6 +928,7 @@ het_status_t het_group_sync(const het_cache_t* hs, uint32_t N, het_stream_t stre
 
 het_status_t het_check(het_cache_t h) {
   if (!h) return HET_ERR_ARG;
+  flush_evict(h, 0, false);
   return sticky(h, 0);
 }
 
@@ -898,6 +936,8 @@ het_status_t het_stats(het_cache_t h, het_stats_t* out) {
   if (!h || !out) return HET_ERR_ARG;
   unsigned long long cnt[C_NUM];
   Ctl ctl;
+  CUDA_TRY(h, cudaDeviceSynchronize());
+  flush_evict(h, 0, false);
   CUDA_TRY(h, cudaDeviceSynchronize());
   CUDA_TRY(h, cudaMemcpy(cnt, h->d.cnt, sizeof(cnt), cudaMemcpyDeviceToHost));
   CUDA_TRY(h, cudaMemcpy(&ctl, h->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
@@ -930,6 +970,7 @@ het_status_t het_read_global(het_cache_t h, const int64_t* keys, uint32_t n, flo
   if (!h) return HET_ERR_ARG;
   if (n == 0) return HET_OK;
   if (!keys) return HET_ERR_ARG;
+  flush_evict(h, st, false);
   std::vector<int64_t> hk(n);
   if (is_device_ptr(keys)) {
     CUDA_TRY(h, cudaMemcpyAsync(hk.data(), keys, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
@@ -1002,17 +1043,20 @@ het_status_t het_debug_lookup_log(het_cache_t h, int64_t* uniq, int32_t* inverse
   cudaStream_t st = (cudaStream_t)stream_;
   if (!h || !U) return HET_ERR_ARG;
   Ctl ctl;
+  Call& c = h->call;
+  if (c.rmode) launch_compact_log(h->d, c, st);   // the rmode lookup keeps no compact log: build it now
   CUDA_TRY(h, cudaMemcpyAsync(&ctl, h->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  int32_t ur = 0;
+  if (c.rmode) CUDA_TRY(h, cudaMemcpyAsync(&ur, c.dbg_U, 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaStreamSynchronize(st));
-  uint32_t u = (uint32_t)ctl.U;
+  uint32_t u = c.rmode ? (uint32_t)ur : (uint32_t)ctl.U;
   *U = u;
   size_t n = (size_t)h->call.n;
-  Call& c = h->call;
   if (uniq) CUDA_TRY(h, cudaMemcpyAsync(uniq, c.uniq, u * 8, cudaMemcpyDefault, st));
-  if (inverse) CUDA_TRY(h, cudaMemcpyAsync(inverse, c.inverse, n * 4, cudaMemcpyDefault, st));
+  if (inverse) CUDA_TRY(h, cudaMemcpyAsync(inverse, c.rmode ? c.dbg_inverse : c.inverse, n * 4, cudaMemcpyDefault, st));
   if (perm) CUDA_TRY(h, cudaMemcpyAsync(perm, c.perm, n * 4, cudaMemcpyDefault, st));
   if (seg_off) CUDA_TRY(h, cudaMemcpyAsync(seg_off, c.seg_off, (u + 1) * 4, cudaMemcpyDefault, st));
-  if (status) CUDA_TRY(h, cudaMemcpyAsync(status, c.status, u, cudaMemcpyDefault, st));
+  if (status) CUDA_TRY(h, cudaMemcpyAsync(status, c.rmode ? c.dbg_status : c.status, u, cudaMemcpyDefault, st));
   CUDA_TRY(h, cudaStreamSynchronize(st));
   return HET_OK;
 }
@@ -1021,6 +1065,7 @@ het_status_t het_debug_victims(het_cache_t h, int64_t* keys, uint8_t* dirty, uin
                                het_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!h || !e) return HET_ERR_ARG;
+  flush_evict(h, st, false);
   Ctl ctl;
   CUDA_TRY(h, cudaMemcpyAsync(&ctl, h->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaStreamSynchronize(st));
@@ -1048,6 +1093,7 @@ het_status_t het_debug_dump_cache(het_cache_t h, int64_t* keys, float* v, float*
                                   het_stream_t stream_) {
   cudaStream_t st = (cudaStream_t)stream_;
   if (!h || !m) return HET_ERR_ARG;
+  flush_evict(h, st, false);
   Dev& d = h->d;
   std::vector<int64_t> ek(d.Ecap);
   CUDA_TRY(h, cudaMemcpyAsync(ek.data(), d.ekey, d.Ecap * 8, cudaMemcpyDeviceToHost, st));

@@ -8,8 +8,9 @@
 //     ekey i64[Ecap] (-1 = free)  v,p float[Ecap][D]  cs,cc u32[Ecap]
 //     eprim u32[Ecap]  (LFU count or LRU tick: the policy's primary order key)
 //     fstack i32[Ecap] + ctl.ftop       free-entry stack
-//   open-addressing hash (Cache.Find): hkey i64[S], hval i32[S],
-//     S = pow2 >= 4*Ecap, 32-slot aligned windows probed by one warp
+//   open-addressing hash (Cache.Find): hslot u64[S] = key << 32 | entry
+//     (keys < 2^32, R15), S = pow2 >= 4*Ecap, 32-slot aligned windows probed
+//     by one warp: one 256 B load returns the entry with the match
 //   count_by_key u32[R]                 persistent LFU counts (R7)
 #pragma once
 #include <cstdint>
@@ -18,8 +19,16 @@
 namespace het {
 
 constexpr uint32_t S_INF = 0xFFFFFFFFu;
-constexpr int64_t HK_EMPTY = -1;
-constexpr int64_t HK_TOMB = -2;
+// hash slot word: key << 32 | entry (entry >= 0); EMPTY ends a probe, TOMB does not
+constexpr uint64_t HS_EMPTY = ~0ull;                  // entry field -1
+constexpr uint64_t HS_TOMB = 0xFFFFFFFFFFFFFFFEull;   // entry field -2
+__host__ __device__ __forceinline__ uint64_t hs_pack(int64_t key, int32_t e) {
+  return ((uint64_t)key << 32) | (uint32_t)e;
+}
+__device__ __forceinline__ bool hs_is(uint64_t w, int64_t key) {   // a live slot of `key`
+  return (w >> 32) == (uint64_t)key && (int32_t)(uint32_t)w >= 0;
+}
+__device__ __forceinline__ int32_t hs_val(uint64_t w) { return (int32_t)(uint32_t)w; }
 constexpr uint32_t EP_FREE = 0xFFFFFFFFu;  // eprim of a free entry
 constexpr uint32_t EP_PIN = 0xFFFFFFFEu;   // eprim of a light-LFU pinned entry (R27): never a victim
 constexpr int LFU_CB_MAX = 16;             // LFU count values kept in key bitmaps
@@ -85,6 +94,15 @@ struct Ctl {
   int32_t npin_cand;
   int32_t pad7_;
   int64_t npinned;
+  // deferred overflow eviction (fused path, LFU bitmap plan): the update lists
+  // the victims of Evict(), the first kernel of the next call
+  // evicts them before anything reads or changes the cache
+  int32_t ev_pending;   // vsel[0, ev_nsel) still to evict
+  int32_t ev_nsel;
+  int32_t ev_ftop0;     // free-stack top when they were listed: victim i frees into fstack[ev_ftop0 + i]
+  int32_t ext_blocks;   // extraction blocks finished (last-block counter)
+  uint32_t plan_flag;   // lk_seq of the published plan (update: block 0 -> the other blocks)
+  int32_t ev_done;      // eviction blocks finished (last-block counter)
 };
 
 struct Dev {
@@ -98,7 +116,7 @@ struct Dev {
   uint32_t* eprim; int32_t* fstack;
   uint32_t* estep;   // lookup sequence number that last touched the entry
   // hash
-  int64_t* hkey; int32_t* hval; int hbits; uint64_t hmask;
+  uint64_t* hslot; int hbits; uint64_t hmask;
   uint32_t* count_by_key;
   Ctl* ctl; unsigned long long* cnt;
   // LFU count bitmaps (P:632 LFU): bit (c, key) set iff
@@ -125,8 +143,18 @@ __device__ __forceinline__ void pin_candidate(const Dev& s, int64_t key, int32_t
 }
 
 // Per-call scratch (sized by n_max at create)
+//
+// Indexing of the per-key arrays (status, uentry, urec, upos, inverse):
+//   rmode 0: by unique index u in [0, U) (compact dedup: uniq, seg_off)
+//   rmode 1: by sorted position r in [0, n) of the key's first occurrence
+//            (N = 1 fused path): the dedup leaves the sorted composites in
+//            sortbuf0 and perm, with no compaction pass; a key's segment is
+//            [r, next key change); non-head positions carry urec[r].x = -1.
+//            het_debug_lookup_log compacts on demand (k_compact_log).
 struct Call {
   int n;                       // occurrences in this call
+  int rmode;                   // 1: per-key arrays indexed by sorted position (see above)
+  int pbits;                   // position bits of the sort composites (key << pbits | pos)
   uint64_t t;                  // caller clock (LRU tick)
   const int64_t* keys;         // [n] device
   int64_t* uniq;               // [n_max]
@@ -139,6 +167,11 @@ struct Call {
   uint64_t* sortbuf1;
   int32_t* blockbuf;           // block counts for scans
   int32_t* hlist;              // [n_max] heavy keys of the current update (segment reduce)
+  int4* urec;                  // [n_max] per unique key, lookup -> update: {entry, j0, cnt | dirty << 31, c_c}
+  int4* upos;                  // [n_max] its first four batch positions (ascending)
+  uint8_t* dbg_status;         // [n_max] rmode: compacted status (debug export)
+  int32_t* dbg_inverse;        // [n_max] rmode: compacted inverse (debug export)
+  int32_t* dbg_U;              // rmode: unique keys of the compacted log
   float* hbuf;                 // [ceil(D/16)][n_max][16] heavy keys' gradient rows, key-contiguous, slice-major
   int hcap;                    // n_max (rows per hbuf slice plane)
 };
@@ -173,14 +206,10 @@ __device__ __forceinline__ int32_t warp_find(const Dev& s, int64_t key, int lane
   uint64_t w = hash_home(s, key);
   for (int it = 0; it < (1 << 20); ++it) {
     uint64_t slot = (w + lane) & s.hmask;
-    int64_t hk = s.hkey[slot];
-    unsigned m = __ballot_sync(0xffffffffu, hk == key);
-    if (m) {
-      int src = __ffs(m) - 1;
-      int32_t val = s.hval[slot];
-      return __shfl_sync(0xffffffffu, val, src);
-    }
-    if (__ballot_sync(0xffffffffu, hk == HK_EMPTY)) return -1;
+    const uint64_t hw = s.hslot[slot];
+    unsigned m = __ballot_sync(0xffffffffu, hs_is(hw, key));
+    if (m) return __shfl_sync(0xffffffffu, hs_val(hw), __ffs(m) - 1);
+    if (__ballot_sync(0xffffffffu, hw == HS_EMPTY)) return -1;
     w = (w + 32) & s.hmask;
   }
   return -1;
@@ -191,15 +220,14 @@ __device__ __forceinline__ int32_t warp_find_slot(const Dev& s, int64_t key, int
   uint64_t w = hash_home(s, key);
   for (int it = 0; it < (1 << 20); ++it) {
     uint64_t slot = (w + lane) & s.hmask;
-    int64_t hk = s.hkey[slot];
-    unsigned m = __ballot_sync(0xffffffffu, hk == key);
+    const uint64_t hw = s.hslot[slot];
+    unsigned m = __ballot_sync(0xffffffffu, hs_is(hw, key));
     if (m) {
       int src = __ffs(m) - 1;
-      int32_t val = s.hval[slot];
       *slot_out = __shfl_sync(0xffffffffu, slot, src);
-      return __shfl_sync(0xffffffffu, val, src);
+      return __shfl_sync(0xffffffffu, hs_val(hw), src);
     }
-    if (__ballot_sync(0xffffffffu, hk == HK_EMPTY)) return -1;
+    if (__ballot_sync(0xffffffffu, hw == HS_EMPTY)) return -1;
     w = (w + 32) & s.hmask;
   }
   return -1;
@@ -210,19 +238,20 @@ __device__ __forceinline__ int32_t warp_find_slot(const Dev& s, int64_t key, int
 __device__ __forceinline__ int32_t thread_find_slot(const Dev& s, int64_t key, uint64_t* slot_out) {
   uint64_t w = hash_home(s, key);
   for (int it = 0; it < (1 << 20); ++it) {
-    const longlong2* win = reinterpret_cast<const longlong2*>(s.hkey + w);
+    const ulonglong2* win = reinterpret_cast<const ulonglong2*>(s.hslot + w);
     bool empty = false;
     int hit = -1;
+    int32_t val = -1;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-      const longlong2 v = win[q];
-      if (v.x == key) hit = 2 * q;
-      if (v.y == key) hit = 2 * q + 1;
-      empty |= (v.x == HK_EMPTY) | (v.y == HK_EMPTY);
+      const ulonglong2 v = win[q];
+      if (hs_is(v.x, key)) { hit = 2 * q; val = hs_val(v.x); }
+      if (hs_is(v.y, key)) { hit = 2 * q + 1; val = hs_val(v.y); }
+      empty |= (v.x == HS_EMPTY) | (v.y == HS_EMPTY);
     }
     if (hit >= 0) {
       *slot_out = w + hit;
-      return s.hval[w + hit];
+      return val;
     }
     if (empty) return -1;
     w = (w + 32) & s.hmask;
@@ -236,21 +265,20 @@ __device__ __forceinline__ void warp_insert(const Dev& s, int64_t key, int32_t e
   uint64_t w = hash_home(s, key);
   for (;;) {
     uint64_t slot = (w + lane) & s.hmask;
-    int64_t hk = s.hkey[slot];
+    const uint64_t hw = s.hslot[slot];
     // prefer tombstones, so EMPTY slots (which end probes) are used up slowly
-    unsigned mt = __ballot_sync(0xffffffffu, hk == HK_TOMB);
-    unsigned me = __ballot_sync(0xffffffffu, hk == HK_EMPTY);
+    unsigned mt = __ballot_sync(0xffffffffu, hw == HS_TOMB);
+    unsigned me = __ballot_sync(0xffffffffu, hw == HS_EMPTY);
     for (int pass = 0; pass < 2; ++pass) {
       unsigned m = pass == 0 ? mt : me;
       while (m) {
         int src = __ffs(m) - 1;
         int ok = 0;
-        if (lane == src) {
-          unsigned long long old = atomicCAS((unsigned long long*)&s.hkey[slot],
-                                             (unsigned long long)hk, (unsigned long long)key);
-          if (old == (unsigned long long)hk) {
-            s.hval[slot] = entry;
-            if (hk == HK_TOMB) atomicSub(&s.ctl->n_tomb, 1);
+        if (lane == src) {   // key and entry in one CAS
+          unsigned long long old = atomicCAS((unsigned long long*)&s.hslot[slot], (unsigned long long)hw,
+                                             (unsigned long long)hs_pack(key, entry));
+          if (old == (unsigned long long)hw) {
+            if (hw == HS_TOMB) atomicSub(&s.ctl->n_tomb, 1);
             ok = 1;
           }
         }
@@ -268,16 +296,16 @@ __device__ __forceinline__ void warp_erase(const Dev& s, int64_t key, int lane) 
   uint64_t w = hash_home(s, key);
   for (;;) {
     uint64_t slot = (w + lane) & s.hmask;
-    int64_t hk = s.hkey[slot];
-    unsigned m = __ballot_sync(0xffffffffu, hk == key);
+    const uint64_t hw = s.hslot[slot];
+    unsigned m = __ballot_sync(0xffffffffu, hs_is(hw, key));
     if (m) {
       if (lane == __ffs(m) - 1) {
-        s.hkey[slot] = HK_TOMB;
+        s.hslot[slot] = HS_TOMB;
         atomicAdd(&s.ctl->n_tomb, 1);
       }
       return;
     }
-    if (__ballot_sync(0xffffffffu, hk == HK_EMPTY)) return;  // not found (should not happen)
+    if (__ballot_sync(0xffffffffu, hw == HS_EMPTY)) return;  // not found (should not happen)
     w = (w + 32) & s.hmask;
   }
 }
@@ -308,6 +336,20 @@ __device__ __forceinline__ void dpop_init(int* dpop) {
 }
 __device__ __forceinline__ void dpop_flush(const Dev& s, int* dpop) {
   if (s.lfu_cb && threadIdx.x < s.lfu_cb && dpop[threadIdx.x]) atomicAdd(&s.pop[threadIdx.x], dpop[threadIdx.x]);
+}
+
+// lookup -> update record of unique key u (warp-uniform call): the entry, its
+// segment, c_c and dirty flag after the lookup (nothing changes them before
+// the update) and the first four positions, so the update's segment reduce
+// starts from two 16 B loads instead of a chain of dependent ones
+__device__ __forceinline__ void write_urec(const Call& c, int u, int32_t e, int j0, int cnt, bool dirty,
+                                           uint32_t cc, int pos_lane, int lane) {
+  const int p0 = __shfl_sync(0xffffffffu, pos_lane, 0), p1 = __shfl_sync(0xffffffffu, pos_lane, 1);
+  const int p2 = __shfl_sync(0xffffffffu, pos_lane, 2), p3 = __shfl_sync(0xffffffffu, pos_lane, 3);
+  if (lane == 0 && e >= 0) {
+    c.urec[u] = make_int4(e, j0, (int)((uint32_t)cnt | (dirty ? 0x80000000u : 0u)), (int)cc);
+    c.upos[u] = make_int4(p0, p1, p2, p3);
+  }
 }
 
 // ---------------------------------------------------------------- TMA bulk copy + mbarrier
@@ -368,7 +410,16 @@ void launch_hash_rebuild(const Dev& s, cudaStream_t st);
 bool fused_ok(const Dev& s, int n);
 int launch_pin_apply(const Dev& s, cudaStream_t st);
 constexpr int FUSED_LOOKUP_MAX = 16384;   // N = 1: fused lookup/update up to this n
-int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st);
+// evict: the previous fused update left listed victims (Ctl::ev_pending) --
+// they are evicted by extra blocks of the same kernel; evbuf: EvBuf;
+// p2pview: the exchange view at N > 1 (PUSH records), else nullptr
+// compact: 1 writes unique/seg_off/U (rmode 0), 0 leaves the sorted
+// composites for the rmode lookup (no serial tail)
+int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st,
+                    void* evbuf, const void* p2pview, bool evict, int compact);
+// rmode: the compact lookup log (uniq, seg_off, dbg_status, dbg_inverse, dbg_U) for the debug export
+void launch_compact_log(const Dev& s, const Call& c, cudaStream_t st);
+int launch_evict_pending(const Dev& s, void* evbuf, const void* p2pview, cudaStream_t st);
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st);
 // SMs left free by the cooperative kernels for NCCL's blocks at N > 1
 // (= NCCL's maxCTAs and the peer-memory dense all-reduce grid; env HET_NCCL_CTAS, default 16)

@@ -394,7 +394,7 @@ __global__ void k_build_pushes(Dev s, Call c, MgpuState m_, const int64_t* vsel,
       for (int d = lane; d < D4; d += 32) dst[d] = pr[d];
     }
     if (mode != 2 && lane == 0) {
-      s.hkey[slot] = HK_TOMB;
+      s.hslot[slot] = HS_TOMB;
       atomicAdd(&ctl->n_tomb, 1);
       if (mode == 0) { vkeys[i] = key; vdirty[i] = dirty ? 1 : 0; }
       if (s.policy == 0) lfu_move(s, key, prim, EP_FREE, dpop);

@@ -428,7 +428,7 @@ __global__ void k_p2p_pushes(Dev s, P2P m, EvView b) {
                     reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D), D4, lane);
     }
     if (lane == 0) {
-      s.hkey[slot] = HK_TOMB;
+      s.hslot[slot] = HS_TOMB;
       atomicAdd(&ctl->n_tomb, 1);
       b.vkeys[i] = key;
       b.vdirty[i] = dirty ? 1 : 0;
@@ -495,6 +495,7 @@ __device__ __forceinline__ void probe_build_key(const Dev& s, const Call& c, con
   }
   st = __shfl_sync(0xffffffffu, st, 0);
   for (int k = lane; k < cnt; k += 32) c.inverse[k < 32 ? pos_lane : c.perm[j0 + k]] = u;
+  write_urec(c, u, e, j0, cnt, ecc > ecs, ecc, pos_lane, lane);   // resident: a hit keeps it, a refetch rewrites it
   if (st != ST_HIT) {
     const int o = (int)(key % m.N);
     const bool dirty = e >= 0 && ecc > ecs;
@@ -624,6 +625,7 @@ __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, 
         warp_copy_row(reinterpret_cast<float4*>(s.v + (int64_t)e * s.D), reinterpret_cast<const float4*>(rec + 4),
                       D4, lane);
         if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
+        write_urec(c, u, e, j0, cnt, false, g, pos_lane, lane);   // fetched: clean, c_c = c_g
       }
     }
   }
@@ -936,7 +938,7 @@ __global__ void k_p2p_evict_keys(Dev s, Call c, P2P m) {
       if (dirty) push_record(s, m, e, key, ecc, lane);
       if (lane == 0) {
         if (dirty) atomicAdd(&sb[2], 16ull + 4ull * s.D);
-        s.hkey[slot] = HK_TOMB;
+        s.hslot[slot] = HS_TOMB;
         atomicAdd(&ctl->n_tomb, 1);
         if (s.policy == 0) lfu_move(s, key, prim, EP_FREE, dpop);
         unpin_count(s, prim);

@@ -42,7 +42,7 @@ __global__ void k_reset_cache(Dev s) {
     s.eprim[i] = EP_FREE;
     s.fstack[i] = (int32_t)(s.Ecap - 1 - i);
   }
-  for (int64_t i = i0; i <= (int64_t)s.hmask; i += stride) s.hkey[i] = HK_EMPTY;
+  for (int64_t i = i0; i <= (int64_t)s.hmask; i += stride) s.hslot[i] = HS_EMPTY;
   if (i0 == 0) {
     s.ctl->ftop = (int32_t)s.Ecap;
     s.ctl->n_tomb = 0;
@@ -61,6 +61,7 @@ __global__ void k_begin(Dev s, uint64_t t, int n) {
   ctl->abort = 0;
   if (t == CLOCK_AUTO) { t = ctl->t_auto; ctl->t_auto = t + 1; }
   ctl->t_cur = t;
+  ctl->lk_seq = ctl->lk_seq + 1;
   s.cnt[C_LOOKUPS] += 1;
   s.cnt[C_KEYS] += (unsigned long long)n;
 }
@@ -278,7 +279,7 @@ __global__ void k_rebuild_clear(Dev s) {
   if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->rebuild = go ? 1 : 0;
   if (!go) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x)
-    s.hkey[i] = HK_EMPTY;
+    s.hslot[i] = HS_EMPTY;
 }
 __global__ void k_rebuild_insert(Dev s) {
   if (!s.ctl->rebuild) return;

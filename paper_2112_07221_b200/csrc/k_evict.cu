@@ -225,7 +225,7 @@ k_ev_apply_local(Dev s, EvBuf b) {
       }
       if (lane == 0) {
         if (dirty) { uint32_t g = s.cg[key]; s.cg[key] = g > ecc ? g : ecc; }
-        s.hkey[slot] = HK_TOMB;
+        s.hslot[slot] = HS_TOMB;
         atomicAdd(&ctl->n_tomb, 1);
         b.vkeys[i] = key;
         b.vdirty[i] = dirty ? 1 : 0;

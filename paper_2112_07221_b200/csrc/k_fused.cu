@@ -103,9 +103,56 @@ __device__ __forceinline__ int block_scan_int(int x, int* warp_sums, int* tot) {
 }
 
 // ------------------------------------------------------------------ K_dd
+__device__ __forceinline__ void evict_listed(const Dev& s, const EvBuf& b, const P2P* pp, int eb, int neb);
+
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// While the dedup ranks the keys, pull into L2 the lines the next kernels
+// will wait on: per key of this block's 32 positions the hash window (two
+// 128 B lines), the LFU count, c_g and the server row (a miss fetches it,
+// P:439); block 0 also the LFU plan's counters and bitmap words around the
+// previous step's threshold (the update's plan).  Hints only: no
+// result depends on them.
+__device__ __forceinline__ void prefetch_lookup_lines(const Dev& s, const uint64_t* comp, int n, int pbits) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p = blockIdx.x * 32 + lane;
+  if (p < n && wid < 8) {
+    const int64_t key = (int64_t)(comp[p] >> pbits);
+    const bool own = key % s.world == s.rank;
+    const int64_t row = key / s.world;
+    if (wid < 2) prefetch_l2(s.hslot + hash_home(s, key) + 16 * wid);
+    else if (wid == 2) { if (s.lfu_persist) prefetch_l2(s.count_by_key + key); }
+    else if (wid == 3) { if (own) prefetch_l2(s.cg + row); }
+    else if ((wid - 4) * 32 < (int)s.D && own) prefetch_l2(s.W + row * s.D + (wid - 4) * 32);
+  }
+  if (blockIdx.x == 0 && wid >= 8 && s.lfu_cb) {
+    const Ctl* ctl = s.ctl;
+    const uint32_t T = ctl->T;
+    const int64_t ks = ctl->Kstar;
+    if (T >= (uint32_t)s.lfu_cb || ks < 0 || ks >= s.R) return;
+    const int64_t kblk = ks >> LFU_BLK_SHIFT;
+    const int t = (wid - 8) * 32 + lane, nt = (DDF_WARPS - 8) * 32;
+    if (t == 0) prefetch_l2(s.pop);
+    for (int64_t i = (int64_t)t * 32; i < s.nbk2; i += (int64_t)nt * 32) prefetch_l2(s.bcnt2 + (int64_t)T * s.nbk2 + i);
+    for (int64_t i = (int64_t)t * 32; i <= kblk + 64 && i < s.nbk; i += (int64_t)nt * 32)
+      prefetch_l2(s.bcnt + (int64_t)T * s.nbk + i);
+    const int64_t w0 = kblk << (LFU_BLK_SHIFT - 5);
+    for (int64_t i = (int64_t)t * 32; i < 256; i += (int64_t)nt * 32)
+      if (w0 + i < s.bm_words) prefetch_l2(s.bm + (int64_t)T * s.bm_words + w0 + i);
+  }
+}
+
+// blocks [0, ndd): the dedup; blocks [ndd, gridDim.x): the overflow eviction
+// the previous update listed (deferred, see k_update_fused) -- independent
+// work, side by side
 __global__ void __launch_bounds__(DDF_THREADS)
-k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, uint64_t t, int lookup) {
+k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, uint64_t t, int lookup, EvBuf eb,
+           P2P pm, int push, int ndd, int compact) {
   pdl_trigger();
+  if ((int)blockIdx.x >= ndd) {
+    evict_listed(s, eb, push ? &pm : nullptr, blockIdx.x - ndd, gridDim.x - ndd);
+    return;
+  }
   extern __shared__ uint64_t comp[];
   __shared__ int part[DDF_WARPS][32];
   __shared__ int warp_sums[32];
@@ -130,6 +177,7 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
     }
   }
   bad = __syncthreads_or(bad);
+  if (!bad && lookup) prefetch_lookup_lines(s, comp, n, pbits);
   if (blockIdx.x == 0 && threadIdx.x == 0) {   // per-call begin, overlapped with the rank work
     if (lookup) {
       if (t == CLOCK_AUTO) { t = ctl->t_auto; ctl->t_auto = t + 1; }
@@ -139,6 +187,7 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
       s.cnt[C_KEYS] += (unsigned long long)n;
     }
     ctl->abort = 0;
+    if (!compact) ctl->U = n;   // rmode: every sorted position is a work item of the lookup
     if (bad) { raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/); ctl->U = 0; c.seg_off[0] = 0; }
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -161,9 +210,10 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
     }
   }
   TL_MAX(2);
+  if (!compact) return;   // rmode: the sorted composites and perm are the dedup (the lookup reads key runs)
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&ctl->dd_done, 1) == (int)gridDim.x - 1;
+  if (threadIdx.x == 0) s_last = atomicAdd(&ctl->dd_done, 1) == ndd - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
@@ -221,6 +271,39 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
 }
 
 // ------------------------------------------------------------------ K_look
+// rmode: the key run starting at sorted position r (warp-uniform): false if r
+// is not the first position of its key.  Lane l loads composite r - 1 + l and
+// the batch position of sorted r + l (both coalesced, in one round trip); a
+// run longer than 31 is followed chunk by chunk.
+__device__ __forceinline__ bool key_run(const Call& c, int r, int lane, int64_t* key, int* cnt, int* pos_lane) {
+  const int n = c.n, pb = c.pbits;
+  const int q = r - 1 + lane;
+  const uint64_t w = (q >= 0 && q < n) ? __ldcg(&c.sortbuf0[q]) : ~0ull;
+  const int pl = r + lane < n ? __ldcg(&c.perm[r + lane]) : 0;
+  const uint64_t kl = w >> pb;
+  const uint64_t k = __shfl_sync(0xffffffffu, kl, 1);
+  const uint64_t kp = __shfl_sync(0xffffffffu, kl, 0);
+  if (r > 0 && kp == k) return false;
+  unsigned same = __ballot_sync(0xffffffffu, lane >= 1 && q < n && kl == k) >> 1;   // bit j: sorted r + j
+  int len = __ffs(~same) - 1;                                                       // 1..31
+  if (same == 0x7FFFFFFFu) {
+    len = 31;
+    for (int b = r + 31;; b += 32) {
+      const int qq = b + lane;
+      const bool eq = qq < n && (__ldcg(&c.sortbuf0[qq]) >> pb) == k;
+      const unsigned m = __ballot_sync(0xffffffffu, eq);
+      const int run = __ffs(~m) - 1;   // -1 when all 32 equal
+      if (run < 0) { len += 32; continue; }
+      len += run;
+      break;
+    }
+  }
+  *key = (int64_t)k;
+  *cnt = len;
+  *pos_lane = lane < len ? pl : 0;
+  return true;
+}
+
 // LFU threshold (T, K*) for this step, one CTA (the last block of k_lookup_fused):
 // T = the smallest count whose cumulative population reaches `need`, K* = the
 // needT-th smallest key of count T.  Loads are issued in parallel: the 16
@@ -347,10 +430,10 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
   __syncthreads();
   Ctl* ctl = s.ctl;
   const int lane = threadIdx.x & 31;
-  const int u = blockIdx.x * LK_WARPS + (threadIdx.x >> 5);
-  const int U = ctl->U;
+  const int u = blockIdx.x * LK_WARPS + (threadIdx.x >> 5);   // rmode: sorted position r
+  const int U = c.rmode ? c.n : ctl->U;
   const int D4 = s.D >> 2;
-  const bool live = !ctl->abort && u < U;
+  bool live = !ctl->abort && u < U;
   // ---- phase A (warp per unique key): Find, CheckValid, touch; with agg (large
   // n: thousands of misses) a miss takes a slot of the block's free-entry
   // reservation -- one atomic per block between the phases instead of one per miss
@@ -359,14 +442,31 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
   int32_t e = -1;
   uint8_t st = ST_HIT;
   uint32_t ecs = 0, ecc = 0, cntk = 0, gpre = 0, mprim = 0;
-  if (live) {
+  if (live && c.rmode) {
+    // one window: lane l holds sorted composite r - 1 + l and the position of
+    // sorted r + l -- the head test, the key, its run length and positions
+    live = key_run(c, u, lane, &key, &cnt, &pos_lane);
+    j0 = u;
+    if (!live && lane == 0) c.urec[u].x = -1;   // not a key's first sorted position: no work for the update
+  } else if (live) {
     key = c.uniq[u];
     j0 = c.seg_off[u];
     cnt = c.seg_off[u + 1] - j0;
     pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
+  }
+  // rows of at most 128 floats live in registers, one float4 per lane: the
+  // server row (a miss or refetch installs it) is loaded with the probe and
+  // the cached row (a hit returns it) as soon as the probe ends, so neither
+  // waits for the decisions
+  const bool reg = D4 <= 32;
+  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 wrow = zero4, vrow = zero4;
+  if (live) {
     if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
-    if (lane == 1 && s.s != S_INF) gpre = s.cg[key];
+    if (lane == 1) gpre = s.cg[key];
+    if (reg && lane < D4) wrow = __ldcg(reinterpret_cast<const float4*>(s.W + key * s.D) + lane);
     e = warp_find(s, key, lane);
+    if (reg && e >= 0 && lane < D4) vrow = __ldcg(reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D) + lane);
     gpre = __shfl_sync(0xffffffffu, gpre, 1);
     TL_MAX(13);
     st = ST_MISS;
@@ -417,13 +517,18 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
   // ---- phase B: sync push / fetch / install, Get scatter
   if (live) {
     float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
+    uint32_t ucc = ecc;              // the entry's c_c and dirty flag as the update will find them
+    bool udirty = ecc > ecs;
     if (st != ST_HIT) {
-      uint32_t g = gpre;
-      if (s.s == S_INF || st == ST_MISS) g = s.cg[key];
+      uint32_t g = gpre;   // c_g[key]: only this warp touches the key's server row and clock
       if (st != ST_MISS) {
         if (ecc > ecs) {  // dirty sync push (L4): W += p, c_g = max
           const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
-          for (int d = lane; d < D4; d += 32) Wr[d] = f4add_(Wr[d], pr[d]);
+          if (reg) {
+            if (lane < D4) { wrow = f4add_(wrow, pr[lane]); Wr[lane] = wrow; }
+          } else {
+            for (int d = lane; d < D4; d += 32) Wr[d] = f4add_(Wr[d], pr[d]);
+          }
           g = g > ecc ? g : ecc;
           if (lane == 0) s.cg[key] = g;
         }
@@ -444,13 +549,33 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
       }
       if (e >= 0) {     // L5: v = W, c_s = c_c = c_g
         float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
-        for (int d = lane; d < D4; d += 32) vr[d] = Wr[d];
+        if (reg) {
+          if (lane < D4) vr[lane] = wrow;
+        } else {
+          for (int d = lane; d < D4; d += 32) vr[d] = Wr[d];
+        }
         if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
+        ucc = g;
+        udirty = false;
       }
+      vrow = wrow;
     }
     TL_MAX(14);
     for (int k = lane; k < cnt; k += 32) c.inverse[k < 32 ? pos_lane : c.perm[j0 + k]] = u;
-    if (e >= 0) {
+    write_urec(c, u, e, j0, cnt, udirty, ucc, pos_lane, lane);
+    if (e >= 0 && reg) {
+      if (lane == 0) c.uentry[u] = e;
+      // L7 Get, scattered to the occurrences of the key (128-bit stores)
+      float4* o4 = reinterpret_cast<float4*>(out);
+      for (int kb = 0; kb < cnt; kb += 32) {
+        const int src = kb == 0 ? pos_lane : (kb + lane < cnt ? c.perm[j0 + kb + lane] : 0);
+        const int m = min(32, cnt - kb);
+        for (int k = 0; k < m; ++k) {
+          const int pos = __shfl_sync(0xffffffffu, src, k);
+          if (lane < D4) __stcs(o4 + (int64_t)pos * D4 + lane, vrow);
+        }
+      }
+    } else if (e >= 0) {
       if (lane == 0) c.uentry[u] = e;
       // L7 Get, scattered to the occurrences of the key (128-bit stores)
       const float4* vr = reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D);
@@ -477,7 +602,12 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
     if (bc[1]) atomicAdd(&s.cnt[C_EXP1], (unsigned long long)bc[1]);
     if (bc[2]) atomicAdd(&s.cnt[C_EXP2], (unsigned long long)bc[2]);
     if (bc[3]) atomicAdd(&s.cnt[C_MISSES], (unsigned long long)bc[3]);
-    if (blockIdx.x == 0 && !ctl->abort) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+    if (c.rmode) {
+      const unsigned nu = bc[0] + bc[1] + bc[2] + bc[3];   // heads of this block
+      if (nu) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)nu);
+    } else if (blockIdx.x == 0 && !ctl->abort) {
+      atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+    }
   }
 }
 
@@ -503,12 +633,25 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
   Ctl* ctl = s.ctl;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int grp = wib / G, gw = wib % G;
-  const int u = blockIdx.x * (LK_WARPS / G) + grp;
-  const int U = ctl->U;
+  const int u = blockIdx.x * (LK_WARPS / G) + grp;   // rmode: sorted position r
+  const int U = c.rmode ? c.n : ctl->U;
   const bool live = !ctl->abort && u < U;
+  bool head = true;
+  int64_t key = 0;
+  int j0 = 0, cnt = 0, pl = 0;
   if (live && gw == 0) {
-    const int64_t key = c.uniq[u];
-    const int j0 = c.seg_off[u], cnt = c.seg_off[u + 1] - j0;
+    if (c.rmode) {
+      head = key_run(c, u, lane, &key, &cnt, &pl);
+      j0 = u;
+      if (!head && lane == 0) { c.urec[u].x = -1; meta[grp].e = -1; }
+    } else {
+      key = c.uniq[u];
+      j0 = c.seg_off[u];
+      cnt = c.seg_off[u + 1] - j0;
+      pl = lane < cnt ? c.perm[j0 + lane] : 0;
+    }
+  }
+  if (live && gw == 0 && head) {
     uint32_t cntk = 0, gpre = 0;
     if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
     if (lane == 1 && s.s != S_INF) gpre = s.cg[key];
@@ -572,6 +715,7 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
       if (e >= 0 && lane == 0) { s.cs[e] = g; s.cc[e] = g; }   // L5 clocks (rows below)
     }
     for (int k = lane; k < cnt; k += 32) c.inverse[c.perm[j0 + k]] = u;
+    write_urec(c, u, e, j0, cnt, st == ST_HIT && ecc > ecs, st == ST_HIT ? ecc : g, pl, lane);
     if (lane == 0) {
       if (e >= 0) c.uentry[u] = e;
       meta[grp] = LkMeta{key, e, j0, cnt, g, st, (uint8_t)push};
@@ -612,7 +756,12 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
     if (bc[1]) atomicAdd(&s.cnt[C_EXP1], (unsigned long long)bc[1]);
     if (bc[2]) atomicAdd(&s.cnt[C_EXP2], (unsigned long long)bc[2]);
     if (bc[3]) atomicAdd(&s.cnt[C_MISSES], (unsigned long long)bc[3]);
-    if (blockIdx.x == 0 && !ctl->abort) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+    if (c.rmode) {
+      const unsigned nu = bc[0] + bc[1] + bc[2] + bc[3];   // heads of this block
+      if (nu) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)nu);
+    } else if (blockIdx.x == 0 && !ctl->abort) {
+      atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+    }
   }
 }
 
@@ -646,7 +795,7 @@ __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_
   if (lane == 0) {
     if (push && dirty) atomicAdd(&s.cnt[C_BEMB_TX], 16ull + 4ull * s.D);
     if (dirty && !push) { uint32_t g = s.cg[key]; s.cg[key] = g > ecc ? g : ecc; }
-    s.hkey[slot] = HK_TOMB;
+    s.hslot[slot] = HS_TOMB;
     atomicAdd(s_tomb, 1u);
     b.vkeys[vi] = key;
     b.vdirty[vi] = dirty ? 1 : 0;
@@ -663,18 +812,23 @@ __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_
 __device__ __forceinline__ void segreduce_key(const Dev& s, const Call& c, const float4* __restrict__ G4, float lr,
                                               int u, int lane, float4* mystg, uint64_t* bar, uint32_t& phase,
                                               int stage_rows) {
-  const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
-  const int32_t e = c.uentry[u];
-  const uint32_t ecc = s.cc[e], ecs = s.cs[e];
-  const int cnt = j1 - j0;
-  const int pos_lane = lane < cnt ? __ldg(&c.perm[j0 + lane]) : 0;
-  const bool dirty = ecc > ecs;
+  // the lookup's record: entry, segment, c_c, dirty flag and the first four
+  // positions -- two independent 16 B loads start the key's work
+  const int4 rec = __ldcg(&c.urec[u]);
+  const int4 p4 = __ldcg(&c.upos[u]);
+  const int32_t e = rec.x;
+  if (e < 0) return;   // rmode: not a key's first sorted position
+  const int j0 = rec.y;
+  const int cnt = rec.z & 0x7FFFFFFF;
+  const bool dirty = rec.z < 0;
+  const uint32_t ecc = (uint32_t)rec.w;
   const int D4 = s.D >> 2;
   const float nlr = -lr;
   float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
   float4* pr = reinterpret_cast<float4*>(s.p + (int64_t)e * s.D);
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   if (stage_rows > 0 && cnt > 4) {
+    const int pos_lane = lane < cnt ? __ldg(&c.perm[j0 + lane]) : 0;
     float4* accrow = mystg + (size_t)stage_rows * D4;
     const uint32_t rowbytes = s.D * 4;
     for (int kb = 0; kb < cnt; kb += stage_rows) {
@@ -701,7 +855,32 @@ __device__ __forceinline__ void segreduce_key(const Dev& s, const Call& c, const
       vr[d] = f4add_(vr[d], dl);
       pr[d] = f4add_(dirty ? pr[d] : zero, dl);
     }
+  } else if (cnt <= 4) {
+    // the common case: every occurrence row, v and p in flight at once
+    for (int d = lane; d - lane < D4; d += 32) {
+      const bool act = d < D4;
+      float4 vv = act ? vr[d] : zero;
+      float4 pp = (act && dirty) ? pr[d] : zero;
+      float4 g0 = zero, g1 = zero, g2 = zero, g3 = zero;
+      if (act) {
+        g0 = __ldcs(G4 + (int64_t)p4.x * D4 + d);
+        if (cnt > 1) g1 = __ldcs(G4 + (int64_t)p4.y * D4 + d);
+        if (cnt > 2) g2 = __ldcs(G4 + (int64_t)p4.z * D4 + d);
+        if (cnt > 3) g3 = __ldcs(G4 + (int64_t)p4.w * D4 + d);
+      }
+      float4 acc = f4add_(zero, g0);                 // +0.0f, then ascending position (R11)
+      if (cnt > 1) acc = f4add_(acc, g1);
+      if (cnt > 2) acc = f4add_(acc, g2);
+      if (cnt > 3) acc = f4add_(acc, g3);
+      if (act) {
+        float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
+                                __fmul_rn(nlr, acc.w));
+        vr[d] = f4add_(vv, dl);
+        pr[d] = f4add_(pp, dl);
+      }
+    }
   } else {
+    const int pos_lane = lane < cnt ? __ldg(&c.perm[j0 + lane]) : 0;
     for (int d = lane; d - lane < D4; d += 32) {
       const bool act = d < D4;
       float4 vv = act ? vr[d] : zero;
@@ -744,9 +923,11 @@ __device__ __forceinline__ void segreduce_key(const Dev& s, const Call& c, const
 // first).
 __device__ __forceinline__ void segreduce_slice(const Dev& s, const Call& c, const float4* __restrict__ G4,
                                                 float lr, int u, int sl, int lane) {
-  const int j0 = c.seg_off[u], cnt = c.seg_off[u + 1] - j0;
-  const int32_t e = c.uentry[u];
-  const bool dirty = s.cc[e] > s.cs[e];
+  const int4 rec = __ldcg(&c.urec[u]);
+  const int32_t e = rec.x;
+  if (e < 0) return;   // rmode: not a key's first sorted position
+  const int j0 = rec.y, cnt = rec.z & 0x7FFFFFFF;
+  const bool dirty = rec.z < 0;
   const int D4 = s.D >> 2;
   const int base = sl * 128 + lane;
   const float nlr = -lr;
@@ -789,8 +970,123 @@ __device__ __forceinline__ void segreduce_slice(const Dev& s, const Call& c, con
   }
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// LFU bitmap path: the victim keys of the listed bitmap blocks (count c < T:
+// all set bits; count T: the keys <= K*), one block per warp, appended to vsel
+__device__ __forceinline__ void extract_victims(const Dev& s, const EvBuf& b, int gw, int nw, int lane) {
+  Ctl* ctl = s.ctl;
+  const uint32_t T = __ldcg(&ctl->T);
+  const int64_t Kstar = __ldcg(&ctl->Kstar);
+  const int ntask = __ldcg(&ctl->ntask);
+  for (int task = gw; task < ntask; task += nw) {
+    const int32_t code = __ldcg(&b.cand[task]);
+    const uint32_t cc = (uint32_t)code >> 27;
+    const int64_t blk = code & ((1 << 27) - 1);
+    const uint32_t* bm = s.bm + (int64_t)cc * s.bm_words;
+    uint32_t w[4];
+    int cl = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r;
+      uint32_t bits = wi < s.bm_words ? __ldcg(&bm[wi]) : 0u;
+      if (cc == T) {   // keep keys <= K*
+        const int64_t k0 = wi << 5;
+        if (k0 > Kstar) bits = 0;
+        else if (k0 + 31 > Kstar) bits &= (1u << (Kstar - k0 + 1)) - 1u;
+      }
+      w[r] = bits;
+      cl += __popc(bits);
+    }
+    int incl = cl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (!total) continue;
+    int base = 0;
+    if (lane == 31) base = atomicAdd(&ctl->nsel, total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int pos = base + incl - cl;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      uint32_t bits = w[r];
+      const int64_t kb = ((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r) << 5;
+      while (bits) {
+        b.vsel[pos++] = kb + (__ffs(bits) - 1);
+        bits &= bits - 1;
+      }
+    }
+  }
+}
+
+// The deferred overflow eviction: victim i of the listed vsel[0, ev_nsel) by
+// warp (gw, nw) of the blocks given this work -- find, Evict push (W += p,
+// c_g = max; N > 1: PUSH record to the owner's inbox), delete, free into
+// fstack[ev_ftop0 + i].  Called by the first kernel of the call
+// after the update (no other kernel touches the cache in between).
+__device__ __forceinline__ void evict_listed(const Dev& s, const EvBuf& b, const P2P* pp, int eb, int neb) {
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ unsigned s_dirty, s_ev, s_tomb;
+  __shared__ int s_go, s_last;
+  Ctl* ctl = s.ctl;
+  dpop_init(dpop);
+  if (threadIdx.x == 0) { s_dirty = 0; s_ev = 0; s_tomb = 0; s_go = __ldcg(&ctl->ev_pending); }
+  __syncthreads();
+  if (!s_go) return;   // uniform per block
+  const int lane = threadIdx.x & 31;
+  const int nwb = blockDim.x >> 5;
+  const int gw = eb * nwb + (threadIdx.x >> 5), nw = neb * nwb;
+  const int nsel = __ldcg(&ctl->ev_nsel);
+  const int64_t ftop0 = __ldcg(&ctl->ev_ftop0);
+  for (int i = gw; i < nsel; i += nw) {
+    const int64_t key = __ldcg(&b.vsel[i]);
+    uint64_t slot = 0;
+    const int32_t e = warp_find_slot(s, key, lane, &slot);
+    if (e >= 0) evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev, &s_tomb, i, ftop0 + i, pp);
+    else if (lane == 0) raise_err(ctl, 3 /*HET_ERR_PROTOCOL: a listed victim is not resident*/);
+  }
+  TL_MAX(12);
+  __syncthreads();
+  dpop_flush(s, dpop);
+  if (threadIdx.x == 0) {
+    if (s_ev) atomicAdd(&s.cnt[C_EVICTIONS], (unsigned long long)s_ev);
+    if (s_dirty) atomicAdd(&s.cnt[C_DIRTY_PUSHES], (unsigned long long)s_dirty);
+    if (s_tomb) atomicAdd(&ctl->n_tomb, (int)s_tomb);
+    if (eb == 0) ctl->ftop = (int32_t)(ftop0 + nsel);   // nothing else moves the free stack in this kernel
+    __threadfence();
+    s_last = atomicAdd(&ctl->ev_done, 1) == neb - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) { ctl->ev_done = 0; ctl->ev_pending = 0; }
+}
+
+// the deferred eviction as its own kernel (before calls that do not start with k_dd_fused)
+__global__ void __launch_bounds__(256) k_evict_pending(Dev s, EvBuf b, P2P pm, int push) {
+  evict_listed(s, b, push ? &pm : nullptr, blockIdx.x, gridDim.x);
+}
+
+// Update (Alg. 3): block 0 plans this step's eviction (need, mode, LFU
+// threshold T / K*, the bitmap blocks holding victims, R9) and
+// publishes the plan; blocks 1..xb extract the victim keys once it is out;
+// the other blocks do the ordered segment reduce + SGD + pending + clock.
+// LFU bitmap plans end there: the victims are evicted by the first kernel of
+// the next call (k_dd_fused / k_evict_pending) -- nothing reads or changes
+// the cache in between, so the result is the oracle's.  The generic selection
+// (LRU, LFU beyond the bitmaps, evict-all) and steps that rebuild the hash
+// continue in this kernel after grid syncs.
 __global__ void __launch_bounds__(UPD_THREADS)
-k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, int stage_rows, P2P pm, int push) {
+k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, int stage_rows, P2P pm, int push,
+               int xb) {
   pdl_wait();
   const P2P* pp = push ? &pm : nullptr;
   extern __shared__ float4 dyn[];
@@ -798,6 +1094,7 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   __shared__ uint64_t bars[UPD_WARPS];
   __shared__ int dpop[LFU_CB_MAX];
   __shared__ unsigned s_dirty, s_ev, s_tomb;
+  __shared__ int s_emode, s_rebuild, s_xlast;
   cg::grid_group grid = cg::this_grid();
   Ctl* ctl = s.ctl;
   dpop_init(dpop);
@@ -807,10 +1104,12 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   TL_MIN(16); TL_MAX(17);
   __syncthreads();
   const bool abort = ctl->abort;
-  const int U = abort ? 0 : ctl->U;
-  // ---- block 0: this step's eviction plan (need, mode, LFU threshold T / K*,
-  // hash maintenance), in parallel with the segment reduce of the other blocks
+  const int U = abort ? 0 : (c.rmode ? c.n : ctl->U);   // rmode: sorted positions, heads carry the work
+  const uint32_t seq = ctl->lk_seq;   // set by the lookup; the plan flag carries it
+  const int D4 = s.D >> 2;
+  const int S = (D4 >= 256 && D4 % 128 == 0) ? D4 / 128 : 1;   // wide rows: 512-column slices on separate warps
   if (blockIdx.x == 0) {
+    // ---- the eviction plan
     __shared__ long long warp_sums[32];
     __shared__ int warp_sums_i[32];
     const int64_t res = s.Ecap - (int64_t)ctl->ftop;
@@ -820,8 +1119,9 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
       const bool none = abort || need <= 0;
       ctl->need = none ? 0 : need;
       ctl->emode = none ? 0 : ((s.policy == 0 && s.lfu_cb && need < res) ? 1 : 2);
-      const int64_t S = (int64_t)s.hmask + 1;
-      ctl->rebuild_req = (int64_t)ctl->n_tomb > S / 8;
+      const int64_t HS = (int64_t)s.hmask + 1;
+      ctl->rebuild_req = (int64_t)ctl->n_tomb > HS / 8;
+      ctl->ev_ftop0 = ctl->ftop;   // stable until the victims are freed
     }
     __syncthreads();
     TL_MAX(22);
@@ -862,20 +1162,47 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
     } else if (threadIdx.x == 0) {
       ctl->ntask = 0;
     }
-    if (threadIdx.x == 0) { ctl->ext_next = 0; ctl->ext_done = 0; ctl->find_next = 0; }
+    __syncthreads();
+    if (threadIdx.x == 0) { __threadfence(); st_release_u32(&ctl->plan_flag, seq); }
     TL_MAX(23);
   }
-  __syncthreads();
+  // the plan as every block reads it (block 0 wrote it; the others wait for its flag)
+  auto read_plan = [&]() {
+    if (threadIdx.x == 0) {
+      if (blockIdx.x != 0)
+        while (ld_acquire_u32(&ctl->plan_flag) != seq) __nanosleep(32);
+      s_emode = abort ? 0 : __ldcg(&ctl->emode);
+      s_rebuild = __ldcg(&ctl->rebuild_req);
+    }
+  };
+  const bool xblock = blockIdx.x >= 1 && blockIdx.x <= xb;
+  // blocks 1..xb: wait for the plan first, then extract (LFU bitmap path)
+  if (xblock) {
+    read_plan();
+    __syncthreads();
+    TL_MAX(11);
+    if (s_emode == 1) extract_victims(s, b, (blockIdx.x - 1) * UPD_WARPS + wid, xb * UPD_WARPS, lane);
+    TL_MAX(20);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_xlast = atomicAdd(&ctl->ext_blocks, 1) == xb - 1;
+    __syncthreads();
+    if (s_xlast && threadIdx.x == 0) {   // every victim key is listed
+      ctl->ext_blocks = 0;
+      const int nsel = __ldcg(&ctl->nsel);
+      const bool defer = s_emode == 1 && !s_rebuild && S == 1;
+      ctl->nvict = s_emode == 1 ? nsel : 0;
+      ctl->ev_nsel = nsel;
+      ctl->ev_pending = (defer && nsel > 0) ? 1 : 0;
+    }
+  }
+  // ---- the other blocks: ordered segment reduce + SGD + pending + clock, warp per unique key
   const int gw = blockIdx.x * UPD_WARPS + wid;
   const int nw = gridDim.x * UPD_WARPS;
-  const int D4 = s.D >> 2;
   float4* mystg = dyn + (size_t)wid * (stage_rows + 1) * D4;
   uint32_t phase = 0;
   const float4* G4 = reinterpret_cast<const float4*>(G);
-  // ---- phase 1: ordered segment reduce + SGD + pending + clock, warp per unique key
-  // block 0 plans; the other blocks' warps take the unique keys
-  const int rw = gw - UPD_WARPS, nrw = nw - UPD_WARPS;
-  const int S = (D4 >= 256 && D4 % 128 == 0) ? D4 / 128 : 1;   // wide rows: 512-column slices on separate warps
+  const int rw = gw - (1 + xb) * UPD_WARPS, nrw = nw - (1 + xb) * UPD_WARPS;
   if (rw >= 0) {
     if (S == 1)
       for (int u = rw; u < U; u += nrw) segreduce_key(s, c, G4, lr, u, lane, mystg, &bars[wid], phase, stage_rows);
@@ -883,69 +1210,27 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
       for (int it = rw; it < U * S; it += nrw) segreduce_slice(s, c, G4, lr, it / S, it % S, lane);
   }
   TL_MAX(18);
-  // ---- every update done and block 0's plan + task list visible
+  if (!xblock) read_plan();   // after this block's segment reduce (block 0: its own plan)
+  __syncthreads();
+  const int emode = s_emode;
+  const bool rebuild = s_rebuild;
+  // LFU bitmap plan (or nothing to evict), no hash rebuild, narrow rows: done
+  // -- the victims wait for the next call's first kernel (uniform decision)
+  if (emode != 2 && !rebuild && S == 1) return;
   grid.sync();
   if (S > 1) {                                  // Cache.Clock once per key, after every slice
-    for (int u = gw * 32 + lane; u < U; u += nw * 32) s.cc[c.uentry[u]] += 1;
-    grid.sync();
-  }
-  const int emode = abort ? 0 : __ldcg(&ctl->emode);
-  const bool rebuild = __ldcg(&ctl->rebuild_req);
-  if (emode == 1) {
-    // extraction of the victim keys, one listed bitmap block per warp
-    const uint32_t T = __ldcg(&ctl->T);
-    const int64_t Kstar = __ldcg(&ctl->Kstar);
-    const int ntask = __ldcg(&ctl->ntask);
-    for (int task = gw; task < ntask; task += nw) {
-      const int32_t code = __ldcg(&b.cand[task]);
-      const uint32_t cc = (uint32_t)code >> 27;
-      const int64_t blk = code & ((1 << 27) - 1);
-      const uint32_t* bm = s.bm + (int64_t)cc * s.bm_words;
-      uint32_t w[4];
-      int cl = 0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r;
-        uint32_t bits = wi < s.bm_words ? __ldcg(&bm[wi]) : 0u;
-        if (cc == T) {   // keep keys <= K*
-          const int64_t k0 = wi << 5;
-          if (k0 > Kstar) bits = 0;
-          else if (k0 + 31 > Kstar) bits &= (1u << (Kstar - k0 + 1)) - 1u;
-        }
-        w[r] = bits;
-        cl += __popc(bits);
-      }
-      int incl = cl;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      if (!total) continue;
-      int base = 0;
-      if (lane == 31) base = atomicAdd(&ctl->nsel, total);
-      base = __shfl_sync(0xffffffffu, base, 31);
-      int pos = base + incl - cl;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        uint32_t bits = w[r];
-        const int64_t kb = ((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r) << 5;
-        while (bits) {
-          b.vsel[pos++] = kb + (__ffs(bits) - 1);
-          bits &= bits - 1;
-        }
-      }
+    for (int u = gw * 32 + lane; u < U; u += nw * 32) {
+      const int32_t e = c.urec[u].x;
+      if (e >= 0) s.cc[e] += 1;
     }
+    grid.sync();
   }
   TL_MAX(19);
-  // ---- phase 2 (LFU bitmap path): every update done; evict, warp per victim
+  // ---- in-kernel eviction: LFU bitmap victims (listed by blocks 1..xb)
   if (emode == 1) {
-    const int64_t ftop0 = __ldcg(&ctl->ftop);   // stable during the update; read before the grid sync
-    grid.sync();
-    TL_MAX(20);
-    const int nsel = ctl->nsel;
-    if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->ftop = (int32_t)(ftop0 + nsel); ctl->nvict = nsel; }
+    const int nsel = __ldcg(&ctl->nsel);
+    const int64_t ftop0 = __ldcg(&ctl->ev_ftop0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->ftop = (int32_t)(ftop0 + nsel);
     for (int i = gw; i < nsel; i += nw) {
       const int64_t key = __ldcg(&b.vsel[i]);
       uint64_t slot = 0;
@@ -981,9 +1266,9 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   // ---- hash maintenance (rare): rebuild from the resident entries
   if (rebuild) {
     grid.sync();
-    const int64_t S = (int64_t)s.hmask + 1;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x)
-      s.hkey[i] = HK_EMPTY;
+    const int64_t HS = (int64_t)s.hmask + 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < HS; i += (int64_t)gridDim.x * blockDim.x)
+      s.hslot[i] = HS_EMPTY;
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->n_tomb = 0; ctl->rebuild_req = 0; }
     for (int64_t e0 = (int64_t)gw * 32; e0 < s.Ecap; e0 += (int64_t)nw * 32) {
@@ -1000,13 +1285,54 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   }
 }
 
+// ------------------------------------------------------------------ debug export of an rmode lookup
+// One CTA: head flags of the sorted composites, a block scan for the unique
+// index u of every head, then unique[u], seg_off[u], status[u] and the
+// inverse by u -- the compact lookup log (R2) the rmode path never builds.
+constexpr int CL_THREADS = 1024, CL_ITEMS = 8;   // n <= 8192 (the rmode dedup's bound)
+__global__ void __launch_bounds__(CL_THREADS) k_compact_log(Dev s, Call c) {
+  __shared__ int u_of[CL_THREADS * CL_ITEMS];
+  __shared__ int warp_sums[32];
+  const int n = s.ctl->abort ? 0 : c.n, pb = c.pbits;
+  const int i0 = threadIdx.x * CL_ITEMS;
+  bool hd[CL_ITEMS];
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < CL_ITEMS; ++k) {
+    const int r = i0 + k;
+    hd[k] = r < n && (r == 0 || (c.sortbuf0[r] >> pb) != (c.sortbuf0[r - 1] >> pb));
+    cnt += hd[k];
+  }
+  int tot = 0;
+  int u = block_scan_int(cnt, warp_sums, &tot);
+#pragma unroll
+  for (int k = 0; k < CL_ITEMS; ++k) {
+    const int r = i0 + k;
+    if (hd[k]) {
+      u_of[r] = u;
+      c.uniq[u] = (int64_t)(c.sortbuf0[r] >> pb);
+      c.seg_off[u] = r;
+      c.dbg_status[u] = c.status[r];
+      ++u;
+    }
+  }
+  if (threadIdx.x == 0) { c.seg_off[tot] = n; *c.dbg_U = tot; }
+  __syncthreads();
+  for (int pos = threadIdx.x; pos < n; pos += blockDim.x) c.dbg_inverse[pos] = u_of[c.inverse[pos]];
+}
+
+void launch_compact_log(const Dev& s, const Call& c, cudaStream_t st) { k_compact_log<<<1, CL_THREADS, 0, st>>>(s, c); }
+
 // ------------------------------------------------------------------ launchers
 constexpr int FUSED_MAX_DD_RANK = 8192;
 constexpr int FUSED_MAX = 8192;
 
 bool fused_ok(const Dev& s, int n) { return n <= FUSED_MAX; }
 
-int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st) {
+constexpr int EV_BLOCKS = 32;   // blocks of the deferred eviction (16 warps each)
+
+int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st,
+                    void* evbuf, const void* p2pview, bool evict, int compact) {
   static uint64_t attr_devs = 0;   // devices whose function attribute is set
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1014,8 +1340,20 @@ int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, i
     cudaFuncSetAttribute(k_dd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, FUSED_MAX * 8);
     attr_devs |= 1ull << (dev & 63);
   }
-  int blocks = std::max(1, (n + 31) / 32);
-  k_dd_fused<<<blocks, DDF_THREADS, (size_t)std::max(n, 1) * 8, st>>>(c.keys, n, pbits, s, c, t, lookup);
+  const int ndd = std::max(1, (n + 31) / 32);
+  P2P pm{};
+  int push = 0;
+  if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
+  k_dd_fused<<<ndd + (evict ? EV_BLOCKS : 0), DDF_THREADS, (size_t)std::max(n, 1) * 8, st>>>(
+      c.keys, n, pbits, s, c, t, lookup, *reinterpret_cast<EvBuf*>(evbuf), pm, push, ndd, compact);
+  return 1;
+}
+
+int launch_evict_pending(const Dev& s, void* evbuf, const void* p2pview, cudaStream_t st) {
+  P2P pm{};
+  int push = 0;
+  if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
+  k_evict_pending<<<EV_BLOCKS, 256, 0, st>>>(s, *reinterpret_cast<EvBuf*>(evbuf), pm, push);
   return 1;
 }
 
@@ -1117,9 +1455,11 @@ int launch_update_fused(const Dev& s, const Call& c, const float* grads, float l
   P2P pm{};
   int push = 0;
   if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
-  void* args[] = {(void*)&sd, (void*)&cd, (void*)&grads, (void*)&lr, (void*)&b, (void*)&sr, (void*)&pm, (void*)&push};
+  int xb = std::max(1, std::min(8, coop_blocks / 16));   // extraction blocks (after block 0's plan)
+  void* args[] = {(void*)&sd, (void*)&cd, (void*)&grads, (void*)&lr, (void*)&b, (void*)&sr, (void*)&pm, (void*)&push,
+                  (void*)&xb};
   if (pdl_mode() >= 2)
-    launch_pdl(k_update_fused, coop_blocks, UPD_THREADS, smem, st, true, true, sd, cd, grads, lr, b, sr, pm, push);
+    launch_pdl(k_update_fused, coop_blocks, UPD_THREADS, smem, st, true, true, sd, cd, grads, lr, b, sr, pm, push, xb);
   else
     cudaLaunchCooperativeKernel((void*)k_update_fused, dim3(coop_blocks), dim3(UPD_THREADS), args, smem, st);
   return 1;

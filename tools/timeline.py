@@ -1,4 +1,10 @@
-"""Fused kernels' timeline from per-warp %globaltimer marks (build with HET_TIMELINE=1)."""
+"""Fused kernels' timeline from per-warp %globaltimer marks (build with HET_TIMELINE=1).
+
+    python tools/timeline.py [--graph]
+
+--graph: the step (lookup + update) captured once and replayed, as bench.py
+times it; otherwise eager launches.  Prints p50/max of every mark, in us from
+the first dedup block's start."""
 import ctypes
 import os
 import sys
@@ -14,6 +20,7 @@ from workload import gen  # noqa: E402
 TLW = 8192
 B, D = 128, 128
 n = B * 26
+graph_mode = "--graph" in sys.argv
 cards = gen.scaled_cards(int(os.environ["TL_ROWS"])) if os.environ.get("TL_ROWS") else gen.cards_for("criteo")
 dev = torch.device("cuda", 0)
 c = het.HetCache(sum(cards), D, 0.1, 100, het.HET_LFU, max_keys_per_call=n)
@@ -29,13 +36,24 @@ while t < 6500:
 keys = gen.criteo_keys(0, t, 20, B, cards, device=dev)
 out = torch.empty((n, D), device=dev)
 names = {0: "dd.start", 2: "dd.work", 3: "dd.tail0", 5: "dd.loaded", 6: "dd.scanned", 4: "dd.tail1",
-         22: "plan.start", 7: "plan.pop", 23: "plan.end", 8: "lk.start", 13: "lk.find", 14: "lk.install",
-         15: "lk.vread", 10: "lk.work", 11: "lk.tail0", 12: "lk.tail1", 16: "up.start", 18: "up.seg", 19: "up.finds",
-         20: "up.sync", 21: "up.evict"}
+         12: "dd.evict", 22: "plan.start", 7: "plan.pop", 23: "plan.end", 8: "lk.start",
+         13: "lk.find", 14: "lk.install", 15: "lk.vread", 10: "lk.work", 16: "up.start", 18: "up.seg",
+         11: "up.xwait", 20: "up.xdone", 19: "up.sync", 21: "up.end"}
+kbuf, gbuf = keys[0].clone(), g.clone()
+graph = None
+if graph_mode:
+    c.step(kbuf, gbuf, out, 0.01)
+    graph = c.capture_step(kbuf, gbuf, out, 0.01)
 for j in range(20):
     torch.cuda.synchronize()
     lib.het_debug_timeline(None, 24, TLW)
-    c.lookup(keys[j], het.HET_CLOCK_AUTO, out=out); c.update(keys[j], g, 0.01)
+    if graph is not None:
+        kbuf.copy_(keys[j])
+        torch.cuda.synchronize()
+        lib.het_debug_timeline(None, 24, TLW)
+        graph.replay()
+    else:
+        c.lookup(keys[j], het.HET_CLOCK_AUTO, out=out); c.update(keys[j], g, 0.01)
     torch.cuda.synchronize()
     lib.het_debug_timeline(buf.ctypes.data, 24, TLW)
     if j < 17:
@@ -43,7 +61,7 @@ for j in range(20):
     v = buf.reshape(24, TLW).astype(np.float64)
     t0 = v[0][v[0] > 0].min()
     parts = []
-    for m in sorted(names):
+    for m in sorted(names, key=lambda m: np.median(v[m][v[m] > 0]) if (v[m] > 0).any() else 1e30):
         x = v[m][v[m] > 0]
         if x.size:
             x = (x - t0) / 1000.0
