@@ -181,6 +181,13 @@ het_status_t het_debug_dump_cache(het_cache_t h, int64_t* keys, float* v, float*
                                   uint32_t* cc, uint32_t* prim, uint32_t cap, uint32_t* m,
                                   het_stream_t stream);
 
+/* The last update's overflow-eviction plan (R9),
+ * for inspection: out8 = {mode (0 none, 1 LFU count bitmaps, 2 generic
+ * selection), need = |cache| - C, victims, threshold T (count or tick), the
+ * largest victim key among primary T (mode 1), counts below T present
+ * (bitmask, mode 1), 0, 0}.  Synchronises `stream`. */
+het_status_t het_debug_eviction_plan(het_cache_t h, int64_t* out8, het_stream_t stream);
+
 /* Per-kernel timing with CUDA events on the launching stream (bench). */
 het_status_t het_profile_enable(het_cache_t h, int on);
 /* Fills up to cap (name, total ms, launches) records; returns count in *k. */

@@ -1133,6 +1133,18 @@ het_status_t het_debug_dump_cache(het_cache_t h, int64_t* keys, float* v, float*
   return HET_OK;
 }
 
+het_status_t het_debug_eviction_plan(het_cache_t h, int64_t* out8, het_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!h || !out8) return HET_ERR_ARG;
+  flush_evict(h, st, false);
+  Ctl ctl;
+  CUDA_TRY(h, cudaMemcpyAsync(&ctl, h->d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  const int64_t v[8] = {ctl.emode, ctl.need, ctl.nvict, ctl.T, ctl.Kstar, ctl.lowmask, 0, 0};
+  std::memcpy(out8, v, sizeof(v));
+  return HET_OK;
+}
+
 het_status_t het_profile_enable(het_cache_t h, int on) {
   if (!h) return HET_ERR_ARG;
   h->prof = on != 0;

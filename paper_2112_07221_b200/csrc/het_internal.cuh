@@ -233,6 +233,33 @@ __device__ __forceinline__ int32_t warp_find_slot(const Dev& s, int64_t key, int
   return -1;
 }
 
+// As warp_find; on a miss also the slot warp_insert would claim (the first
+// window holding a TOMB or EMPTY slot, its first TOMB else its first EMPTY)
+// and that slot's word, so the insert is one CAS without a second probe.
+__device__ __forceinline__ int32_t warp_find_cand(const Dev& s, int64_t key, int lane, uint64_t* cslot,
+                                                  uint64_t* cword) {
+  uint64_t w = hash_home(s, key);
+  *cslot = ~0ull;
+  for (int it = 0; it < (1 << 20); ++it) {
+    uint64_t slot = (w + lane) & s.hmask;
+    const uint64_t hw = s.hslot[slot];
+    unsigned m = __ballot_sync(0xffffffffu, hs_is(hw, key));
+    if (m) return __shfl_sync(0xffffffffu, hs_val(hw), __ffs(m) - 1);
+    const unsigned me = __ballot_sync(0xffffffffu, hw == HS_EMPTY);
+    if (*cslot == ~0ull) {
+      const unsigned mt = __ballot_sync(0xffffffffu, hw == HS_TOMB);
+      if (mt | me) {
+        const int src = __ffs(mt ? mt : me) - 1;
+        *cslot = __shfl_sync(0xffffffffu, slot, src);
+        *cword = __shfl_sync(0xffffffffu, hw, src);
+      }
+    }
+    if (me) return -1;
+    w = (w + 32) & s.hmask;
+  }
+  return -1;
+}
+
 // Single-thread find (for many keys per warp): scans whole 32-slot windows
 // (16 x 16 B loads) with the same stop rule as warp_find.
 __device__ __forceinline__ int32_t thread_find_slot(const Dev& s, int64_t key, uint64_t* slot_out) {
@@ -289,6 +316,22 @@ __device__ __forceinline__ void warp_insert(const Dev& s, int64_t key, int32_t e
     }
     w = (w + 32) & s.hmask;
   }
+}
+
+// Insert a key known to be absent at the candidate slot warp_find_cand
+// returned (one CAS); a slot taken meanwhile falls back to warp_insert.
+__device__ __forceinline__ void warp_insert_at(const Dev& s, int64_t key, int32_t entry, int lane, uint64_t cslot,
+                                               uint64_t cword) {
+  int ok = 0;
+  if (lane == 0 && cslot != ~0ull) {
+    const unsigned long long old = atomicCAS((unsigned long long*)&s.hslot[cslot], (unsigned long long)cword,
+                                             (unsigned long long)hs_pack(key, entry));
+    if (old == (unsigned long long)cword) {
+      if (cword == HS_TOMB) atomicSub(&s.ctl->n_tomb, 1);
+      ok = 1;
+    }
+  }
+  if (!__shfl_sync(0xffffffffu, ok, 0)) warp_insert(s, key, entry, lane);
 }
 
 // Warp-cooperative delete: the key is present.

@@ -62,6 +62,7 @@ __global__ void k_begin(Dev s, uint64_t t, int n) {
   if (t == CLOCK_AUTO) { t = ctl->t_auto; ctl->t_auto = t + 1; }
   ctl->t_cur = t;
   ctl->lk_seq = ctl->lk_seq + 1;
+  ctl->nsel = 0;   // the fused update's victim list (its extraction blocks append)
   s.cnt[C_LOOKUPS] += 1;
   s.cnt[C_KEYS] += (unsigned long long)n;
 }

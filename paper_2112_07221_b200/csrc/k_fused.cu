@@ -37,7 +37,7 @@ namespace het {
 #ifdef HET_TIMELINE
 // per-warp slots (no contention): g_tlw[mark][warp], read and reduced on the host
 constexpr int TLW = 8192;
-__device__ unsigned long long g_tlw[24 * TLW];
+__device__ unsigned long long g_tlw[32 * TLW];
 __device__ __forceinline__ unsigned long long tl_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -52,8 +52,8 @@ extern "C" int het_debug_timeline(unsigned long long* out, int marks, int warps)
   if (out) cudaMemcpyFromSymbol(out, g_tlw, sizeof(unsigned long long) * (size_t)marks * TLW);
   cudaMemset((void*)0, 0, 0);
   static unsigned long long* zero = nullptr;
-  if (!zero) zero = (unsigned long long*)calloc(24 * TLW, 8);
-  cudaMemcpyToSymbol(g_tlw, zero, sizeof(unsigned long long) * 24 * TLW);
+  if (!zero) zero = (unsigned long long*)calloc(32 * TLW, 8);
+  cudaMemcpyToSymbol(g_tlw, zero, sizeof(unsigned long long) * 32 * TLW);
   (void)warps;
   return 0;
 }
@@ -113,11 +113,11 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 // P:439); block 0 also the LFU plan's counters and bitmap words around the
 // previous step's threshold (the update's plan).  Hints only: no
 // result depends on them.
-__device__ __forceinline__ void prefetch_lookup_lines(const Dev& s, const uint64_t* comp, int n, int pbits) {
+__device__ __forceinline__ void prefetch_lookup_lines(const Dev& s, const uint32_t* kq, int n) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int p = blockIdx.x * 32 + lane;
   if (p < n && wid < 8) {
-    const int64_t key = (int64_t)(comp[p] >> pbits);
+    const int64_t key = (int64_t)kq[p];
     const bool own = key % s.world == s.rank;
     const int64_t row = key / s.world;
     if (wid < 2) prefetch_l2(s.hslot + hash_home(s, key) + 16 * wid);
@@ -139,7 +139,124 @@ __device__ __forceinline__ void prefetch_lookup_lines(const Dev& s, const uint64
     const int64_t w0 = kblk << (LFU_BLK_SHIFT - 5);
     for (int64_t i = (int64_t)t * 32; i < 256; i += (int64_t)nt * 32)
       if (w0 + i < s.bm_words) prefetch_l2(s.bm + (int64_t)T * s.bm_words + w0 + i);
+    // the words of every non-empty count-T block up to K*'s (the next
+    // extraction reads them): one pass over the block counters
+    const uint32_t* bc = s.bcnt + (int64_t)T * s.nbk;
+    for (int64_t k = t; k <= kblk + 1 && k < s.nbk; k += nt)
+      if (__ldcg(&bc[k]))
+        for (int l = 0; l < 4; ++l)
+          prefetch_l2(s.bm + (int64_t)T * s.bm_words + (k << (LFU_BLK_SHIFT - 5)) + 32 * l);
   }
+}
+
+// #{q in [q0, q1) : key_q <= m} (le) or < m, over whole 128-bit vectors
+// (q0 a multiple of 4; keys past q1 in the last vector are padding above
+// every key), two vectors and two partial sums per iteration
+__device__ __forceinline__ int count_le(const uint4* __restrict__ k4, int q0, int q1, uint32_t m, bool le) {
+  if (q0 >= q1) return 0;
+  int c0 = 0, c1 = 0;
+  const int v0 = q0 >> 2, v1 = (q1 + 3) >> 2;
+  int v = v0;
+  if (le) {
+    for (; v + 1 < v1; v += 2) {
+      const uint4 a = k4[v], b = k4[v + 1];
+      c0 += (a.x <= m) + (a.y <= m) + (a.z <= m) + (a.w <= m);
+      c1 += (b.x <= m) + (b.y <= m) + (b.z <= m) + (b.w <= m);
+    }
+    if (v < v1) { const uint4 a = k4[v]; c0 += (a.x <= m) + (a.y <= m) + (a.z <= m) + (a.w <= m); }
+  } else {
+    for (; v + 1 < v1; v += 2) {
+      const uint4 a = k4[v], b = k4[v + 1];
+      c0 += (a.x < m) + (a.y < m) + (a.z < m) + (a.w < m);
+      c1 += (b.x < m) + (b.y < m) + (b.z < m) + (b.w < m);
+    }
+    if (v < v1) { const uint4 a = k4[v]; c0 += (a.x < m) + (a.y < m) + (a.z < m) + (a.w < m); }
+  }
+  return c0 + c1;
+}
+
+// per-call begin (block 0, thread 0): clock, sequence, counters, abort reset
+__device__ __forceinline__ void dd_begin(const Dev& s, const Call& c, int n, uint64_t t, int lookup, int bad,
+                                         int compact) {
+  Ctl* ctl = s.ctl;
+  if (lookup) {
+    if (t == CLOCK_AUTO) { t = ctl->t_auto; ctl->t_auto = t + 1; }
+    ctl->t_cur = t;
+    ctl->lk_seq = ctl->lk_seq + 1;
+    s.cnt[C_LOOKUPS] += 1;
+    s.cnt[C_KEYS] += (unsigned long long)n;
+  }
+  ctl->abort = 0;
+  ctl->nsel = 0;              // the update's victim list (its extraction blocks append)
+  if (!compact) ctl->U = n;   // rmode: every sorted position is a work item of the lookup
+  if (bad) { raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/); ctl->U = 0; c.seg_off[0] = 0; }
+}
+
+// rmode dedup (K1): the stable sort position of every occurrence, r(p) =
+// #{q : key_q < key_p} + #{q < p : key_q == key_p}, counted over the 32-bit
+// keys in shared memory (R15: keys < 2^32), four per 128-bit load; block b
+// ranks positions [32b, 32b + 32), its warps split the q range.  Writes the
+// sorted composites (key << pbits | p) and perm; the lookup reads key runs.
+__device__ __forceinline__ void dd_rank_rmode(const int64_t* __restrict__ keys, int n, int pbits, const Dev& s,
+                                              const Call& c, uint64_t t, int lookup, uint32_t* kq,
+                                              int (*part)[32]) {
+  int bad = 0;
+  {  // all key loads of this thread in flight at once
+    int64_t kk[DDF_ITEMS];
+#pragma unroll
+    for (int i = 0; i < DDF_ITEMS; ++i) {
+      const int q = threadIdx.x + i * DDF_THREADS;
+      kk[i] = q < n ? __ldg(&keys[q]) : 0;
+    }
+#pragma unroll
+    for (int i = 0; i < DDF_ITEMS; ++i) {
+      const int q = threadIdx.x + i * DDF_THREADS;
+      if (q < n) {
+        if (kk[i] < 0 || kk[i] >= s.R) bad = 1;
+        kq[q] = (uint32_t)kk[i];
+      }
+    }
+    const int npad = (n + 3) & ~3;   // pad to whole 128-bit loads with a key above every real one
+    if (threadIdx.x < npad - n) kq[n + threadIdx.x] = 0xFFFFFFFFu;
+  }
+  bad = __syncthreads_or(bad);
+  TL_MAX(1);
+  if (!bad && lookup) prefetch_lookup_lines(s, kq, n);
+  if (blockIdx.x == 0 && threadIdx.x == 0) dd_begin(s, c, n, t, lookup, bad, 0);
+  if (bad) return;
+  TL_MAX(3);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p = blockIdx.x * 32 + lane;
+  const uint32_t mine = p < n ? kq[p] : 0xFFFFFFFFu;
+  const int per = (((n + DDF_WARPS - 1) / DDF_WARPS) + 3) & ~3;
+  const int q0 = min(n, wid * per), q1 = min(n, q0 + per);
+  const int pmin = blockIdx.x * 32, pmax = pmin + 31;
+  const uint4* k4 = reinterpret_cast<const uint4*>(kq);
+  int cnt = 0;
+  if (q1 <= pmin) {           // every q before every p of the block: key_q <= key_p (q1 = q0 + per: whole vectors)
+    cnt = count_le(k4, q0, q1, mine, true);
+  } else if (q0 > pmax) {     // every q after every p: key_q < key_p (ranges end on a multiple of 4 or
+    cnt = count_le(k4, q0, q1, mine, false);   // in the padding, which never counts)
+  } else {                    // the range meets the block's own positions: before / among / after them
+    const int a = max(q0, min(q1, pmin)), z = max(a, min(q1, pmax + 1));
+    cnt = count_le(k4, q0, a, mine, true);       // q0 and pmin are multiples of 4
+    for (int q = a; q < z; ++q) {
+      const uint32_t x = kq[q];
+      cnt += (x < mine) || (x == mine && q < p);
+    }
+    cnt += count_le(k4, z, q1, mine, false);     // pmax + 1 is a multiple of 4; padding never counts
+  }
+  part[wid][lane] = cnt;
+  __syncthreads();
+  TL_MAX(5);
+  if (wid == 0 && p < n) {
+    int r = 0;
+#pragma unroll
+    for (int w = 0; w < DDF_WARPS; ++w) r += part[w][lane];
+    c.sortbuf0[r] = ((uint64_t)mine << pbits) | (uint64_t)p;
+    c.perm[r] = p;                 // stable position grouping
+  }
+  TL_MAX(2);
 }
 
 // blocks [0, ndd): the dedup; blocks [ndd, gridDim.x): the overflow eviction
@@ -153,12 +270,16 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
     evict_listed(s, eb, push ? &pm : nullptr, blockIdx.x - ndd, gridDim.x - ndd);
     return;
   }
-  extern __shared__ uint64_t comp[];
+  extern __shared__ __align__(16) uint64_t comp[];
   __shared__ int part[DDF_WARPS][32];
   __shared__ int warp_sums[32];
   __shared__ int s_last;
   Ctl* ctl = s.ctl;
-  TL_MIN(0); TL_MAX(1);
+  TL_MIN(0);
+  if (!compact) {
+    dd_rank_rmode(keys, n, pbits, s, c, t, lookup, reinterpret_cast<uint32_t*>(comp), part);
+    return;
+  }
   int bad = 0;
   {  // all key loads of this thread in flight at once
     int64_t kk[DDF_ITEMS];
@@ -177,19 +298,7 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
     }
   }
   bad = __syncthreads_or(bad);
-  if (!bad && lookup) prefetch_lookup_lines(s, comp, n, pbits);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {   // per-call begin, overlapped with the rank work
-    if (lookup) {
-      if (t == CLOCK_AUTO) { t = ctl->t_auto; ctl->t_auto = t + 1; }
-      ctl->t_cur = t;
-      ctl->lk_seq = ctl->lk_seq + 1;
-      s.cnt[C_LOOKUPS] += 1;
-      s.cnt[C_KEYS] += (unsigned long long)n;
-    }
-    ctl->abort = 0;
-    if (!compact) ctl->U = n;   // rmode: every sorted position is a work item of the lookup
-    if (bad) { raise_err(ctl, 2 /*HET_ERR_KEY_RANGE*/); ctl->U = 0; c.seg_off[0] = 0; }
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) dd_begin(s, c, n, t, lookup, bad, 1);   // overlapped with the rank work
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int p = blockIdx.x * 32 + lane;
   if (!bad) {
@@ -210,7 +319,6 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
     }
   }
   TL_MAX(2);
-  if (!compact) return;   // rmode: the sorted composites and perm are the dedup (the lookup reads key runs)
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&ctl->dd_done, 1) == ndd - 1;
@@ -309,8 +417,18 @@ __device__ __forceinline__ bool key_run(const Call& c, int r, int lane, int64_t*
 // needT-th smallest key of count T.  Loads are issued in parallel: the 16
 // populations by 16 lanes, the block counters of bitmap T in chunks of
 // blockDim (coalesced, block-wide prefix), stopping at the chunk holding K*.
-__device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_sums, int64_t need) {
-  Ctl* ctl = s.ctl;
+struct Plan {          // an eviction plan (shared memory of the block that derives it)
+  int emode;           // 0 none, 1 LFU count bitmaps, 2 generic selection
+  int rebuild;         // hash rebuild requested (tombstones > S/8)
+  uint32_t T;          // threshold count
+  uint32_t lowmask;    // counts < T with residents (all of them victims)
+  int64_t Kstar;       // largest victim key of count T
+  int64_t needT;       // victims among count T
+  int64_t need;        // |cache| - C
+  int64_t ftop;        // free-stack top (victim i frees into fstack[ftop + i])
+};
+
+__device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_sums, int64_t need, Plan* pl) {
   __shared__ int s_T;
   __shared__ long long s_needT;
   __shared__ long long s_blk, s_before;
@@ -328,12 +446,12 @@ __device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_su
     const unsigned hit = __ballot_sync(0xffffffffu, lane < s.lfu_cb && excl < need && incl >= need);
     const unsigned nonempty = __ballot_sync(0xffffffffu, pc > 0);
     if (lane == 0) {
-      ctl->emode = 2;                       // until K* is found below
+      pl->emode = 2;                        // until K* is found below
       s_T = hit ? __ffs(hit) - 1 : -1;
     }
     if (hit && lane == __ffs(hit) - 1) {
       s_needT = need - excl;
-      ctl->lowmask = nonempty & ((1u << lane) - 1u);
+      pl->lowmask = nonempty & ((1u << lane) - 1u);
     }
   }
   __syncthreads();
@@ -358,6 +476,7 @@ __device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_su
     carry += tot;
     __syncthreads();
   }
+  TL_MAX(24);
   // level 1: the block inside the super-block (64 counters, one warp)
   if (s_done && threadIdx.x < 32) {
     const int64_t b0 = s_sb << 6;
@@ -374,7 +493,7 @@ __device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_su
     if (x1 > 0 && ex + x0 < needT && ex + x0 + x1 >= needT) { s_blk = k0 + 1; s_before = ex + x0; }
   }
   __syncthreads();
-  TL_MAX(9);
+  TL_MAX(25);
   if (s_blk < 0) return;
   if (threadIdx.x < 32) {
     const int64_t blk = s_blk;
@@ -403,10 +522,10 @@ __device__ void lfu_threshold(const Dev& s, int* warp_sums_i, long long* warp_su
           uint32_t bits = w[q];
           for (int kk = 1; kk < r; ++kk) bits &= bits - 1;
           int64_t key = (((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + q) << 5) + (__ffs(bits) - 1);
-          ctl->Kstar = key;
-          ctl->T = (uint32_t)T;
-          ctl->needT = needT;
-          ctl->emode = 1;
+          pl->Kstar = key;
+          pl->T = (uint32_t)T;
+          pl->needT = needT;
+          pl->emode = 1;
           break;
         }
         r -= pc;
@@ -426,7 +545,7 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
   if (threadIdx.x < 4) bc[threadIdx.x] = 0;
   if (threadIdx.x == 0) { s_nmiss = 0; s_minp = 0xFFFFFFFFu; }
   dpop_init(dpop);
-  TL_MIN(8); TL_MAX(9);
+  TL_MIN(8);
   __syncthreads();
   Ctl* ctl = s.ctl;
   const int lane = threadIdx.x & 31;
@@ -461,11 +580,12 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
   const bool reg = D4 <= 32;
   const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
   float4 wrow = zero4, vrow = zero4;
+  uint64_t cslot = ~0ull, cword = 0;   // a miss's insert slot, from the probe
   if (live) {
     if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
     if (lane == 1) gpre = s.cg[key];
     if (reg && lane < D4) wrow = __ldcg(reinterpret_cast<const float4*>(s.W + key * s.D) + lane);
-    e = warp_find(s, key, lane);
+    e = warp_find_cand(s, key, lane, &cslot, &cword);
     if (reg && e >= 0 && lane < D4) vrow = __ldcg(reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D) + lane);
     gpre = __shfl_sync(0xffffffffu, gpre, 1);
     TL_MAX(13);
@@ -498,6 +618,7 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
         } else {
           moff = atomicSub(&ctl->ftop, 1) - 1;      // the entry's free-stack index
           atomicMin(&ctl->min_install, mprim);
+          TL_MAX(28);
         }
       }
       c.status[u] = st;
@@ -539,7 +660,9 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
           e = -1;
         } else {
           e = s.fstack[idx];
-          warp_insert(s, key, e, lane);
+          TL_MAX(29);
+          warp_insert_at(s, key, e, lane, cslot, cword);
+          TL_MAX(30);
           if (lane == 0) {
             s.ekey[e] = key;
             s.eprim[e] = mprim;
@@ -979,54 +1102,124 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// LFU bitmap path: the victim keys of the listed bitmap blocks (count c < T:
-// all set bits; count T: the keys <= K*), one block per warp, appended to vsel
-__device__ __forceinline__ void extract_victims(const Dev& s, const EvBuf& b, int gw, int nw, int lane) {
+// LFU bitmap path: the victim keys -- every resident key of count c < T (the
+// counts in lowmask) and the keys <= K* of count T -- appended to vsel.
+// Warp (gw, nw) takes chunks of 16 bitmap blocks (4096 keys each): one block
+// counter per lane, then the words of up to XB non-empty blocks at once
+// (4 words per lane each) and one vsel reservation for them.
+constexpr int XCH = 16;   // bitmap blocks per extraction chunk
+constexpr int XB = 4;     // non-empty blocks whose words are in flight at once (the batch logic assumes 4)
+__device__ __forceinline__ void extract_victims(const Dev& s, const EvBuf& b, const Plan& pl, int gw, int nw,
+                                                int lane) {
   Ctl* ctl = s.ctl;
-  const uint32_t T = __ldcg(&ctl->T);
-  const int64_t Kstar = __ldcg(&ctl->Kstar);
-  const int ntask = __ldcg(&ctl->ntask);
-  for (int task = gw; task < ntask; task += nw) {
-    const int32_t code = __ldcg(&b.cand[task]);
-    const uint32_t cc = (uint32_t)code >> 27;
-    const int64_t blk = code & ((1 << 27) - 1);
+  const uint32_t T = pl.T;
+  const int64_t Kstar = pl.Kstar;
+  const uint32_t lowmask = pl.lowmask;
+  const int64_t kblk = Kstar >> LFU_BLK_SHIFT;
+  const int64_t nch_full = (s.nbk + XCH - 1) / XCH, nch_T = (kblk + XCH) / XCH;
+  int64_t total = nch_T;                       // chunks: counts < T in lowmask (all blocks), then count T
+  for (uint32_t cc = 0; cc < T; ++cc) if ((lowmask >> cc) & 1) total += nch_full;
+  for (int64_t it = gw; it < total; it += nw) {
+    uint32_t cc = T;
+    int64_t ch = it;
+    for (uint32_t x = 0; x < T; ++x) {
+      if (!((lowmask >> x) & 1)) continue;
+      if (ch < nch_full) { cc = x; break; }
+      ch -= nch_full;
+    }
+    const int64_t nb = cc < T ? s.nbk : kblk + 1;
+    const int64_t blk_l = ch * XCH + lane;
+    const uint32_t bcv = (lane < XCH && blk_l < nb) ? __ldcg(&s.bcnt[(int64_t)cc * s.nbk + blk_l]) : 0u;
+    unsigned nz = __ballot_sync(0xffffffffu, bcv != 0);
+    TL_MAX(9);
     const uint32_t* bm = s.bm + (int64_t)cc * s.bm_words;
-    uint32_t w[4];
-    int cl = 0;
+    while (nz) {
+      int32_t blk[XB];   // fixed slots (registers): block of batch slot j, or -1
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int64_t wi = (blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r;
-      uint32_t bits = wi < s.bm_words ? __ldcg(&bm[wi]) : 0u;
-      if (cc == T) {   // keep keys <= K*
-        const int64_t k0 = wi << 5;
-        if (k0 > Kstar) bits = 0;
-        else if (k0 + 31 > Kstar) bits &= (1u << (Kstar - k0 + 1)) - 1u;
+      for (int j = 0; j < XB; ++j) {
+        blk[j] = nz ? (int32_t)(ch * XCH) + (__ffs(nz) - 1) : -1;
+        nz &= nz - 1;
       }
-      w[r] = bits;
-      cl += __popc(bits);
-    }
-    int incl = cl;
+      const int nbat = (blk[XB - 1] >= 0) ? XB : (blk[2] >= 0 ? 3 : (blk[1] >= 0 ? 2 : 1));
+      uint32_t w[XB][4];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (!total) continue;
-    int base = 0;
-    if (lane == 31) base = atomicAdd(&ctl->nsel, total);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    int pos = base + incl - cl;
+      for (int j = 0; j < XB; ++j)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      uint32_t bits = w[r];
-      const int64_t kb = ((blk << (LFU_BLK_SHIFT - 5)) + lane * 4 + r) << 5;
-      while (bits) {
-        b.vsel[pos++] = kb + (__ffs(bits) - 1);
-        bits &= bits - 1;
+        for (int r = 0; r < 4; ++r) {
+          const int64_t wi = j < nbat ? ((int64_t)blk[j] << (LFU_BLK_SHIFT - 5)) + lane * 4 + r : 0;
+          w[j][r] = (j < nbat && wi < s.bm_words) ? __ldcg(&bm[wi]) : 0u;
+        }
+      TL_MAX(4);
+      int cl[XB], incl[XB], tot = 0;
+#pragma unroll
+      for (int j = 0; j < XB; ++j) {
+        cl[j] = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (cc == T && j < nbat) {   // keep keys <= K*
+            const int64_t k0 = (((int64_t)blk[j] << (LFU_BLK_SHIFT - 5)) + lane * 4 + r) << 5;
+            if (k0 > Kstar) w[j][r] = 0;
+            else if (k0 + 31 > Kstar) w[j][r] &= (1u << (Kstar - k0 + 1)) - 1u;
+          }
+          cl[j] += __popc(w[j][r]);
+        }
+        incl[j] = cl[j];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl[j], o);
+          if (lane >= o) incl[j] += y;
+        }
+        tot += __shfl_sync(0xffffffffu, incl[j], 31);
       }
+      TL_MAX(17);
+      if (!tot) continue;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&ctl->nsel, tot);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      TL_MAX(31);
+      // the batch's victims fill vsel[base, base + tot), lane by lane in key order
+#pragma unroll
+      for (int j = 0; j < XB; ++j) {
+        int pos = base + incl[j] - cl[j];
+        base += __shfl_sync(0xffffffffu, incl[j], 31);
+        if (j >= nbat) continue;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          uint32_t bits = w[j][r];
+          const int64_t kb = (((int64_t)blk[j] << (LFU_BLK_SHIFT - 5)) + lane * 4 + r) << 5;
+          while (bits) {
+            b.vsel[pos++] = kb + (__ffs(bits) - 1);
+            bits &= bits - 1;
+          }
+        }
+      }
+      TL_MAX(6);
     }
   }
+}
+
+// This step's eviction plan from the cache state after the lookup (counts
+// final: L6 precedes U3).  Deterministic: block 0 and every
+// extraction block derive the same plan from the same state, so the
+// extraction needs no hand-off from block 0.
+__device__ __forceinline__ void make_plan(const Dev& s, bool abort, Plan* pl) {
+  __shared__ long long warp_sums[32];
+  __shared__ int warp_sums_i[32];
+  Ctl* ctl = s.ctl;
+  if (threadIdx.x == 0) {
+    const int64_t ftop = __ldcg(&ctl->ftop);
+    const int64_t res = s.Ecap - ftop;
+    const int64_t need = res - s.C;
+    const bool none = abort || need <= 0;
+    pl->need = none ? 0 : need;
+    pl->ftop = ftop;
+    pl->emode = none ? 0 : ((s.policy == 0 && s.lfu_cb && need < res) ? 1 : 2);
+    pl->rebuild = (int64_t)__ldcg(&ctl->n_tomb) > ((int64_t)s.hmask + 1) / 8;
+    pl->T = 0; pl->lowmask = 0; pl->Kstar = -1; pl->needT = 0;
+  }
+  __syncthreads();
+  if (pl->emode == 1) lfu_threshold(s, warp_sums_i, warp_sums, pl->need, pl);
+  __syncthreads();
 }
 
 // The deferred overflow eviction: victim i of the listed vsel[0, ev_nsel) by
@@ -1081,7 +1274,8 @@ __global__ void __launch_bounds__(256) k_evict_pending(Dev s, EvBuf b, P2P pm, i
 // the other blocks do the ordered segment reduce + SGD + pending + clock.
 // LFU bitmap plans end there: the victims are evicted by the first kernel of
 // the next call (k_dd_fused / k_evict_pending) -- nothing reads or changes
-// the cache in between, so the result is the oracle's.  The generic selection
+// the cache in between, so the result is that of Evict() at the end of the
+// update (R9).  The generic selection
 // (LRU, LFU beyond the bitmaps, evict-all) and steps that rebuild the hash
 // continue in this kernel after grid syncs.
 __global__ void __launch_bounds__(UPD_THREADS)
@@ -1101,87 +1295,53 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   if (threadIdx.x == 0) { s_dirty = 0; s_ev = 0; s_tomb = 0; }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) { mbar_init(&bars[wid], 1); fence_mbar_init(); }
-  TL_MIN(16); TL_MAX(17);
+  TL_MIN(16);
   __syncthreads();
   const bool abort = ctl->abort;
   const int U = abort ? 0 : (c.rmode ? c.n : ctl->U);   // rmode: sorted positions, heads carry the work
   const uint32_t seq = ctl->lk_seq;   // set by the lookup; the plan flag carries it
   const int D4 = s.D >> 2;
   const int S = (D4 >= 256 && D4 % 128 == 0) ? D4 / 128 : 1;   // wide rows: 512-column slices on separate warps
-  if (blockIdx.x == 0) {
-    // ---- the eviction plan
-    __shared__ long long warp_sums[32];
-    __shared__ int warp_sums_i[32];
-    const int64_t res = s.Ecap - (int64_t)ctl->ftop;
-    const int64_t need = res - s.C;
-    if (threadIdx.x == 0) {
-      ctl->nvict = 0; ctl->ncand = 0; ctl->nsub = 0; ctl->vmode = 0; ctl->nsel = 0;
-      const bool none = abort || need <= 0;
-      ctl->need = none ? 0 : need;
-      ctl->emode = none ? 0 : ((s.policy == 0 && s.lfu_cb && need < res) ? 1 : 2);
-      const int64_t HS = (int64_t)s.hmask + 1;
-      ctl->rebuild_req = (int64_t)ctl->n_tomb > HS / 8;
-      ctl->ev_ftop0 = ctl->ftop;   // stable until the victims are freed
-    }
-    __syncthreads();
+  const bool xblock = blockIdx.x >= 1 && blockIdx.x <= xb;
+  __shared__ Plan pl;
+  if (blockIdx.x == 0 || xblock) {
+    // ---- the eviction plan: block 0 publishes it for the other blocks'
+    // end-of-kernel decision; the extraction blocks derive it themselves
     TL_MAX(22);
-    if (ctl->emode == 1) lfu_threshold(s, warp_sums_i, warp_sums, need);
-    __syncthreads();
-    if (threadIdx.x == 0) ctl->generic = ctl->emode == 2;
-    __syncthreads();
-    // task list: every non-empty count bitmap block holding victims -- all
-    // blocks of the counts < T in lowmask, blocks up to K*'s for count T --
-    // one coalesced pass over the block counters by the whole block
-    if (ctl->emode == 1) {
-      __shared__ int s_nt;
-      if (threadIdx.x == 0) s_nt = 0;
-      __syncthreads();
-      const uint32_t T = ctl->T;
-      const int64_t kblk = ctl->Kstar >> LFU_BLK_SHIFT;
-      const uint32_t lowmask = ctl->lowmask;
-      for (uint32_t cc = 0; cc <= T; ++cc) {
-        if (cc < T && !((lowmask >> cc) & 1)) continue;
-        const int64_t nb = cc < T ? s.nbk : kblk + 1;
-        const uint32_t* bc = s.bcnt + (int64_t)cc * s.nbk;
-        for (int64_t k0 = 0; k0 < nb; k0 += (int64_t)blockDim.x * 16) {
-          uint32_t x[16];                       // 16 independent loads per thread in flight
-#pragma unroll
-          for (int r = 0; r < 16; ++r) {
-            const int64_t k = k0 + r * blockDim.x + threadIdx.x;
-            x[r] = k < nb ? __ldcg(&bc[k]) : 0u;
-          }
-#pragma unroll
-          for (int r = 0; r < 16; ++r) {
-            const int64_t k = k0 + r * blockDim.x + threadIdx.x;
-            if (x[r]) b.cand[atomicAdd(&s_nt, 1)] = (int32_t)(((int64_t)cc << 27) | k);
-          }
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) ctl->ntask = s_nt;
-    } else if (threadIdx.x == 0) {
-      ctl->ntask = 0;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) { __threadfence(); st_release_u32(&ctl->plan_flag, seq); }
+    make_plan(s, abort, &pl);
+    TL_MAX(26);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->ncand = 0; ctl->nsub = 0; ctl->vmode = 0;
+    ctl->need = pl.need;
+    ctl->emode = pl.emode;
+    ctl->rebuild_req = pl.rebuild;
+    ctl->ev_ftop0 = (int32_t)pl.ftop;   // stable until the victims are freed
+    ctl->T = pl.T;
+    ctl->Kstar = pl.Kstar;
+    ctl->needT = pl.needT;
+    ctl->lowmask = pl.lowmask;
+    ctl->generic = pl.emode == 2;
+    __threadfence();
+    st_release_u32(&ctl->plan_flag, seq);
     TL_MAX(23);
   }
-  // the plan as every block reads it (block 0 wrote it; the others wait for its flag)
+  // the plan's mode as the other blocks read it (block 0's flag)
   auto read_plan = [&]() {
     if (threadIdx.x == 0) {
       if (blockIdx.x != 0)
-        while (ld_acquire_u32(&ctl->plan_flag) != seq) __nanosleep(32);
+        while (ld_acquire_u32(&ctl->plan_flag) != seq) __nanosleep(64);
       s_emode = abort ? 0 : __ldcg(&ctl->emode);
       s_rebuild = __ldcg(&ctl->rebuild_req);
     }
   };
-  const bool xblock = blockIdx.x >= 1 && blockIdx.x <= xb;
-  // blocks 1..xb: wait for the plan first, then extract (LFU bitmap path)
+  // blocks 1..xb: extract the victim keys (LFU bitmap path); ctl->nsel was
+  // reset by this call's first kernel
   if (xblock) {
-    read_plan();
+    if (threadIdx.x == 0) { s_emode = pl.emode; s_rebuild = pl.rebuild; }
     __syncthreads();
     TL_MAX(11);
-    if (s_emode == 1) extract_victims(s, b, (blockIdx.x - 1) * UPD_WARPS + wid, xb * UPD_WARPS, lane);
+    if (s_emode == 1) extract_victims(s, b, pl, (blockIdx.x - 1) * UPD_WARPS + wid, xb * UPD_WARPS, lane);
     TL_MAX(20);
     __threadfence();
     __syncthreads();
@@ -1329,7 +1489,7 @@ constexpr int FUSED_MAX = 8192;
 
 bool fused_ok(const Dev& s, int n) { return n <= FUSED_MAX; }
 
-constexpr int EV_BLOCKS = 32;   // blocks of the deferred eviction (16 warps each)
+constexpr int EV_BLOCKS = 32;   // blocks of the deferred eviction in k_dd_fused (16 warps each)
 
 int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st,
                     void* evbuf, const void* p2pview, bool evict, int compact) {
@@ -1353,7 +1513,7 @@ int launch_evict_pending(const Dev& s, void* evbuf, const void* p2pview, cudaStr
   P2P pm{};
   int push = 0;
   if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
-  k_evict_pending<<<EV_BLOCKS, 256, 0, st>>>(s, *reinterpret_cast<EvBuf*>(evbuf), pm, push);
+  k_evict_pending<<<2 * EV_BLOCKS, 256, 0, st>>>(s, *reinterpret_cast<EvBuf*>(evbuf), pm, push);
   return 1;
 }
 

@@ -55,7 +55,7 @@ EXPORTS = ["het_get_unique_id", "het_cache_create", "het_lookup", "het_update", 
            "het_debug_lookup_log", "het_debug_victims", "het_debug_dump_cache",
            "het_profile_enable", "het_profile_read", "het_cache_destroy", "het_last_error",
            "het_group_create", "het_group_lookup", "het_group_update", "het_group_evict",
-           "het_group_sync", "het_group_dense_allreduce"]
+           "het_group_sync", "het_group_dense_allreduce", "het_debug_eviction_plan"]
 
 _lib = None
 
@@ -92,6 +92,7 @@ def load():
         "het_group_evict": [P, U32, P, P, P],
         "het_group_sync": [P, U32, P],
         "het_group_dense_allreduce": [P, U32, P, U64, P],
+        "het_debug_eviction_plan": [P, P, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -254,6 +255,13 @@ def het_group_dense_allreduce(hs, bufs, count, stream=None):
     _check(hs[0], load().het_group_dense_allreduce(_arr(ctypes.c_void_p, hs), len(hs),
                                                    _arr(ctypes.c_void_p, [_ptr(b) for b in bufs]), count,
                                                    _stream(stream)), "het_group_dense_allreduce")
+
+
+def het_debug_eviction_plan(h):
+    """The last update's eviction plan: mode, need, victims, T, K*, lowmask."""
+    out = np.zeros(8, np.int64)
+    _check(h, load().het_debug_eviction_plan(h, _ptr(out), _stream(None)), "het_debug_eviction_plan")
+    return dict(zip(["mode", "need", "victims", "T", "Kstar", "lowmask"], [int(x) for x in out[:6]]))
 
 
 def het_cache_destroy(h):

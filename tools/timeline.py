@@ -26,7 +26,7 @@ dev = torch.device("cuda", 0)
 c = het.HetCache(sum(cards), D, 0.1, 100, het.HET_LFU, max_keys_per_call=n)
 lib = het.load()
 lib.het_debug_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
-buf = np.zeros(24 * TLW, np.uint64)
+buf = np.zeros(32 * TLW, np.uint64)
 g = gen.grads(0, 0, n, D, device=dev)
 t = 0
 while t < 6500:
@@ -35,10 +35,12 @@ while t < 6500:
         c.lookup(keys[j], het.HET_CLOCK_AUTO); c.update(keys[j], g, 0.01); t += 1
 keys = gen.criteo_keys(0, t, 20, B, cards, device=dev)
 out = torch.empty((n, D), device=dev)
-names = {0: "dd.start", 2: "dd.work", 3: "dd.tail0", 5: "dd.loaded", 6: "dd.scanned", 4: "dd.tail1",
+names = {0: "dd.start", 2: "dd.work",
          12: "dd.evict", 22: "plan.start", 7: "plan.pop", 23: "plan.end", 8: "lk.start",
          13: "lk.find", 14: "lk.install", 15: "lk.vread", 10: "lk.work", 16: "up.start", 18: "up.seg",
-         11: "up.xwait", 20: "up.xdone", 19: "up.sync", 21: "up.end"}
+         11: "up.xwait", 20: "up.xdone", 19: "up.sync", 21: "up.end", 24: "plan.l2", 25: "plan.l1",
+         26: "plan.kstar", 28: "lk.mpop", 29: "lk.mfstack", 30: "lk.minsert",
+         9: "x.bc", 4: "x.issued", 17: "x.words", 6: "x.written", 31: "x.atomic", 1: "dd.keys", 3: "dd.prefetch", 5: "dd.count"}
 kbuf, gbuf = keys[0].clone(), g.clone()
 graph = None
 if graph_mode:
@@ -46,19 +48,19 @@ if graph_mode:
     graph = c.capture_step(kbuf, gbuf, out, 0.01)
 for j in range(20):
     torch.cuda.synchronize()
-    lib.het_debug_timeline(None, 24, TLW)
+    lib.het_debug_timeline(None, 32, TLW)
     if graph is not None:
         kbuf.copy_(keys[j])
         torch.cuda.synchronize()
-        lib.het_debug_timeline(None, 24, TLW)
+        lib.het_debug_timeline(None, 32, TLW)
         graph.replay()
     else:
         c.lookup(keys[j], het.HET_CLOCK_AUTO, out=out); c.update(keys[j], g, 0.01)
     torch.cuda.synchronize()
-    lib.het_debug_timeline(buf.ctypes.data, 24, TLW)
+    lib.het_debug_timeline(buf.ctypes.data, 32, TLW)
     if j < 17:
         continue
-    v = buf.reshape(24, TLW).astype(np.float64)
+    v = buf.reshape(32, TLW).astype(np.float64)
     t0 = v[0][v[0] > 0].min()
     parts = []
     for m in sorted(names, key=lambda m: np.median(v[m][v[m] > 0]) if (v[m] > 0).any() else 1e30):
@@ -67,3 +69,4 @@ for j in range(20):
             x = (x - t0) / 1000.0
             parts.append(f"{names[m]} p50 {np.median(x):.1f} max {x.max():.1f}")
     print(" | ".join(parts))
+    print("plan", het.het_debug_eviction_plan(c.h))
