@@ -351,6 +351,7 @@ static het_status_t create_impl(uint64_t rows, uint32_t D, double cache_frac, ui
     A(c.hlist, nm);
     A(c.urec, nm);
     A(c.upos, nm);
+    A(c.ucnt, nm);
     A(c.dbg_status, nm);
     A(c.dbg_inverse, nm);
     A(c.dbg_U, 1);
@@ -537,8 +538,8 @@ static het_status_t lookup_pre(het_cache* h, const int64_t* keys, uint32_t n, ui
   // per-phase kernels with the sliced heavy-key segment reduce), N > 1 over
   // the peer-memory exchange for every n; the dedup kernel follows n
   h->fused = !h->no_fused && (d.world == 1 ? (int)n <= FUSED_LOOKUP_MAX : mgpu_p2p(h->mg) != nullptr);
-  // N = 1 after the fused dedup: per-key work indexed by sorted position (no compaction pass)
-  c.rmode = (h->fused && fused_ok(d, (int)n) && d.world == 1) ? 1 : 0;
+  // after the fused dedup: per-key work indexed by sorted position (no compaction pass, R29)
+  c.rmode = (h->fused && fused_ok(d, (int)n)) ? 1 : 0;
   if (h->fused && fused_ok(d, (int)n)) {   // the dedup kernel also runs the deferred eviction
     // a captured graph replays after its own update: keep the eviction blocks
     // (they test the device flag and return when nothing is listed)

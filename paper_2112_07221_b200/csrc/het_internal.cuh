@@ -34,7 +34,8 @@ constexpr uint32_t EP_PIN = 0xFFFFFFFEu;   // eprim of a light-LFU pinned entry 
 constexpr int LFU_CB_MAX = 16;             // LFU count values kept in key bitmaps
 constexpr int LFU_BLK_SHIFT = 12;          // 4096 keys per bitmap block counter
 
-enum : uint8_t { ST_HIT = 0, ST_EXP1 = 1, ST_EXP2 = 2, ST_MISS = 3, ST_NEEDQ = 4 };
+enum : uint8_t { ST_HIT = 0, ST_EXP1 = 1, ST_EXP2 = 2, ST_MISS = 3, ST_NEEDQ = 4,
+                 ST_SKIP = 5 /* rmode: not a key's first sorted position */ };
 
 // device counters (u64), order shared with het_stats_t
 enum {
@@ -169,6 +170,7 @@ struct Call {
   int32_t* hlist;              // [n_max] heavy keys of the current update (segment reduce)
   int4* urec;                  // [n_max] per unique key, lookup -> update: {entry, j0, cnt | dirty << 31, c_c}
   int4* upos;                  // [n_max] its first four batch positions (ascending)
+  int32_t* ucnt;               // [n_max] rmode at N > 1: the key's occurrences (uniq[r] holds the key)
   uint8_t* dbg_status;         // [n_max] rmode: compacted status (debug export)
   int32_t* dbg_inverse;        // [n_max] rmode: compacted inverse (debug export)
   int32_t* dbg_U;              // rmode: unique keys of the compacted log
@@ -395,6 +397,44 @@ __device__ __forceinline__ void write_urec(const Call& c, int u, int32_t e, int 
   }
 }
 
+// rmode: the key run starting at sorted position r (warp-uniform): false if r
+// is not the first position of its key.  Lane l loads composite r - 1 + l and
+// the batch position of sorted r + l (both coalesced, in one round trip); a
+// run longer than 31 is followed chunk by chunk.
+__device__ __forceinline__ bool key_run(const Call& c, int r, int lane, int64_t* key, int* cnt, int* pos_lane) {
+  const int n = c.n, pb = c.pbits;
+  const int q = r - 1 + lane;
+  const uint64_t w = (q >= 0 && q < n) ? __ldcg(&c.sortbuf0[q]) : ~0ull;
+  const int pl = r + lane < n ? __ldcg(&c.perm[r + lane]) : 0;
+  const uint64_t kl = w >> pb;
+  const uint64_t k = __shfl_sync(0xffffffffu, kl, 1);
+  const uint64_t kp = __shfl_sync(0xffffffffu, kl, 0);
+  if (r > 0 && kp == k) return false;
+  unsigned same = __ballot_sync(0xffffffffu, lane >= 1 && q < n && kl == k) >> 1;   // bit j: sorted r + j
+  int len = __ffs(~same) - 1;                                                       // 1..31
+  if (same == 0x7FFFFFFFu) {
+    len = 31;
+    for (int b = r + 31;; b += 32) {
+      const int qq = b + lane;
+      const bool eq = qq < n && (__ldcg(&c.sortbuf0[qq]) >> pb) == k;
+      const unsigned m = __ballot_sync(0xffffffffu, eq);
+      const int run = __ffs(~m) - 1;   // -1 when all 32 equal
+      if (run < 0) { len += 32; continue; }
+      len += run;
+      break;
+    }
+  }
+  *key = (int64_t)k;
+  *cnt = len;
+  *pos_lane = lane < len ? pl : 0;
+  return true;
+}
+
+// LFU threshold (T, K*) for this step, one CTA (the last block of k_lookup_fused):
+// T = the smallest count whose cumulative population reaches `need`, K* = the
+// needT-th smallest key of count T.  Loads are issued in parallel: the 16
+// populations by 16 lanes, the block counters of bitmap T in chunks of
+// blockDim (coalesced, block-wide prefix), stopping at the chunk holding K*.
 // ---------------------------------------------------------------- TMA bulk copy + mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {

@@ -451,17 +451,44 @@ __global__ void k_p2p_pushes(Dev s, P2P m, EvView b) {
 }
 
 // ---------------------------------------------------------------- fused round (n <= 8192)
-// probe + request build for one unique key (warp): Cache.Find, condition (1),
-// the LFU/LRU touch, the inverse of its positions and, unless it is a valid
-// hit, its request record (+ pending row) straight into the owner's inbox.
-__device__ __forceinline__ void probe_build_key(const Dev& s, const Call& c, const P2P& m, int u, int lane,
-                                                unsigned* bc, int* dpop, unsigned long long* sb) {
+// probe + request build (warp per unique key; rmode: per sorted position,
+// non-heads skip), in two phases around a block barrier so that the request
+// slots in each owner's inbox are reserved with one atomic per (block, owner)
+// instead of one per key (thousands of records per owner per round):
+//  A: Cache.Find, condition (1), the LFU/LRU touch, the inverse and the
+//     lookup -> update record; a request takes a block-local slot
+//  B: the record (+ pending row of a dirty entry) straight into the owner's
+//     inbox at its reserved slot
+struct PBKey {            // phase A -> phase B (warp-uniform)
+  int64_t key;
+  int32_t e;
+  uint32_t ecc;
+  int32_t o;              // owner, -1: no request
+  int32_t lslot;          // block-local slot among this block's requests to o
+  uint8_t st;
+  bool dirty;
+};
+
+__device__ __forceinline__ PBKey probe_build_a(const Dev& s, const Call& c, const P2P& m, int u, int lane,
+                                               unsigned* bc, int* dpop, int* s_cnt) {
   Ctl* ctl = s.ctl;
-  const int D4 = s.D >> 2;
-  const int64_t key = c.uniq[u];
-  const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
-  const int cnt = j1 - j0;
-  const int pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
+  PBKey k{};
+  k.o = -1;
+  int64_t key;
+  int j0, cnt, pos_lane;
+  if (c.rmode) {
+    if (!key_run(c, u, lane, &key, &cnt, &pos_lane)) {   // not the key's first sorted position
+      if (lane == 0) { c.urec[u].x = -1; c.status[u] = ST_SKIP; }
+      k.st = ST_SKIP;
+      return k;
+    }
+    j0 = u;
+  } else {
+    key = c.uniq[u];
+    j0 = c.seg_off[u];
+    cnt = c.seg_off[u + 1] - j0;
+    pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
+  }
   uint32_t cntk = 0;
   if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
   const int32_t e = warp_find(s, key, lane);
@@ -489,44 +516,81 @@ __device__ __forceinline__ void probe_build_key(const Dev& s, const Call& c, con
     }
     c.status[u] = st;
     c.uentry[u] = e;
-    if (st == ST_HIT) atomicAdd(&bc[0], 1u);
-    else if (st == ST_EXP1) atomicAdd(&bc[1], 1u);
-    else if (st == ST_MISS) atomicAdd(&bc[3], 1u);
+    atomicAdd(&bc[st == ST_HIT ? 0 : st == ST_EXP1 ? 1 : st == ST_MISS ? 3 : 2], 1u);   // 2: NEEDQ (finished at install)
   }
   st = __shfl_sync(0xffffffffu, st, 0);
-  for (int k = lane; k < cnt; k += 32) c.inverse[k < 32 ? pos_lane : c.perm[j0 + k]] = u;
+  for (int q = lane; q < cnt; q += 32) c.inverse[q < 32 ? pos_lane : c.perm[j0 + q]] = u;
   write_urec(c, u, e, j0, cnt, ecc > ecs, ecc, pos_lane, lane);   // resident: a hit keeps it, a refetch rewrites it
+  if (c.rmode && lane == 0) { c.uniq[u] = key; c.ucnt[u] = cnt; }   // for the install phase
+  k.key = key; k.e = e; k.ecc = ecc; k.st = st;
   if (st != ST_HIT) {
-    const int o = (int)(key % m.N);
-    const bool dirty = e >= 0 && ecc > ecs;
-    int slot = 0;
-    if (lane == 0) slot = atomicAdd(&m.lcnt[o], 1);
-    slot = __shfl_sync(0xffffffffu, slot, 0);
-    const int64_t j = m.c3cnt[o] + slot;
-    if (lane == 0) {
-      Rec r;
-      r.key = key; r.cc = ecc;
-      r.kind = (st == ST_NEEDQ ? K_NEEDQ : st == ST_EXP1 ? K_EXP1 : K_MISS) | (dirty ? K_DIRTY : 0);
-      reqrec(m, o, m.rank)[j] = r;
-      m.uslot[u] = (int32_t)(o * m.CAPS + slot);
-      atomicAdd(&sb[st == ST_NEEDQ ? 0 : 2], 16ull);
-      if (dirty) atomicAdd(&sb[2], 4ull * s.D);
+    k.o = (int)(key % m.N);
+    k.dirty = e >= 0 && ecc > ecs;
+    int ls = 0;
+    if (lane == 0) ls = atomicAdd(&s_cnt[k.o], 1);
+    k.lslot = __shfl_sync(0xffffffffu, ls, 0);
+  }
+  return k;
+}
+
+__device__ __forceinline__ void probe_build_b(const Dev& s, const Call& c, const P2P& m, int u, int lane,
+                                              const PBKey& k, const int* s_base, unsigned long long* sb) {
+  if (k.o < 0) return;
+  const int D4 = s.D >> 2;
+  const int slot = s_base[k.o] + k.lslot;
+  const int64_t j = m.c3cnt[k.o] + slot;
+  if (lane == 0) {
+    Rec r;
+    r.key = k.key; r.cc = k.ecc;
+    r.kind = (k.st == ST_NEEDQ ? K_NEEDQ : k.st == ST_EXP1 ? K_EXP1 : K_MISS) | (k.dirty ? K_DIRTY : 0);
+    reqrec(m, k.o, m.rank)[j] = r;
+    m.uslot[u] = (int32_t)(k.o * m.CAPS + slot);
+    atomicAdd(&sb[k.st == ST_NEEDQ ? 0 : 2], 16ull);
+    if (k.dirty) atomicAdd(&sb[2], 4ull * s.D);
+  }
+  if (k.dirty)
+    warp_copy_row(reinterpret_cast<float4*>(reqrow(m, k.o, m.rank, j)),
+                  reinterpret_cast<const float4*>(s.p + (int64_t)k.e * s.D), D4, lane);
+}
+
+// every warp of the block takes keys u = base + warp, base over the grid in
+// steps of gridDim * warps-per-block (the same trip count in every warp, so
+// the block barriers line up)
+__device__ __forceinline__ void probe_build_all(const Dev& s, const Call& c, const P2P& m, int U, unsigned* bc,
+                                                int* dpop, unsigned long long* sb) {
+  __shared__ int s_cnt[P2P_MAX_WORLD], s_base[P2P_MAX_WORLD];
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  if (threadIdx.x < P2P_MAX_WORLD) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int base = blockIdx.x * wpb; base < U; base += gridDim.x * wpb) {
+    const int u = base + (threadIdx.x >> 5);
+    PBKey k{};
+    k.o = -1;
+    if (u < U) k = probe_build_a(s, c, m, u, lane, bc, dpop, s_cnt);
+    __syncthreads();
+    if (threadIdx.x < m.N) {
+      s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(&m.lcnt[threadIdx.x], s_cnt[threadIdx.x]) : 0;
+      s_cnt[threadIdx.x] = 0;
     }
-    if (dirty)
-      warp_copy_row(reinterpret_cast<float4*>(reqrow(m, o, m.rank, j)),
-                    reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D), D4, lane);
+    __syncthreads();
+    if (u < U) probe_build_b(s, c, m, u, lane, k, s_base, sb);
   }
 }
 
-__device__ __forceinline__ void probe_build_flush(const Dev& s, unsigned* bc, int* dpop, unsigned long long* sb,
-                                                  int U) {
+__device__ __forceinline__ void probe_build_flush(const Dev& s, const Call& c, unsigned* bc, int* dpop,
+                                                  unsigned long long* sb, int U) {
   dpop_flush(s, dpop);
   bytes_flush(s, sb);
   if (threadIdx.x == 0) {
     if (bc[0]) atomicAdd(&s.cnt[C_HITS], (unsigned long long)bc[0]);
     if (bc[1]) atomicAdd(&s.cnt[C_EXP1], (unsigned long long)bc[1]);
     if (bc[3]) atomicAdd(&s.cnt[C_MISSES], (unsigned long long)bc[3]);
-    if (blockIdx.x == 0 && !s.ctl->abort) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+    if (c.rmode) {   // heads of this block: hits + exp1 + misses + clock-checked (finished at install)
+      const unsigned nu = bc[0] + bc[1] + bc[2] + bc[3];
+      if (nu) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)nu);
+    } else if (blockIdx.x == 0 && !s.ctl->abort) {
+      atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+    }
   }
 }
 
@@ -555,13 +619,11 @@ k_probe_build(Dev s, Call c, P2P m) {
   bytes_init(sb);
   __syncthreads();
   Ctl* ctl = s.ctl;
-  const int lane = threadIdx.x & 31;
-  const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const unsigned long long ep = *m.epoch + 1;
-  const int U = ctl->abort ? 0 : ctl->U;
-  if (u < U) probe_build_key(s, c, m, u, lane, bc, dpop, sb);
+  const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);
+  probe_build_all(s, c, m, U, bc, dpop, sb);
   __syncthreads();
-  probe_build_flush(s, bc, dpop, sb, U);
+  probe_build_flush(s, c, bc, dpop, sb, U);
   PTL(1);
   if (!last_block(&m.done[0])) return;
   publish_requests(m, ep);
@@ -580,10 +642,11 @@ __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, 
   Ctl* ctl = s.ctl;
   const int D4 = s.D >> 2;
   uint8_t st = c.status[u];
+  if (st == ST_SKIP) return;   // rmode: not a key's first sorted position
   int32_t e = c.uentry[u];
   const int64_t key = c.uniq[u];
-  const int j0 = c.seg_off[u], j1 = c.seg_off[u + 1];
-  const int cnt = j1 - j0;
+  const int j0 = c.rmode ? u : c.seg_off[u];
+  const int cnt = c.rmode ? c.ucnt[u] : c.seg_off[u + 1] - j0;
   const int pos_lane = lane < cnt ? c.perm[j0 + lane] : 0;
   bool ok = true;
   if (st != ST_HIT) {
@@ -676,7 +739,7 @@ k_install_gather(Dev s, Call c, P2P m, float* __restrict__ out) {
   Ctl* ctl = s.ctl;
   const int lane = threadIdx.x & 31;
   const int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int U = (s_ok && !ctl->abort) ? ctl->U : 0;
+  const int U = (s_ok && !ctl->abort) ? (c.rmode ? c.n : ctl->U) : 0;
   if (u < U) install_gather_key(s, c, m, u, lane, out, bc, dpop, sb);
   __syncthreads();
   install_gather_flush(s, bc, dpop, sb);
@@ -685,11 +748,13 @@ k_install_gather(Dev s, Call c, P2P m, float* __restrict__ out) {
 }
 
 // ---------------------------------------------------------------- the whole round, one cooperative kernel
+constexpr int EX_THREADS = 1024;   // 32 warps per SM: a WDL-sized batch's keys in one pass per phase
 // One block per SM (so concurrent NCCL kernels always find room: no
 // cross-GPU resource cycle), grid syncs between the phases instead of kernel
 // boundaries.  Every block reaches every grid sync (no early returns).
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(EX_THREADS)
 k_exchange(Dev s, Call c, P2P m, float* __restrict__ out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: launched while the dedup runs
   cg::grid_group grid = cg::this_grid();
   __shared__ unsigned bc[4];
   __shared__ int dpop[LFU_CB_MAX];
@@ -707,10 +772,10 @@ k_exchange(Dev s, Call c, P2P m, float* __restrict__ out) {
   bytes_init(sb);
   __syncthreads();
   PTL(0);
-  const int U = ctl->abort ? 0 : ctl->U;
-  for (int u = gw; u < U; u += nw) probe_build_key(s, c, m, u, lane, bc, dpop, sb);
+  const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);   // rmode: sorted positions, heads carry the work
+  probe_build_all(s, c, m, U, bc, dpop, sb);
   __syncthreads();
-  probe_build_flush(s, bc, dpop, sb, U);
+  probe_build_flush(s, c, bc, dpop, sb, U);
   PTL(1);
   __threadfence();
   grid.sync();
@@ -759,7 +824,7 @@ k_exchange(Dev s, Call c, P2P m, float* __restrict__ out) {
   if (threadIdx.x == 0) s_ok = wait_flags(respflag(m, m.rank), m.N, ep, ctl);
   __syncthreads();
   PTL(10);
-  const int U2 = (s_ok && !ctl->abort) ? ctl->U : 0;
+  const int U2 = (s_ok && !ctl->abort) ? (c.rmode ? c.n : ctl->U) : 0;
   {
     // the block's misses take one free-stack reservation (one atomic per
     // block instead of one per miss: the Reddit-shaped batches miss ~7K keys)
@@ -1173,14 +1238,18 @@ int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaSt
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    Dev dd = d;
-    Call cc = c;
-    P2P vv = v;
-    float* oo = out;
-    void* args[] = {&dd, &cc, &vv, &oo};
-    if (cudaLaunchCooperativeKernel((void*)k_exchange, dim3(nsm - coop_sm_reserve()), dim3(512), args, 0, st) ==
-        cudaSuccess)
-      return 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nsm - coop_sm_reserve());
+    cfg.blockDim = dim3(EX_THREADS);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // overlaps the dedup's tail
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, k_exchange, d, c, v, out) == cudaSuccess) return 1;
     cudaGetLastError();   // fall through to the split round
   }
   int l = 0;

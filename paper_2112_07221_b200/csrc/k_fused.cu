@@ -379,44 +379,6 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
 }
 
 // ------------------------------------------------------------------ K_look
-// rmode: the key run starting at sorted position r (warp-uniform): false if r
-// is not the first position of its key.  Lane l loads composite r - 1 + l and
-// the batch position of sorted r + l (both coalesced, in one round trip); a
-// run longer than 31 is followed chunk by chunk.
-__device__ __forceinline__ bool key_run(const Call& c, int r, int lane, int64_t* key, int* cnt, int* pos_lane) {
-  const int n = c.n, pb = c.pbits;
-  const int q = r - 1 + lane;
-  const uint64_t w = (q >= 0 && q < n) ? __ldcg(&c.sortbuf0[q]) : ~0ull;
-  const int pl = r + lane < n ? __ldcg(&c.perm[r + lane]) : 0;
-  const uint64_t kl = w >> pb;
-  const uint64_t k = __shfl_sync(0xffffffffu, kl, 1);
-  const uint64_t kp = __shfl_sync(0xffffffffu, kl, 0);
-  if (r > 0 && kp == k) return false;
-  unsigned same = __ballot_sync(0xffffffffu, lane >= 1 && q < n && kl == k) >> 1;   // bit j: sorted r + j
-  int len = __ffs(~same) - 1;                                                       // 1..31
-  if (same == 0x7FFFFFFFu) {
-    len = 31;
-    for (int b = r + 31;; b += 32) {
-      const int qq = b + lane;
-      const bool eq = qq < n && (__ldcg(&c.sortbuf0[qq]) >> pb) == k;
-      const unsigned m = __ballot_sync(0xffffffffu, eq);
-      const int run = __ffs(~m) - 1;   // -1 when all 32 equal
-      if (run < 0) { len += 32; continue; }
-      len += run;
-      break;
-    }
-  }
-  *key = (int64_t)k;
-  *cnt = len;
-  *pos_lane = lane < len ? pl : 0;
-  return true;
-}
-
-// LFU threshold (T, K*) for this step, one CTA (the last block of k_lookup_fused):
-// T = the smallest count whose cumulative population reaches `need`, K* = the
-// needT-th smallest key of count T.  Loads are issued in parallel: the 16
-// populations by 16 lanes, the block counters of bitmap T in chunks of
-// blockDim (coalesced, block-wide prefix), stopping at the chunk holding K*.
 struct Plan {          // an eviction plan (shared memory of the block that derives it)
   int emode;           // 0 none, 1 LFU count bitmaps, 2 generic selection
   int rebuild;         // hash rebuild requested (tombstones > S/8)

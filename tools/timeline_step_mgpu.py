@@ -28,7 +28,7 @@ lib = het.load()
 lib.het_debug_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
 lib.het_debug_timeline_p2p.argtypes = [ctypes.c_void_p]
 TLW, PTW = 8192, 8192
-tl = np.zeros(24 * TLW, np.uint64)
+tl = np.zeros(32 * TLW, np.uint64)
 pt = np.zeros(16 * PTW, np.uint64)
 g = gen.grads(rank, 0, n, D, device=dev)
 dense = gen.dense_grads(rank, 0, 1 << 20, device=dev) if world > 1 and os.environ.get("TL_DENSE", "1") == "1" else None
@@ -47,29 +47,30 @@ graph = c.capture_step(kbuf, g, out, 0.01, dense)
 for j in range(10):
     kbuf.copy_(keys[j]); graph.replay()
 torch.cuda.synchronize()
-names_tl = {0: "dd.start", 4: "dd.end", 8: "lk.start", 10: "lk.work", 16: "up.start", 18: "up.seg", 19: "up.finds", 20: "up.sync", 21: "up.evict"}
+names_tl = {0: "dd.start", 2: "dd.rank", 3: "dd.tail0", 4: "dd.end", 12: "dd.evict", 16: "up.start", 18: "up.seg",
+            26: "plan.kstar", 20: "up.xdone", 19: "up.sync", 21: "up.end"}
 names_pt = {0: "x.start", 1: "x.probe", 2: "x.pub", 4: "x.reqwait", 5: "x.link", 7: "x.proc", 8: "x.resppub",
             10: "x.respwait", 11: "x.end"}
 for j in range(10, 16):
     kbuf.copy_(keys[j])
     torch.cuda.synchronize()
     dist.barrier()
-    lib.het_debug_timeline(None, 24, TLW)
+    lib.het_debug_timeline(None, 32, TLW)
     lib.het_debug_timeline_p2p(None)
     torch.cuda.synchronize()
     dist.barrier()
     graph.replay()
     torch.cuda.synchronize()
-    lib.het_debug_timeline(tl.ctypes.data, 24, TLW)
+    lib.het_debug_timeline(tl.ctypes.data, 32, TLW)
     lib.het_debug_timeline_p2p(pt.ctypes.data)
     if j < 13:
         continue
-    a = tl.reshape(24, TLW).astype(np.float64)
+    a = tl.reshape(32, TLW).astype(np.float64)
     b = pt.reshape(16, PTW).astype(np.float64)
     t0 = a[0][a[0] > 0].min()
     parts = []
-    for nm, arr, m in [(names_tl[k], a, k) for k in (0, 4, 8, 10)] + [(names_pt[k], b, k) for k in sorted(names_pt)] + \
-            [(names_tl[k], a, k) for k in (16, 18, 19, 20, 21)]:
+    for nm, arr, m in [(names_tl[k], a, k) for k in (0, 2, 3, 4, 12)] + [(names_pt[k], b, k) for k in sorted(names_pt)] + \
+            [(names_tl[k], a, k) for k in (16, 18, 26, 20, 19, 21)]:
         x = arr[m][arr[m] > 0]
         if x.size:
             x = (x - t0) / 1000.0
