@@ -352,6 +352,8 @@ static het_status_t create_impl(uint64_t rows, uint32_t D, double cache_frac, ui
     A(c.urec, nm);
     A(c.upos, nm);
     A(c.ucnt, nm);
+    A(c.ucslot, nm);
+    A(c.ucword, nm);
     A(c.dbg_status, nm);
     A(c.dbg_inverse, nm);
     A(c.dbg_U, 1);

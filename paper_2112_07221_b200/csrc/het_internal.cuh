@@ -171,6 +171,8 @@ struct Call {
   int4* urec;                  // [n_max] per unique key, lookup -> update: {entry, j0, cnt | dirty << 31, c_c}
   int4* upos;                  // [n_max] its first four batch positions (ascending)
   int32_t* ucnt;               // [n_max] rmode at N > 1: the key's occurrences (uniq[r] holds the key)
+  uint64_t* ucslot;            // [n_max] N > 1: a miss's hash insert slot from the probe (warp_find_cand)
+  uint64_t* ucword;            // [n_max]         and that slot's word
   uint8_t* dbg_status;         // [n_max] rmode: compacted status (debug export)
   int32_t* dbg_inverse;        // [n_max] rmode: compacted inverse (debug export)
   int32_t* dbg_U;              // rmode: unique keys of the compacted log

@@ -134,23 +134,29 @@ __global__ void k_p2p_build(Dev s, Call c, P2P m, int drain) {
 // Link every received record into its row's list (grid-stride); tot[src] =
 // records from src this round.
 __device__ __forceinline__ void link_records(const P2P& m, const int32_t* tot) {
+  int64_t all = 0;                        // every source's records as one index space: one pass
+  for (int src = 0; src < m.N; ++src) all += tot[src];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int src = 0; src < m.N; ++src) {
-    const Rec* rr = reqrec(m, m.rank, src);
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot[src]; j += stride) {
-      const int64_t row = rr[j].key / m.N;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g - threadIdx.x % 32 < all; g += stride) {
+    bool live = g < all;
+    int src = 0;
+    int64_t j = g;
+    while (live && src < m.N - 1 && j >= tot[src]) { j -= tot[src]; ++src; }
+    int64_t row = 0;
+    int32_t old = 0;
+    if (live) {
+      row = reqrec(m, m.rank, src)[j].key / m.N;
       const int32_t id = (int32_t)(src * m.CAPS + j);
-      const int32_t old = atomicExch(&m.head[row], id);
+      old = atomicExch(&m.head[row], id);
       m.next[id] = old;
-      // first record of a row: append the row to the leader list (one atomic per warp)
-      const unsigned am = __activemask();
-      const unsigned lm = __ballot_sync(am, old < 0);
-      const int lead = __ffs(am) - 1, lane = threadIdx.x & 31;
-      int b = 0;
-      if (lane == lead && lm) b = atomicAdd(m.nlead, __popc(lm));
-      b = __shfl_sync(am, b, lead);
-      if (old < 0) m.leaders[b + __popc(lm & ((1u << lane) - 1))] = id;
     }
+    // first record of a row: append the ROW to the leader list (one atomic per warp)
+    const unsigned lm = __ballot_sync(0xffffffffu, live && old < 0);
+    const int lane = threadIdx.x & 31;
+    int b = 0;
+    if (lane == 0 && lm) b = atomicAdd(m.nlead, __popc(lm));
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (live && old < 0) m.leaders[b + __popc(lm & ((1u << lane) - 1))] = (int32_t)row;
   }
 }
 
@@ -185,24 +191,32 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
   const int D4 = s.D >> 2;
   const Rec* base = reqrec(m, m.rank, 0);
   for (int li = gw; li < nl; li += nw) {
-    const int64_t row = base[m.leaders[li]].key / m.N;
+    const int64_t row = m.leaders[li];
+    // the row's server row and c_g do not depend on the list: load them first
+    uint32_t g0 = 0;
+    if (lane == 0) g0 = s.cg[row];
+    const float4 wpre = lane < D4 ? reinterpret_cast<const float4*>(s.W + row * s.D)[lane]
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);   // the first 128 columns
     // walk the row's list once (lane 0), sort by id = (source rank, pushes
-    // before requests), hand record i to lane i
+    // before requests) across the lanes, hand record i to lane i
     int cnt = 0;
     if (lane == 0) {
       int32_t cur = m.head[row];
-      int32_t buf[32];
-      while (cur >= 0 && cnt < 32) { buf[cnt++] = cur; cur = m.next[cur]; }
+      while (cur >= 0 && cnt < 32) { wbuf[wi][cnt++] = cur; cur = m.next[cur]; }
       m.head[row] = -1;
-      for (int a = 1; a < cnt; ++a) {         // insertion sort (tiny)
-        int32_t x = buf[a]; int k = a - 1;
-        while (k >= 0 && buf[k] > x) { buf[k + 1] = buf[k]; --k; }
-        buf[k + 1] = x;
-      }
-      for (int a = 0; a < cnt; ++a) wbuf[wi][a] = buf[a];
     }
     __syncwarp();
     cnt = __shfl_sync(0xffffffffu, cnt, 0);
+    g0 = __shfl_sync(0xffffffffu, g0, 0);
+    {
+      const int32_t mine = lane < cnt ? wbuf[wi][lane] : 0x7FFFFFFF;
+      int rank = 0;
+      for (int k = 0; k < cnt; ++k) rank += __shfl_sync(0xffffffffu, mine, k) < mine;
+      __syncwarp();
+      if (lane < cnt) wbuf[wi][rank] = mine;
+      __syncwarp();
+    }
+    PTL(12);
     const bool have = lane < cnt;
     const int32_t id = have ? wbuf[wi][lane] : 0;
     const int src = id / (int)m.CAPS;
@@ -210,7 +224,6 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
     Rec r{};
     bool push = false;
     if (have) { r = base[id]; push = j < m.qpush[src]; }
-    const uint32_t g0 = s.cg[row];
     // U4(t-1): eviction pushes raise c_g (max is order-free); L3: condition (2)
     // for clock-checked hits against c_g after them; L4: sync pushes of the
     // requests that are not valid hits
@@ -248,6 +261,7 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
       reinterpret_cast<uint32_t*>(rec_l)[0] = g;
       reinterpret_cast<uint32_t*>(rec_l)[1] = valid ? 1u : 0u;
     }
+    PTL(13);
     // row data, lane per float4, records in sorted order: pushes, then sync pushes
     const unsigned needrow = (pushm | syncm);
     const unsigned answer = __ballot_sync(0xffffffffu, req && !valid);
@@ -255,7 +269,8 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
     for (int d0 = lane; d0 - lane < D4; d0 += 32 * RB) {   // RB columns per lane per pass (wide rows)
       float4 w[RB];
 #pragma unroll
-      for (int b = 0; b < RB; ++b) w[b] = d0 + 32 * b < D4 ? Wr[d0 + 32 * b] : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int b = 0; b < RB; ++b)
+        w[b] = (d0 == lane && b == 0) ? wpre : (d0 + 32 * b < D4 ? Wr[d0 + 32 * b] : make_float4(0.f, 0.f, 0.f, 0.f));
       for (int pass = 0; pass < 2; ++pass) {
         unsigned mm = pass == 0 ? pushm : syncm;
         while (mm) {
@@ -285,6 +300,7 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
           if (d0 + 32 * b < D4) reinterpret_cast<float4*>(rec + 4)[d0 + 32 * b] = w[b];
       }
     }
+    PTL(14);
     __syncwarp();
   }
 }
@@ -470,7 +486,7 @@ struct PBKey {            // phase A -> phase B (warp-uniform)
 };
 
 __device__ __forceinline__ PBKey probe_build_a(const Dev& s, const Call& c, const P2P& m, int u, int lane,
-                                               unsigned* bc, int* dpop, int* s_cnt) {
+                                               unsigned* bc, int* dpop, int* s_cnt, float* __restrict__ out) {
   Ctl* ctl = s.ctl;
   PBKey k{};
   k.o = -1;
@@ -491,9 +507,11 @@ __device__ __forceinline__ PBKey probe_build_a(const Dev& s, const Call& c, cons
   }
   uint32_t cntk = 0;
   if (lane == 0 && s.lfu_persist) cntk = s.count_by_key[key];
-  const int32_t e = warp_find(s, key, lane);
+  uint64_t cslot = ~0ull, cword = 0;
+  const int32_t e = warp_find_cand(s, key, lane, &cslot, &cword);
   uint32_t ecs = 0, ecc = 0;
   if (e >= 0) { ecs = s.cs[e]; ecc = s.cc[e]; }
+  else if (lane == 0) { c.ucslot[u] = cslot; c.ucword[u] = cword; }   // the install's CAS slot
   uint8_t st = ST_MISS;
   if (lane == 0) {
     const uint32_t oldc = (e >= 0 && s.policy == 0) ? s.eprim[e] : 0u;
@@ -523,6 +541,24 @@ __device__ __forceinline__ PBKey probe_build_a(const Dev& s, const Call& c, cons
   write_urec(c, u, e, j0, cnt, ecc > ecs, ecc, pos_lane, lane);   // resident: a hit keeps it, a refetch rewrites it
   if (c.rmode && lane == 0) { c.uniq[u] = key; c.ucnt[u] = cnt; }   // for the install phase
   k.key = key; k.e = e; k.ecc = ecc; k.st = st;
+  if (st == ST_HIT || st == ST_NEEDQ) {
+    // Cache.Get now: a hit's row, and a clock-checked hit's row (the
+    // install overwrites the occurrences of the rare one condition (2) refuses)
+    const int D4 = s.D >> 2;
+    const float4* vr = reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    for (int d = lane; d - lane < D4; d += 32) {
+      const float4 val = d < D4 ? vr[d] : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int kb = 0; kb < cnt; kb += 32) {
+        const int srcp = kb == 0 ? pos_lane : (kb + lane < cnt ? c.perm[j0 + kb + lane] : 0);
+        const int mm = min(32, cnt - kb);
+        for (int q = 0; q < mm; ++q) {
+          const int pos = __shfl_sync(0xffffffffu, srcp, q);
+          if (d < D4) __stcs(o4 + (int64_t)pos * D4 + d, val);
+        }
+      }
+    }
+  }
   if (st != ST_HIT) {
     k.o = (int)(key % m.N);
     k.dirty = e >= 0 && ecc > ecs;
@@ -557,7 +593,7 @@ __device__ __forceinline__ void probe_build_b(const Dev& s, const Call& c, const
 // steps of gridDim * warps-per-block (the same trip count in every warp, so
 // the block barriers line up)
 __device__ __forceinline__ void probe_build_all(const Dev& s, const Call& c, const P2P& m, int U, unsigned* bc,
-                                                int* dpop, unsigned long long* sb) {
+                                                int* dpop, unsigned long long* sb, float* __restrict__ out) {
   __shared__ int s_cnt[P2P_MAX_WORLD], s_base[P2P_MAX_WORLD];
   const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
   if (threadIdx.x < P2P_MAX_WORLD) s_cnt[threadIdx.x] = 0;
@@ -566,7 +602,7 @@ __device__ __forceinline__ void probe_build_all(const Dev& s, const Call& c, con
     const int u = base + (threadIdx.x >> 5);
     PBKey k{};
     k.o = -1;
-    if (u < U) k = probe_build_a(s, c, m, u, lane, bc, dpop, s_cnt);
+    if (u < U) k = probe_build_a(s, c, m, u, lane, bc, dpop, s_cnt, out);
     __syncthreads();
     if (threadIdx.x < m.N) {
       s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(&m.lcnt[threadIdx.x], s_cnt[threadIdx.x]) : 0;
@@ -609,7 +645,7 @@ __device__ __forceinline__ void publish_requests(const P2P& m, unsigned long lon
 }
 
 __global__ void __launch_bounds__(256)
-k_probe_build(Dev s, Call c, P2P m) {
+k_probe_build(Dev s, Call c, P2P m, float* __restrict__ out) {
   __shared__ unsigned bc[4];
   __shared__ int dpop[LFU_CB_MAX];
   __shared__ unsigned long long sb[4];
@@ -621,7 +657,7 @@ k_probe_build(Dev s, Call c, P2P m) {
   Ctl* ctl = s.ctl;
   const unsigned long long ep = *m.epoch + 1;
   const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);
-  probe_build_all(s, c, m, U, bc, dpop, sb);
+  probe_build_all(s, c, m, U, bc, dpop, sb, out);
   __syncthreads();
   probe_build_flush(s, c, bc, dpop, sb, U);
   PTL(1);
@@ -673,7 +709,7 @@ __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, 
           ok = false;
         } else {
           e = s.fstack[idx];
-          warp_insert(s, key, e, lane);
+          warp_insert_at(s, key, e, lane, c.ucslot[u], c.ucword[u]);
           if (lane == 0) {
             s.ekey[e] = key;
             const uint32_t prim = s.policy == 0 ? (s.lfu_persist ? s.count_by_key[key] : 1u) : (uint32_t)ctl->t_cur;
@@ -692,7 +728,10 @@ __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, 
       }
     }
   }
-  if (ok && e >= 0) {
+  bool fresh = st != ST_HIT;   // the probe already scattered hits and clock-checked hits condition (2) kept
+  if (st == ST_NEEDQ) fresh = reinterpret_cast<const uint32_t*>(
+                                  resprec(m, m.rank, m.uslot[u] / (int)m.CAPS, m.uslot[u] % (int)m.CAPS))[1] == 0;
+  if (ok && e >= 0 && fresh) {
     const float4* vr = reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D);
     float4* o4 = reinterpret_cast<float4*>(out);
     for (int d0 = lane; d0 - lane < D4; d0 += 32 * RB) {
@@ -773,7 +812,7 @@ k_exchange(Dev s, Call c, P2P m, float* __restrict__ out) {
   __syncthreads();
   PTL(0);
   const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);   // rmode: sorted positions, heads carry the work
-  probe_build_all(s, c, m, U, bc, dpop, sb);
+  probe_build_all(s, c, m, U, bc, dpop, sb, out);
   __syncthreads();
   probe_build_flush(s, c, bc, dpop, sb, U);
   PTL(1);
@@ -1223,7 +1262,7 @@ int p2p_lookup_phase(P2PState* p, const Dev& d, const Call& c, float* out, int p
   P2P& v = p->v;   // lcnt is zero here: the previous round's publish reset it
   const int blocks = std::max(1, (c.n + 7) / 8);
   switch (phase) {
-    case RP_BUILD: k_probe_build<<<blocks, 256, 0, st>>>(d, c, v); return 1;
+    case RP_BUILD: k_probe_build<<<blocks, 256, 0, st>>>(d, c, v, out); return 1;
     case RP_LINK: k_p2p_link<<<148, 256, 0, st>>>(d, v); return 1;
     case RP_PROCESS: k_p2p_process<<<148 * 2, 256, 0, st>>>(d, v); return 1;
     default: k_install_gather<<<blocks, 256, 0, st>>>(d, c, v, out); return 1;

@@ -49,8 +49,8 @@ for j in range(10):
 torch.cuda.synchronize()
 names_tl = {0: "dd.start", 2: "dd.rank", 3: "dd.tail0", 4: "dd.end", 12: "dd.evict", 16: "up.start", 18: "up.seg",
             26: "plan.kstar", 20: "up.xdone", 19: "up.sync", 21: "up.end"}
-names_pt = {0: "x.start", 1: "x.probe", 2: "x.pub", 4: "x.reqwait", 5: "x.link", 7: "x.proc", 8: "x.resppub",
-            10: "x.respwait", 11: "x.end"}
+names_pt = {0: "x.start", 1: "x.probe", 2: "x.pub", 4: "x.reqwait", 5: "x.link", 12: "p.list", 13: "p.clock",
+            14: "p.rows", 7: "x.proc", 8: "x.resppub", 10: "x.respwait", 11: "x.end"}
 for j in range(10, 16):
     kbuf.copy_(keys[j])
     torch.cuda.synchronize()
