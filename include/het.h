@@ -128,6 +128,19 @@ het_status_t het_cache_create(uint64_t rows, uint32_t D, double cache_frac, uint
 het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t clock_t,
                         float* out, het_stream_t stream);
 
+/* Message fusion's prefetch (NEXT-1; "pre-fetch the next mini-batch
+ * of data in advance"): run the dedup of the NEXT het_lookup's keys now -- for
+ * example on a side stream while the dense backward and het_update of this
+ * step run.  The next het_lookup with the same `keys` pointer and `n` skips its
+ * own dedup; any other next lookup ignores the prefetch.  The dedup is a
+ * function of the keys alone, so every result is unchanged; a key outside
+ * [0, rows) is reported by that lookup (sticky HET_ERR_KEY_RANGE).  The
+ * caller orders the lookup after the prefetch (same stream or an event) and
+ * keeps `keys` unchanged in between.  A no-op on paths without a separate
+ * dedup kernel (n > 16384, HET_NO_FUSED).  Local: allowed on loopback
+ * members and at N > 1 without the other ranks. */
+het_status_t het_prefetch(het_cache_t h, const int64_t* keys, uint32_t n, het_stream_t stream);
+
 /* Het.Write (Alg. 3) for the keys of the immediately preceding
  * het_lookup (a write of keys the read did not return is a
  * protocol violation).  n != the lookup's n: HET_ERR_PROTOCOL, returned at

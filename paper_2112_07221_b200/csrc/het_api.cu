@@ -56,6 +56,7 @@ struct het_cache {
   int64_t* victim_sel = nullptr;
   // staging for host pointers (allocated on first use)
   int64_t* stage_keys = nullptr;
+  int64_t* stage_pref = nullptr;   // het_prefetch's host keys
   float* stage_rows = nullptr;
   float* stage_out = nullptr;
   // protocol state
@@ -67,6 +68,12 @@ struct het_cache {
   bool ev_pending = false;     // a fused update may have left listed victims (evicted by the next call's first kernel)
   bool ev_captured = false;    // a fused update was captured into a CUDA graph (replays leave victims listed)
   std::shared_ptr<het_group> group;    // loopback member (nullptr: one process per GPU)
+  // het_prefetch (NEXT-1): the next lookup's dedup, run ahead into the
+  // alternate sort/perm buffers
+  uint64_t* sb_alt = nullptr;
+  int32_t* perm_alt = nullptr;
+  const int64_t* pref_keys = nullptr;  // as the caller passed them (nullptr: nothing prefetched)
+  uint32_t pref_n = 0;
   int64_t overflow_bound = 0;  // worst-case residents above C since the last eviction
   uint64_t lookups = 0, keys = 0, updates = 0, launches = 0;
   // multi-GPU
@@ -353,6 +360,9 @@ static het_status_t create_impl(uint64_t rows, uint32_t D, double cache_frac, ui
     A(c.upos, nm);
     A(c.ucnt, nm);
     A(c.ucslot, nm);
+    A(c.pref_bad, 1);
+    A(h->sb_alt, nm);
+    A(h->perm_alt, nm);
     A(c.ucword, nm);
     A(c.dbg_status, nm);
     A(c.dbg_inverse, nm);
@@ -540,17 +550,25 @@ static het_status_t lookup_pre(het_cache* h, const int64_t* keys, uint32_t n, ui
   // per-phase kernels with the sliced heavy-key segment reduce), N > 1 over
   // the peer-memory exchange for every n; the dedup kernel follows n
   h->fused = !h->no_fused && (d.world == 1 ? (int)n <= FUSED_LOOKUP_MAX : mgpu_p2p(h->mg) != nullptr);
-  // after the fused dedup: per-key work indexed by sorted position (no compaction pass, R29)
-  c.rmode = (h->fused && fused_ok(d, (int)n)) ? 1 : 0;
-  if (h->fused && fused_ok(d, (int)n)) {   // the dedup kernel also runs the deferred eviction
+  // after the fused dedups: per-key work indexed by sorted position (no compaction pass, R29)
+  c.rmode = (h->fused && (int)n <= RMODE_MAX) ? 1 : 0;
+  const bool pref = c.rmode && h->pref_keys && ukeys == h->pref_keys && n == h->pref_n;
+  h->pref_keys = nullptr;   // consumed, or not the keys it was for
+  if (c.rmode) {   // the dedup kernel also runs the deferred eviction
     // a captured graph replays after its own update: keep the eviction blocks
     // (they test the device flag and return when nothing is listed)
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cap);
     const bool ev = h->ev_pending || cap == cudaStreamCaptureStatusActive;
     Prof p(h, "dedup", st);
-    h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st, h->evbuf_host, p2p_view(h), ev,
-                                   c.rmode ? 0 : 1);
+    if (pref) {   // het_prefetch ran this dedup: take its buffers, begin + evict only
+      std::swap(c.sortbuf0, h->sb_alt);
+      std::swap(c.perm, h->perm_alt);
+      h->launches += launch_begin_evict(d, c, (int)n, clock_t, st, h->evbuf_host, p2p_view(h), ev);
+    } else if (fused_ok(d, (int)n))
+      h->launches += launch_dd_fused(d, c, (int)n, h->pbits, clock_t, 1, st, h->evbuf_host, p2p_view(h), ev, 0);
+    else
+      h->launches += launch_dd_bucket(d, c, (int)n, h->pbits, clock_t, 1, st, h->evbuf_host, p2p_view(h), ev);
     h->ev_pending = false;
   } else {
     flush_evict(h, st);
@@ -631,6 +649,41 @@ static het_status_t lookup_post(het_cache* h, LkCtx& x, cudaStream_t st) {
   h->have_lookup = true;
   h->last_n = n;
   h->overflow_bound += n;
+  return HET_OK;
+}
+
+// NEXT-1 ("pre-fetch the next mini-batch of data in advance"): the
+// dedup of the next lookup's keys, enqueued now (e.g. on a side stream while
+// the dense backward and het_update run) into the alternate buffers; the next
+// het_lookup with the same pointer and n skips its dedup.  The dedup is a
+// function of the keys alone, so results are unchanged.
+het_status_t het_prefetch(het_cache_t h, const int64_t* keys, uint32_t n, het_stream_t stream_) {
+  cudaStream_t st = (cudaStream_t)stream_;
+  if (!h) return HET_ERR_ARG;
+  if (n > h->n_max) return fail(h, HET_ERR_CAPACITY, "n exceeds max_keys_per_call");
+  if (n && !keys) return fail(h, HET_ERR_ARG, "null keys");
+  h->pref_keys = nullptr;
+  if (h->no_fused || n == 0 || (int)n > RMODE_MAX) return HET_OK;   // nothing to run ahead on this path
+  const int64_t* dkeys = keys;
+  if (!is_device_ptr(keys)) {
+    if (!h->stage_pref) CUDA_TRY(h, (dalloc(h, &h->stage_pref, h->n_max)));
+    CUDA_TRY(h, cudaMemcpyAsync(h->stage_pref, keys, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    dkeys = h->stage_pref;
+  }
+  Call pc = h->call;   // the alternate buffers; nothing else of the call is written
+  pc.keys = dkeys;
+  pc.n = (int)n;
+  pc.sortbuf0 = h->sb_alt;
+  pc.perm = h->perm_alt;
+  pc.rmode = 1;
+  Dev& d = h->d;
+  if (fused_ok(d, (int)n))
+    h->launches += launch_dd_fused(d, pc, (int)n, h->pbits, 0, 2, st, h->evbuf_host, p2p_view(h), false, 0);
+  else
+    h->launches += launch_dd_bucket(d, pc, (int)n, h->pbits, 0, 2, st, h->evbuf_host, p2p_view(h), false);
+  CUDA_TRY(h, cudaGetLastError());
+  h->pref_keys = keys;
+  h->pref_n = n;
   return HET_OK;
 }
 

@@ -16,7 +16,18 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <cassert>
+
 namespace het {
+
+// Bounds-checked builds (HET_DIAG=HET_BOUNDS): device asserts on the indices
+// the hot kernels compute -- free-stack slots, entries, inbox slots, sort
+// positions (compute-sanitizer is not available on the GPU pool).
+#ifdef HET_BOUNDS
+#define HET_ASSERT(c) assert(c)
+#else
+#define HET_ASSERT(c) do {} while (0)
+#endif
 
 constexpr uint32_t S_INF = 0xFFFFFFFFu;
 // hash slot word: key << 32 | entry (entry >= 0); EMPTY ends a probe, TOMB does not
@@ -171,6 +182,7 @@ struct Call {
   int4* urec;                  // [n_max] per unique key, lookup -> update: {entry, j0, cnt | dirty << 31, c_c}
   int4* upos;                  // [n_max] its first four batch positions (ascending)
   int32_t* ucnt;               // [n_max] rmode at N > 1: the key's occurrences (uniq[r] holds the key)
+  int32_t* pref_bad;           // het_prefetch: 1 when the prefetched keys held one outside [0, R)
   uint64_t* ucslot;            // [n_max] N > 1: a miss's hash insert slot from the probe (warp_find_cand)
   uint64_t* ucword;            // [n_max]         and that slot's word
   uint8_t* dbg_status;         // [n_max] rmode: compacted status (debug export)
@@ -212,7 +224,11 @@ __device__ __forceinline__ int32_t warp_find(const Dev& s, int64_t key, int lane
     uint64_t slot = (w + lane) & s.hmask;
     const uint64_t hw = s.hslot[slot];
     unsigned m = __ballot_sync(0xffffffffu, hs_is(hw, key));
-    if (m) return __shfl_sync(0xffffffffu, hs_val(hw), __ffs(m) - 1);
+    if (m) {
+      const int32_t e = __shfl_sync(0xffffffffu, hs_val(hw), __ffs(m) - 1);
+      HET_ASSERT(e >= 0 && e < s.Ecap);
+      return e;
+    }
     if (__ballot_sync(0xffffffffu, hw == HS_EMPTY)) return -1;
     w = (w + 32) & s.hmask;
   }
@@ -499,12 +515,21 @@ constexpr int FUSED_LOOKUP_MAX = 16384;   // N = 1: fused lookup/update up to th
 // they are evicted by extra blocks of the same kernel; evbuf: EvBuf;
 // p2pview: the exchange view at N > 1 (PUSH records), else nullptr
 // compact: 1 writes unique/seg_off/U (rmode 0), 0 leaves the sorted
-// composites for the rmode lookup (no serial tail)
+// composites for the rmode lookup (no serial tail).  lookup: 1 a lookup's
+// dedup (the per-call begin), 0 an evict's, 2 het_prefetch's (no side effect
+// on the cache state: only the sorted composites, perm and c.pref_bad)
 int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st,
                     void* evbuf, const void* p2pview, bool evict, int compact);
 // rmode: the compact lookup log (uniq, seg_off, dbg_status, dbg_inverse, dbg_U) for the debug export
 void launch_compact_log(const Dev& s, const Call& c, cudaStream_t st);
 int launch_evict_pending(const Dev& s, void* evbuf, const void* p2pview, cudaStream_t st);
+// a lookup whose dedup het_prefetch already ran: the per-call begin (+ the deferred eviction)
+int launch_begin_evict(const Dev& s, const Call& c, int n, uint64_t t, cudaStream_t st, void* evbuf,
+                       const void* p2pview, bool evict);
+// rmode dedup for 8192 < n <= 16384: one CTA, bucketed exact rank (+ the deferred eviction)
+int launch_dd_bucket(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st,
+                     void* evbuf, const void* p2pview, bool evict);
+constexpr int RMODE_MAX = 16384;   // rmode dedups serve n <= this
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st);
 // SMs left free by the cooperative kernels for NCCL's blocks at N > 1
 // (= NCCL's maxCTAs and the peer-memory dense all-reduce grid; env HET_NCCL_CTAS, default 16)

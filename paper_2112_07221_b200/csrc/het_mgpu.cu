@@ -315,7 +315,9 @@ __global__ void k_install(Dev s, Call c, MgpuState m_) {
           if (lane == 0) raise_err(ctl, 4);
           continue;
         }
+        HET_ASSERT(idx >= 0 && idx < s.Ecap);
         e = s.fstack[idx];
+        HET_ASSERT(e >= 0 && e < s.Ecap);
         warp_insert(s, key, e, lane);
         if (lane == 0) {
           s.ekey[e] = key;

@@ -369,7 +369,9 @@ __global__ void k_p2p_install(Dev s, Call c, P2P m) {
             if (lane == 0) raise_err(ctl, 4);
             continue;
           }
+          HET_ASSERT(idx >= 0 && idx < s.Ecap);
           e = s.fstack[idx];
+          HET_ASSERT(e >= 0 && e < s.Ecap);
           warp_insert(s, key, e, lane);
           if (lane == 0) {
             s.ekey[e] = key;
@@ -579,6 +581,7 @@ __device__ __forceinline__ void probe_build_b(const Dev& s, const Call& c, const
     Rec r;
     r.key = k.key; r.cc = k.ecc;
     r.kind = (k.st == ST_NEEDQ ? K_NEEDQ : k.st == ST_EXP1 ? K_EXP1 : K_MISS) | (k.dirty ? K_DIRTY : 0);
+    HET_ASSERT(j >= 0 && j < m.CAPS);
     reqrec(m, k.o, m.rank)[j] = r;
     m.uslot[u] = (int32_t)(k.o * m.CAPS + slot);
     atomicAdd(&sb[k.st == ST_NEEDQ ? 0 : 2], 16ull);
@@ -708,7 +711,9 @@ __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, 
           if (lane == 0) raise_err(ctl, 4);
           ok = false;
         } else {
+          HET_ASSERT(idx >= 0 && idx < s.Ecap);
           e = s.fstack[idx];
+          HET_ASSERT(e >= 0 && e < s.Ecap);
           warp_insert_at(s, key, e, lane, c.ucslot[u], c.ucword[u]);
           if (lane == 0) {
             s.ekey[e] = key;

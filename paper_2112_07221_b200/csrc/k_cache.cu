@@ -214,7 +214,9 @@ k_sync_fetch_local(Dev s, Call c) {
         if (lane == 0) raise_err(ctl, 4 /*HET_ERR_CAPACITY*/);
         ok = false;
       } else {
+        HET_ASSERT(idx >= 0 && idx < s.Ecap);
         e = s.fstack[idx];
+        HET_ASSERT(e >= 0 && e < s.Ecap);
         warp_insert(s, key, e, lane);
         g = s.cg[row];
         if (lane == 0) {

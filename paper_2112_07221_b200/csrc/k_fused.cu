@@ -222,7 +222,10 @@ __device__ __forceinline__ void dd_rank_rmode(const int64_t* __restrict__ keys, 
   bad = __syncthreads_or(bad);
   TL_MAX(1);
   if (!bad && lookup) prefetch_lookup_lines(s, kq, n);
-  if (blockIdx.x == 0 && threadIdx.x == 0) dd_begin(s, c, n, t, lookup, bad, 0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (lookup == 2) *c.pref_bad = bad;   // het_prefetch: the consuming lookup raises it
+    else dd_begin(s, c, n, t, lookup, bad, 0);
+  }
   if (bad) return;
   TL_MAX(3);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -253,6 +256,7 @@ __device__ __forceinline__ void dd_rank_rmode(const int64_t* __restrict__ keys, 
     int r = 0;
 #pragma unroll
     for (int w = 0; w < DDF_WARPS; ++w) r += part[w][lane];
+    HET_ASSERT(r >= 0 && r < n);
     c.sortbuf0[r] = ((uint64_t)mine << pbits) | (uint64_t)p;
     c.perm[r] = p;                 // stable position grouping
   }
@@ -621,7 +625,9 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
           if (lane == 0) raise_err(ctl, 4 /*HET_ERR_CAPACITY*/);
           e = -1;
         } else {
+          HET_ASSERT(idx >= 0 && idx < s.Ecap);
           e = s.fstack[idx];
+          HET_ASSERT(e >= 0 && e < s.Ecap);
           TL_MAX(29);
           warp_insert_at(s, key, e, lane, cslot, cword);
           TL_MAX(30);
@@ -786,7 +792,9 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
           if (lane == 0) raise_err(ctl, 4 /*HET_ERR_CAPACITY*/);
           e = -1;
         } else {
+          HET_ASSERT(idx >= 0 && idx < s.Ecap);
           e = s.fstack[idx];
+          HET_ASSERT(e >= 0 && e < s.Ecap);
           warp_insert(s, key, e, lane);
           if (lane == 0) {
             s.ekey[e] = key;
@@ -888,6 +896,7 @@ __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_
     unpin_count(s, prim);
     s.eprim[e] = EP_FREE;
     s.ekey[e] = -1;
+    HET_ASSERT(fpos >= 0 && fpos < s.Ecap && e >= 0 && e < s.Ecap);
     s.fstack[fpos] = e;
     atomicAdd(s_ev, 1u);
     if (dirty) atomicAdd(s_dirty, 1u);
@@ -1407,13 +1416,134 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   }
 }
 
+// ------------------------------------------------------------------ K1 for 8192 < n <= 16384 (rmode)
+// One CTA ranks every occurrence by a counting sort over 4096 key buckets
+// (the top 12 bits of the key range: the keys are permuted ids, R15) and an
+// exact rank inside each bucket: r(p) = offset(bucket) + #{q in the bucket:
+// key_q < key_p, or key_q = key_p and q < p} -- the same stable sort as the
+// rank count (R2), with n^2/4096 compares instead of n^2 (the Reddit-shaped
+// batches: 14,208 distinct ids).  Extra blocks run the deferred eviction as
+// in k_dd_fused.
+constexpr int BK_THREADS = 1024, BK_BITS = 12, BK_N = 1 << BK_BITS, BK_MAX = 16384;
+constexpr int EV_BLOCKS = 32;   // blocks of the deferred eviction beside the dedup
+__global__ void __launch_bounds__(BK_THREADS)
+k_dd_bucket(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, uint64_t t, int lookup, EvBuf eb,
+            P2P pm, int push) {
+  pdl_trigger();
+  if (blockIdx.x > 0) {
+    evict_listed(s, eb, push ? &pm : nullptr, blockIdx.x - 1, gridDim.x - 1);
+    return;
+  }
+  extern __shared__ __align__(16) uint32_t bk[];
+  uint32_t* skey = bk;                 // [n]   the keys (32-bit)
+  uint32_t* sord = bk + BK_MAX;        // [n]   positions grouped by bucket
+  uint32_t* soff = bk + 2 * BK_MAX;    // [BK_N] bucket offsets
+  uint32_t* scur = soff + BK_N;        // [BK_N] counts, then scatter cursors
+  __shared__ int warp_sums[32];
+  const int sh = max(0, s.kbits - BK_BITS);
+  for (int b = threadIdx.x; b < BK_N; b += BK_THREADS) scur[b] = 0;
+  __syncthreads();
+  int bad = 0;
+  for (int q = threadIdx.x; q < n; q += BK_THREADS) {
+    const int64_t k = __ldg(&keys[q]);
+    if (k < 0 || k >= s.R) { bad = 1; continue; }
+    skey[q] = (uint32_t)k;
+    atomicAdd(&scur[(uint32_t)k >> sh], 1u);
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    if (lookup == 2) *c.pref_bad = bad;   // het_prefetch: the consuming lookup raises it
+    else dd_begin(s, c, n, t, lookup, bad, 0);
+  }
+  if (bad) return;
+  // the lookup's lines, as in k_dd_fused (hints)
+  for (int q = threadIdx.x; q < n; q += BK_THREADS) {
+    const int64_t key = skey[q];
+    prefetch_l2(s.hslot + hash_home(s, key));
+    prefetch_l2(s.hslot + hash_home(s, key) + 16);
+    if (key % s.world != s.rank) continue;
+    const int64_t row = key / s.world;
+    prefetch_l2(s.cg + row);
+    if (s.lfu_persist) prefetch_l2(s.count_by_key + key);
+    for (uint32_t d = 0; d < s.D && d < 128; d += 32) prefetch_l2(s.W + row * s.D + d);
+  }
+  // exclusive scan of the bucket counts (4 per thread)
+  {
+    const int b0 = threadIdx.x * (BK_N / BK_THREADS);
+    uint32_t v[BK_N / BK_THREADS];
+    int sum = 0;
+#pragma unroll
+    for (int j = 0; j < BK_N / BK_THREADS; ++j) { v[j] = scur[b0 + j]; sum += v[j]; }
+    int tot = 0;
+    int ex = block_scan_int(sum, warp_sums, &tot);
+#pragma unroll
+    for (int j = 0; j < BK_N / BK_THREADS; ++j) { soff[b0 + j] = ex; scur[b0 + j] = ex; ex += v[j]; }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < n; q += BK_THREADS) sord[atomicAdd(&scur[skey[q] >> sh], 1u)] = q;
+  __syncthreads();
+  // exact rank inside the bucket (scur now holds each bucket's end)
+  for (int q = threadIdx.x; q < n; q += BK_THREADS) {
+    const uint32_t k = skey[q], b = k >> sh;
+    const uint32_t i0 = soff[b], i1 = scur[b];
+    uint32_t r = i0;
+    for (uint32_t i = i0; i < i1; ++i) {
+      const uint32_t qq = sord[i], kk = skey[qq];
+      r += (kk < k) || (kk == k && (int)qq < q);
+    }
+    HET_ASSERT(r < (uint32_t)n);
+    c.sortbuf0[r] = ((uint64_t)k << pbits) | (uint64_t)q;
+    c.perm[r] = q;
+  }
+}
+
+// a lookup whose keys het_prefetch already deduplicated (NEXT-1):
+// block 0 does the per-call begin (and raises a key outside [0, R) found by
+// the prefetch), the other blocks the deferred eviction
+__global__ void __launch_bounds__(256) k_begin_evict(Dev s, Call c, int n, uint64_t t, EvBuf eb, P2P pm, int push) {
+  pdl_trigger();
+  if (blockIdx.x > 0) {
+    evict_listed(s, eb, push ? &pm : nullptr, blockIdx.x - 1, gridDim.x - 1);
+    return;
+  }
+  if (threadIdx.x == 0) dd_begin(s, c, n, t, 1, *c.pref_bad, 0);
+}
+
+int launch_begin_evict(const Dev& s, const Call& c, int n, uint64_t t, cudaStream_t st, void* evbuf,
+                       const void* p2pview, bool evict) {
+  P2P pm{};
+  int push = 0;
+  if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
+  k_begin_evict<<<1 + (evict ? 2 * EV_BLOCKS : 0), 256, 0, st>>>(s, c, n, t, *reinterpret_cast<EvBuf*>(evbuf), pm,
+                                                                   push);
+  return 1;
+}
+
+int launch_dd_bucket(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st,
+                     void* evbuf, const void* p2pview, bool evict) {
+  const size_t smem = (2 * (size_t)BK_MAX + 2 * BK_N) * 4;
+  static uint64_t attr_devs = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!((attr_devs >> (dev & 63)) & 1)) {
+    cudaFuncSetAttribute(k_dd_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_devs |= 1ull << (dev & 63);
+  }
+  P2P pm{};
+  int push = 0;
+  if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
+  k_dd_bucket<<<1 + (evict ? EV_BLOCKS : 0), BK_THREADS, smem, st>>>(c.keys, n, pbits, s, c, t, lookup,
+                                                                      *reinterpret_cast<EvBuf*>(evbuf), pm, push);
+  return 1;
+}
+
 // ------------------------------------------------------------------ debug export of an rmode lookup
 // One CTA: head flags of the sorted composites, a block scan for the unique
 // index u of every head, then unique[u], seg_off[u], status[u] and the
 // inverse by u -- the compact lookup log (R2) the rmode path never builds.
-constexpr int CL_THREADS = 1024, CL_ITEMS = 8;   // n <= 8192 (the rmode dedup's bound)
+constexpr int CL_THREADS = 1024, CL_ITEMS = 16;   // n <= 16384 (the rmode dedups' bound)
 __global__ void __launch_bounds__(CL_THREADS) k_compact_log(Dev s, Call c) {
-  __shared__ int u_of[CL_THREADS * CL_ITEMS];
+  extern __shared__ int u_of[];   // [n]
   __shared__ int warp_sums[32];
   const int n = s.ctl->abort ? 0 : c.n, pb = c.pbits;
   const int i0 = threadIdx.x * CL_ITEMS;
@@ -1443,7 +1573,11 @@ __global__ void __launch_bounds__(CL_THREADS) k_compact_log(Dev s, Call c) {
   for (int pos = threadIdx.x; pos < n; pos += blockDim.x) c.dbg_inverse[pos] = u_of[c.inverse[pos]];
 }
 
-void launch_compact_log(const Dev& s, const Call& c, cudaStream_t st) { k_compact_log<<<1, CL_THREADS, 0, st>>>(s, c); }
+void launch_compact_log(const Dev& s, const Call& c, cudaStream_t st) {
+  const size_t smem = (size_t)std::max(c.n, 1) * 4;
+  cudaFuncSetAttribute(k_compact_log, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_compact_log<<<1, CL_THREADS, smem, st>>>(s, c);
+}
 
 // ------------------------------------------------------------------ launchers
 constexpr int FUSED_MAX_DD_RANK = 8192;
@@ -1451,7 +1585,6 @@ constexpr int FUSED_MAX = 8192;
 
 bool fused_ok(const Dev& s, int n) { return n <= FUSED_MAX; }
 
-constexpr int EV_BLOCKS = 32;   // blocks of the deferred eviction in k_dd_fused (16 warps each)
 
 int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st,
                     void* evbuf, const void* p2pview, bool evict, int compact) {

@@ -118,6 +118,7 @@ __device__ __forceinline__ void push_record(const Dev& s, const P2P& m, int32_t 
   int ps = 0;
   if (lane == 0) ps = atomicAdd(&m.c3cnt[o], 1);
   ps = __shfl_sync(0xffffffffu, ps, 0);
+  HET_ASSERT(ps >= 0 && ps < m.CAPS);
   if (lane == 0) {
     Rec r;
     r.key = key; r.cc = ecc; r.kind = K_PUSH | K_DIRTY;

@@ -55,7 +55,7 @@ EXPORTS = ["het_get_unique_id", "het_cache_create", "het_lookup", "het_update", 
            "het_debug_lookup_log", "het_debug_victims", "het_debug_dump_cache",
            "het_profile_enable", "het_profile_read", "het_cache_destroy", "het_last_error",
            "het_group_create", "het_group_lookup", "het_group_update", "het_group_evict",
-           "het_group_sync", "het_group_dense_allreduce", "het_debug_eviction_plan"]
+           "het_group_sync", "het_group_dense_allreduce", "het_debug_eviction_plan", "het_prefetch"]
 
 _lib = None
 
@@ -93,6 +93,7 @@ def load():
         "het_group_sync": [P, U32, P],
         "het_group_dense_allreduce": [P, U32, P, U64, P],
         "het_debug_eviction_plan": [P, P, P],
+        "het_prefetch": [P, P, U32, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -163,6 +164,10 @@ def het_cache_create(rows, D, cache_frac, s, policy=HET_LFU, rank=0, world=1, un
 
 def het_lookup(h, keys, n, clock, out, stream=None):
     _check(h, load().het_lookup(h, _ptr(keys), n, clock, _ptr(out), _stream(stream)), "het_lookup")
+
+
+def het_prefetch(h, keys, n, stream=None):
+    _check(h, load().het_prefetch(h, _ptr(keys), n, _stream(stream)), "het_prefetch")
 
 
 def het_update(h, keys, n, grads, lr, stream=None):
@@ -304,6 +309,10 @@ class HetCache:
 
     def update(self, keys, grads, lr):
         het_update(self.h, keys, keys.numel(), grads, lr)
+
+    def prefetch(self, keys, stream=None):
+        """NEXT-1: dedup of the next lookup's keys now (e.g. on a side stream)."""
+        het_prefetch(self.h, keys, keys.numel(), stream)
 
     def step(self, keys, grads, out, lr, dense=None, side=None):
         """One training step of the sparse path: lookup (HET_CLOCK_AUTO) +

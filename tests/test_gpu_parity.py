@@ -524,3 +524,58 @@ def test_scale_shaped_wide_rows(D, B, T):
         p.g.update(kd, torch.from_numpy(grads).cuda(), LR)
         p.o.update([grads], LR)
     p.compare_stats()
+
+
+@pytest.mark.parametrize("B", [128, 400])   # n = 3,328 (multi-CTA rank dedup) and 10,400 (bucket dedup)
+def test_prefetch_next_batch(B):
+    """NEXT-1: het_prefetch runs the next lookup's dedup
+    ahead -- here on a side stream while this step's update runs -- and the
+    lookup with the same keys skips its own; every result stays the oracle's.
+    A prefetch of other keys is ignored; host keys work; a key outside [0, R)
+    found by the prefetch is reported by the lookup that consumes it."""
+    het = _het()
+    R, D, s, frac = 20000, 16, 3, 0.1
+    cards = gen.scaled_cards(R)
+    n = B * 26
+    p = Pair(R, D, frac, s, LFU, n_max=n)
+    p.g_policy = LFU
+    side = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    keys = [gen.criteo_keys(0, t, 1, B, cards)[0].numpy() for t in range(31)]
+    kd = [torch.from_numpy(k).cuda() for k in keys]
+    for t in range(30):
+        out = p.g.lookup(kd[t], t).cpu().numpy()
+        assert_rows(out, p.o.lookup(t, [keys[t]])[0])
+        gl, ol = p.g.lookup_log(), p.o.lookup_log(0)
+        assert np.array_equal(gl["unique"], ol["unique"]) and np.array_equal(gl["status"], ol["status"]), t
+        assert np.array_equal(gl["inverse"][:n], ol["inverse"]), t
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            nxt = kd[t + 1] if t % 7 != 3 else kd[(t + 5) % 31]        # t % 7 == 3: a batch the next lookup is not
+            het.het_prefetch(p.g.h, nxt, nxt.numel(), stream=side)
+        grads = gen.grads(0, t, n, D).numpy()
+        p.g.update(kd[t], torch.from_numpy(grads).cuda(), LR)
+        p.o.update([grads], LR)
+        main.wait_stream(side)
+        gk, gd = p.g.victims()
+        ok, od = p.o.victims(0)
+        order = np.argsort(ok, kind="stable")
+        assert np.array_equal(gk, ok[order]) and np.array_equal(gd, od[order]), t
+    p.compare_stats()
+    p.compare_cache()
+    # host keys
+    hk = keys[30]
+    het.het_prefetch(p.g.h, hk, hk.size)
+    out = np.zeros((hk.size, D), np.float32)
+    het.het_lookup(p.g.h, hk, hk.size, 30, out)
+    torch.cuda.synchronize()
+    assert_rows(out, p.o.lookup(30, [hk])[0])
+    p.finish()
+    # a key outside [0, R) seen by the prefetch
+    bad = kd[0].clone()
+    bad[5] = R
+    het.het_prefetch(p.g.h, bad, bad.numel())
+    p.g.lookup(bad, 31)
+    with pytest.raises(het.HetError) as e:
+        het.het_check(p.g.h)
+    assert e.value.code == 2
