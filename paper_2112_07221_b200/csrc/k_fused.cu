@@ -37,7 +37,7 @@ namespace het {
 #ifdef HET_TIMELINE
 // per-warp slots (no contention): g_tlw[mark][warp], read and reduced on the host
 constexpr int TLW = 8192;
-__device__ unsigned long long g_tlw[32 * TLW];
+__device__ unsigned long long g_tlw[40 * TLW];   // rows 32..39: ad-hoc marks (TL_X)
 __device__ __forceinline__ unsigned long long tl_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -46,19 +46,21 @@ __device__ __forceinline__ unsigned long long tl_now() {
 #define TL_W(i) do { if ((threadIdx.x & 31) == 0) { int w_ = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; \
   if (w_ < TLW) g_tlw[(i) * TLW + w_] = tl_now(); } } while (0)
 #define TL_MIN(i) TL_W(i)
+#define TL_X(i) TL_W(32 + (i))
 #define TL_MAX(i) TL_W(i)
 extern "C" int het_debug_timeline(unsigned long long* out, int marks, int warps) {
   cudaDeviceSynchronize();
   if (out) cudaMemcpyFromSymbol(out, g_tlw, sizeof(unsigned long long) * (size_t)marks * TLW);
   cudaMemset((void*)0, 0, 0);
   static unsigned long long* zero = nullptr;
-  if (!zero) zero = (unsigned long long*)calloc(32 * TLW, 8);
-  cudaMemcpyToSymbol(g_tlw, zero, sizeof(unsigned long long) * 32 * TLW);
+  if (!zero) zero = (unsigned long long*)calloc(40 * TLW, 8);
+  cudaMemcpyToSymbol(g_tlw, zero, sizeof(unsigned long long) * 40 * TLW);
   (void)warps;
   return 0;
 }
 #else
 #define TL_MIN(i) do {} while (0)
+#define TL_X(i) do {} while (0)
 #define TL_MAX(i) do {} while (0)
 #endif
 
@@ -1417,7 +1419,7 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
 }
 
 // ------------------------------------------------------------------ K1 for 8192 < n <= 16384 (rmode)
-// One CTA ranks every occurrence by a counting sort over 4096 key buckets
+// Eight CTAs rank every occurrence by a counting sort over 4096 key buckets
 // (the top 12 bits of the key range: the keys are permuted ids, R15) and an
 // exact rank inside each bucket: r(p) = offset(bucket) + #{q in the bucket:
 // key_q < key_p, or key_q = key_p and q < p} -- the same stable sort as the
@@ -1425,15 +1427,34 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
 // batches: 14,208 distinct ids).  Extra blocks run the deferred eviction as
 // in k_dd_fused.
 constexpr int BK_THREADS = 1024, BK_BITS = 12, BK_N = 1 << BK_BITS, BK_MAX = 16384;
+constexpr int BK_PF = 16;       // blocks issuing the lookup's L2 prefetches
+constexpr int BK_CTAS = 8;      // CTAs that each build the bucket order and rank 1/8 of it
 constexpr int EV_BLOCKS = 32;   // blocks of the deferred eviction beside the dedup
 __global__ void __launch_bounds__(BK_THREADS)
 k_dd_bucket(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, uint64_t t, int lookup, EvBuf eb,
             P2P pm, int push) {
   pdl_trigger();
-  if (blockIdx.x > 0) {
-    evict_listed(s, eb, push ? &pm : nullptr, blockIdx.x - 1, gridDim.x - 1);
+  if ((int)blockIdx.x >= BK_CTAS + BK_PF) {
+    evict_listed(s, eb, push ? &pm : nullptr, blockIdx.x - BK_CTAS - BK_PF, gridDim.x - BK_CTAS - BK_PF);
     return;
   }
+  if ((int)blockIdx.x >= BK_CTAS) {   // the lookup's lines (hints), spread over BK_PF blocks
+    if (!lookup) return;
+    const int pb = blockIdx.x - BK_CTAS;
+    for (int q = pb * BK_THREADS + threadIdx.x; q < n; q += BK_PF * BK_THREADS) {   // one pass
+      const int64_t key = __ldg(&keys[q]);
+      if (key < 0 || key >= s.R) continue;
+      prefetch_l2(s.hslot + hash_home(s, key));
+      prefetch_l2(s.hslot + hash_home(s, key) + 16);
+      if (s.lfu_persist) prefetch_l2(s.count_by_key + key);
+      if (key % s.world != s.rank) continue;
+      const int64_t row = key / s.world;
+      prefetch_l2(s.cg + row);
+      for (uint32_t d = 0; d < s.D && d < 128; d += 32) prefetch_l2(s.W + row * s.D + d);
+    }
+    return;
+  }
+  TL_MIN(0);
   extern __shared__ __align__(16) uint32_t bk[];
   uint32_t* skey = bk;                 // [n]   the keys (32-bit)
   uint32_t* sord = bk + BK_MAX;        // [n]   positions grouped by bucket
@@ -1444,29 +1465,30 @@ k_dd_bucket(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, u
   for (int b = threadIdx.x; b < BK_N; b += BK_THREADS) scur[b] = 0;
   __syncthreads();
   int bad = 0;
-  for (int q = threadIdx.x; q < n; q += BK_THREADS) {
-    const int64_t k = __ldg(&keys[q]);
-    if (k < 0 || k >= s.R) { bad = 1; continue; }
-    skey[q] = (uint32_t)k;
-    atomicAdd(&scur[(uint32_t)k >> sh], 1u);
+  {  // every key load of this thread in flight at once
+    constexpr int IT = BK_MAX / BK_THREADS;
+    int64_t kk[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const int q = threadIdx.x + i * BK_THREADS;
+      kk[i] = q < n ? __ldg(&keys[q]) : 0;
+    }
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const int q = threadIdx.x + i * BK_THREADS;
+      if (q >= n) continue;
+      if (kk[i] < 0 || kk[i] >= s.R) { bad = 1; continue; }
+      skey[q] = (uint32_t)kk[i];
+      atomicAdd(&scur[(uint32_t)kk[i] >> sh], 1u);
+    }
   }
   bad = __syncthreads_or(bad);
-  if (threadIdx.x == 0) {
+  TL_X(4);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (lookup == 2) *c.pref_bad = bad;   // het_prefetch: the consuming lookup raises it
     else dd_begin(s, c, n, t, lookup, bad, 0);
   }
   if (bad) return;
-  // the lookup's lines, as in k_dd_fused (hints)
-  for (int q = threadIdx.x; q < n; q += BK_THREADS) {
-    const int64_t key = skey[q];
-    prefetch_l2(s.hslot + hash_home(s, key));
-    prefetch_l2(s.hslot + hash_home(s, key) + 16);
-    if (key % s.world != s.rank) continue;
-    const int64_t row = key / s.world;
-    prefetch_l2(s.cg + row);
-    if (s.lfu_persist) prefetch_l2(s.count_by_key + key);
-    for (uint32_t d = 0; d < s.D && d < 128; d += 32) prefetch_l2(s.W + row * s.D + d);
-  }
   // exclusive scan of the bucket counts (4 per thread)
   {
     const int b0 = threadIdx.x * (BK_N / BK_THREADS);
@@ -1480,21 +1502,29 @@ k_dd_bucket(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, u
     for (int j = 0; j < BK_N / BK_THREADS; ++j) { soff[b0 + j] = ex; scur[b0 + j] = ex; ex += v[j]; }
   }
   __syncthreads();
+  TL_X(0);
   for (int q = threadIdx.x; q < n; q += BK_THREADS) sord[atomicAdd(&scur[skey[q] >> sh], 1u)] = q;
   __syncthreads();
-  // exact rank inside the bucket (scur now holds each bucket's end)
-  for (int q = threadIdx.x; q < n; q += BK_THREADS) {
+  TL_X(1);
+  // exact rank inside the bucket (scur now holds each bucket's end); CTA b
+  // ranks positions [b per, (b+1) per) (the compare loops are shared-memory
+  // bound: one CTA alone takes ~15 us at n = 14,208).  Every CTA built the
+  // same buckets (in its own order inside a bucket, which the rank ignores).
+  const int per = (n + BK_CTAS - 1) / BK_CTAS;
+  const int q_lo = blockIdx.x * per, q_hi = min(n, q_lo + per);
+  for (int q = q_lo + (int)threadIdx.x; q < q_hi; q += BK_THREADS) {
     const uint32_t k = skey[q], b = k >> sh;
-    const uint32_t i0 = soff[b], i1 = scur[b];
-    uint32_t r = i0;
-    for (uint32_t i = i0; i < i1; ++i) {
-      const uint32_t qq = sord[i], kk = skey[qq];
+    const uint32_t j0 = soff[b], j1 = scur[b];
+    uint32_t r = j0;
+    for (uint32_t j = j0; j < j1; ++j) {
+      const uint32_t qq = sord[j], kk = skey[qq];
       r += (kk < k) || (kk == k && (int)qq < q);
     }
     HET_ASSERT(r < (uint32_t)n);
     c.sortbuf0[r] = ((uint64_t)k << pbits) | (uint64_t)q;
     c.perm[r] = q;
   }
+  TL_X(3);
 }
 
 // a lookup whose keys het_prefetch already deduplicated (NEXT-1):
@@ -1521,7 +1551,7 @@ int launch_begin_evict(const Dev& s, const Call& c, int n, uint64_t t, cudaStrea
 
 int launch_dd_bucket(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st,
                      void* evbuf, const void* p2pview, bool evict) {
-  const size_t smem = (2 * (size_t)BK_MAX + 2 * BK_N) * 4;
+  const size_t smem = (2 * (size_t)BK_MAX + 2 * BK_N) * 4;   // keys, bucket order, offsets: 160 KB
   static uint64_t attr_devs = 0;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1532,7 +1562,7 @@ int launch_dd_bucket(const Dev& s, const Call& c, int n, int pbits, uint64_t t, 
   P2P pm{};
   int push = 0;
   if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
-  k_dd_bucket<<<1 + (evict ? EV_BLOCKS : 0), BK_THREADS, smem, st>>>(c.keys, n, pbits, s, c, t, lookup,
+  k_dd_bucket<<<BK_CTAS + BK_PF + (evict ? EV_BLOCKS : 0), BK_THREADS, smem, st>>>(c.keys, n, pbits, s, c, t, lookup,
                                                                       *reinterpret_cast<EvBuf*>(evbuf), pm, push);
   return 1;
 }
