@@ -81,6 +81,11 @@ struct het_cache {
   // segment reduce of large batches: heavy keys on a forked stream
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // host gradients: staged on a copy stream, so the H2D overlaps the lookup's
+  // kernels and its D2H of the rows (full-duplex link); the events order it
+  // after the previous update's reads of the staging buffer and before this one's
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_rows_free = nullptr, ev_rows_ready = nullptr;
   // profiling
   bool prof = false;
   std::vector<ProfRec> prof_pending;
@@ -305,7 +310,10 @@ static het_status_t create_impl(uint64_t rows, uint32_t D, double cache_frac, ui
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_rows_free, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_rows_ready, cudaEventDisableTiming) != cudaSuccess) {
     het_cache_destroy(h);
     return HET_ERR_CUDA;
   }
@@ -768,9 +776,20 @@ static het_status_t update_impl(het_cache* h, const int64_t* keys, uint32_t n, c
     k_check_keys<<<std::min<int>(148, (n + 255) / 256), 256, 0, st>>>(keys, (int)n, h->call, d.ctl);
     h->launches += 1;
   }
+  bool staged = false;
   if (n && !is_device_ptr(grads)) {
     if (!h->stage_rows) CUDA_TRY(h, (dalloc(h, &h->stage_rows, (size_t)h->n_max * h->D)));
-    CUDA_TRY(h, cudaMemcpyAsync(h->stage_rows, grads, (size_t)n * h->D * 4, cudaMemcpyHostToDevice, st));
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    if (cap == cudaStreamCaptureStatusNone) {   // H2D on the copy stream, beside the lookup's work
+      CUDA_TRY(h, cudaStreamWaitEvent(h->copy, h->ev_rows_free, 0));
+      CUDA_TRY(h, cudaMemcpyAsync(h->stage_rows, grads, (size_t)n * h->D * 4, cudaMemcpyHostToDevice, h->copy));
+      CUDA_TRY(h, cudaEventRecord(h->ev_rows_ready, h->copy));
+      CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_rows_ready, 0));
+      staged = true;
+    } else {
+      CUDA_TRY(h, cudaMemcpyAsync(h->stage_rows, grads, (size_t)n * h->D * 4, cudaMemcpyHostToDevice, st));
+    }
     grads = h->stage_rows;
   }
   if (h->fused) {
@@ -789,6 +808,7 @@ static het_status_t update_impl(het_cache* h, const int64_t* keys, uint32_t n, c
     het_status_t rc = evict_overflow(h, st);
     if (rc) return fail(h, rc, "evict failed");
   }
+  if (staged) CUDA_TRY(h, cudaEventRecord(h->ev_rows_free, st));   // the staging buffer is read by now
   CUDA_TRY(h, cudaGetLastError());
   h->have_lookup = false;
   return HET_OK;
@@ -1242,6 +1262,9 @@ het_status_t het_cache_destroy(het_cache_t h) {
   if (h->side) cudaStreamDestroy(h->side);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->copy) cudaStreamDestroy(h->copy);
+  if (h->ev_rows_free) cudaEventDestroy(h->ev_rows_free);
+  if (h->ev_rows_ready) cudaEventDestroy(h->ev_rows_ready);
   for (void* q : h->allocs) cudaFree(q);
   for (ProfRec& r : h->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
