@@ -75,6 +75,7 @@ constexpr int DDF_THREADS = 512;
 constexpr int DDF_WARPS = DDF_THREADS / 32;
 constexpr int DDF_ITEMS = 16;   // FUSED_MAX / DDF_THREADS (elements per lane in the finish)
 constexpr int LK_WARPS = 8;
+constexpr int SW_F4 = 64;   // wide rows: float4 per slice (256 columns), two per lane
 constexpr int UPD_THREADS = 256;
 constexpr int UPD_WARPS = UPD_THREADS / 32;
 
@@ -725,8 +726,9 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
   __syncthreads();
   Ctl* ctl = s.ctl;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int grp = wib / G, gw = wib % G;
-  const int u = blockIdx.x * (LK_WARPS / G) + grp;   // rmode: sorted position r
+  const int GG = G > 0 ? G : 1;   // G == 0: one warp per key, decisions only
+  const int grp = wib / GG, gw = wib % GG;
+  const int u = blockIdx.x * (LK_WARPS / GG) + grp;   // rmode: sorted position r
   const int U = c.rmode ? c.n : ctl->U;
   const bool live = !ctl->abort && u < U;
   bool head = true;
@@ -814,10 +816,15 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
     if (lane == 0) {
       if (e >= 0) c.uentry[u] = e;
       meta[grp] = LkMeta{key, e, j0, cnt, g, st, (uint8_t)push};
+      if (G == 0) {   // decisions only: the row moves are k_lookup_wide_mv's (key, fetch | push << 1)
+        c.uniq[u] = key;
+        c.ucnt[u] = (e >= 0 ? (st != ST_HIT ? 1 : 0) | (push ? 2 : 0) : 0) | (e >= 0 ? 4 : 0);
+      }
     }
   }
+  if (G == 0 && live && c.rmode && gw == 0 && !head && lane == 0) c.ucnt[u] = 0;
   __syncthreads();
-  if (live) {
+  if (live && G > 0) {
     const LkMeta mt = meta[grp];
     const int D4 = s.D >> 2;
     const int d0 = gw * (D4 / G), d1 = d0 + D4 / G;
@@ -860,6 +867,56 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
   }
 }
 
+// The row moves of the wide lookup (after k_lookup_wide with G = 0): warp per
+// (key, 256-column slice) item -- the Evict push W += p of a dirty expired
+// entry, the Fetch v = W of a refetch or miss, and the
+// Get scatter of the slice to every occurrence -- at full occupancy.
+// Per column the same operations in the same order as the one-kernel form.
+__global__ void __launch_bounds__(256) k_lookup_wide_mv(Dev s, Call c, float* __restrict__ out) {
+  pdl_wait();
+  const Ctl* ctl = s.ctl;
+  const int U = ctl->abort ? 0 : c.n;   // rmode
+  const int D4 = s.D >> 2, S = D4 / SW_F4;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  float4* o4 = reinterpret_cast<float4*>(out);
+  for (int it = gw; it < U * S; it += nw) {
+    const int u = it / S;
+    const int fl = __ldcg(&c.ucnt[u]);
+    if (!(fl & 4)) continue;   // not a head / no entry
+    const int4 rec = __ldcg(&c.urec[u]);
+    const int32_t e = rec.x;
+    const int j0 = rec.y, cnt = rec.z & 0x7FFFFFFF;
+    const int base = (it % S) * SW_F4 + lane;
+    float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
+    float4 val[2];
+    if (fl & 1) {
+      const int64_t key = __ldcg(&c.uniq[u]);
+      float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
+      const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float4 w = Wr[base + 32 * j];
+        if (fl & 2) { w = f4add_(w, pr[base + 32 * j]); Wr[base + 32 * j] = w; }
+        vr[base + 32 * j] = w;
+        val[j] = w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) val[j] = vr[base + 32 * j];
+    }
+    for (int kb = 0; kb < cnt; kb += 32) {
+      const int src = kb + lane < cnt ? c.perm[j0 + kb + lane] : 0;
+      const int m = min(32, cnt - kb);
+      for (int k = 0; k < m; ++k) {
+        const int64_t pos = __shfl_sync(0xffffffffu, src, k);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) __stcs(o4 + pos * D4 + base + 32 * j, val[j]);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K_upd
 // Evict push of one resident entry at N = 1 (warp-cooperative) + delete + free
 // push != nullptr (N > 1): the Evict push goes to the owner's inbox, carried
@@ -870,7 +927,6 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
 __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_t e, int64_t key, uint64_t slot,
                                             int lane, int* dpop, unsigned* s_dirty, unsigned* s_ev,
                                             unsigned* s_tomb, int vi, int64_t fpos, const P2P* push = nullptr) {
-  Ctl* ctl = s.ctl;
   const uint32_t ecs = s.cs[e], ecc = s.cc[e], prim = s.eprim[e];
   const bool dirty = ecc > ecs;
   const int D4 = s.D >> 2;
@@ -1011,58 +1067,329 @@ __device__ __forceinline__ void segreduce_key(const Dev& s, const Call& c, const
   if (lane == 0) s.cc[e] = ecc + 1;
 }
 
-// Wide rows (D >= 1024): item (u, slice) of 512 columns per warp, so a
-// key's columns are reduced on several SMs at once.  Per column the order is
-// unchanged (+0.0f, then ascending batch position, R11); each lane keeps four
-// column accumulators and four occurrences in flight (16 loads).  The clock
-// step c_c += 1 is taken after the grid sync (every slice read the dirty flag
-// first).
-__device__ __forceinline__ void segreduce_slice(const Dev& s, const Call& c, const float4* __restrict__ G4,
-                                                float lr, int u, int sl, int lane) {
-  const int4 rec = __ldcg(&c.urec[u]);
-  const int32_t e = rec.x;
-  if (e < 0) return;   // rmode: not a key's first sorted position
-  const int j0 = rec.y, cnt = rec.z & 0x7FFFFFFF;
-  const bool dirty = rec.z < 0;
-  const int D4 = s.D >> 2;
-  const int base = sl * 128 + lane;
-  const float nlr = -lr;
-  float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
-  float4* pr = reinterpret_cast<float4*>(s.p + (int64_t)e * s.D);
+// Wide rows (D >= 1024, BASELINE configs[4]: 16 KB rows): the ordered
+// segment reduce + SGD + pending of every (key, 256-column slice) item, warp
+// per item, in its own kernel so that it runs at 4 blocks per SM (the
+// cooperative update holds 2): per column the order is unchanged (+0.0f, then
+// ascending batch position, R11).  Each lane keeps two columns; with <= 4
+// occurrences their positions come with the lookup's record and every
+// occurrence slice, v and p are in flight at once, and the next item's record
+// loads while this one is reduced.  The clock step follows in k_update_fused.
+__global__ void __launch_bounds__(256, 4) k_seg_wide(Dev s, Call c, const float* __restrict__ G, float lr) {
+  pdl_wait();
+  const Ctl* ctl = s.ctl;
+  const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);
+  const int D4 = s.D >> 2, S = D4 / SW_F4;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const float4* G4 = reinterpret_cast<const float4*>(G);
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 vv[4], pp[4], acc[4];
+  const float nlr = -lr;
+  const int items = U * S;
+  int4 rec = make_int4(-1, 0, 0, 0), p4 = make_int4(0, 0, 0, 0);
+  if (gw < items) { rec = __ldcg(&c.urec[gw / S]); p4 = __ldcg(&c.upos[gw / S]); }
+  for (int it = gw; it < items; it += nw) {
+    const int nx = it + nw;
+    int4 rn = make_int4(-1, 0, 0, 0), pn = make_int4(0, 0, 0, 0);
+    if (nx < items) { rn = __ldcg(&c.urec[nx / S]); pn = __ldcg(&c.upos[nx / S]); }
+    const int32_t e = rec.x;
+    if (e >= 0) {   // rmode: non-heads carry no work
+      const int j0 = rec.y, cnt = rec.z & 0x7FFFFFFF;
+      const bool dirty = rec.z < 0;
+      const int base = (it % S) * SW_F4 + lane;
+      float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
+      float4* pr = reinterpret_cast<float4*>(s.p + (int64_t)e * s.D);
+      float4 acc[2] = {zero, zero};
+      if (cnt <= 4) {
+        const int pq[4] = {p4.x, p4.y, p4.z, p4.w};
+        float4 g[4][2];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    vv[j] = vr[base + 32 * j];
-    pp[j] = dirty ? pr[base + 32 * j] : zero;
-    acc[j] = zero;
-  }
-  for (int kb = 0; kb < cnt; kb += 32) {
-    const int src = kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0;
-    const int m = min(32, cnt - kb);
-    for (int k = 0; k < m; k += 4) {
-      float4 g[4][4];
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int pq = __shfl_sync(0xffffffffu, src, min(k + q, m - 1));
+          for (int j = 0; j < 2; ++j) g[q][j] = q < cnt ? __ldcs(G4 + (int64_t)pq[q] * D4 + base + 32 * j) : zero;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          g[q][j] = k + q < m ? __ldcs(G4 + (int64_t)pq * D4 + base + 32 * j) : zero;
+        for (int q = 0; q < 4; ++q)
+          if (q < cnt) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) acc[j] = f4add_(acc[j], g[q][j]);
+          }
+      } else {
+        for (int kb = 0; kb < cnt; kb += 32) {
+          const int src = kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0;
+          const int m = min(32, cnt - kb);
+          for (int k = 0; k < m; k += 4) {
+            float4 g[4][2];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int pq = __shfl_sync(0xffffffffu, src, min(k + q, m - 1));
+#pragma unroll
+              for (int j = 0; j < 2; ++j) g[q][j] = k + q < m ? __ldcs(G4 + (int64_t)pq * D4 + base + 32 * j) : zero;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (k + q < m) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) acc[j] = f4add_(acc[j], g[q][j]);
+              }
+          }
+        }
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (k + q < m) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j] = f4add_(acc[j], g[q][j]);
-        }
+      for (int j = 0; j < 2; ++j) {
+        const float4 vv = vr[base + 32 * j];
+        const float4 pp = dirty ? pr[base + 32 * j] : zero;
+        const float4 dl = make_float4(__fmul_rn(nlr, acc[j].x), __fmul_rn(nlr, acc[j].y), __fmul_rn(nlr, acc[j].z),
+                                      __fmul_rn(nlr, acc[j].w));
+        vr[base + 32 * j] = f4add_(vv, dl);
+        pr[base + 32 * j] = f4add_(pp, dl);
+      }
+    }
+    rec = rn;
+    p4 = pn;
+  }
+}
+
+// The same items staged by the copy engine (BASELINE configs[4]; measured:
+// k_seg_wide keeps ~12 GB/s per SM in flight and a 128-occurrence key is 32
+// dependent load rounds on one warp).  Item = (key, 512-column slice); its
+// occurrence rows are cut into stages of <= TS_CH rows; a producer warp per
+// CTA issues one 2 KB bulk copy per row slice (cp.async.bulk, complete_tx on
+// the stage's full barrier) plus v and p (if dirty) with the item's last
+// stage; four consumer warps, a float4 column per thread, add the staged rows
+// in ascending position into a register accumulator carried across the
+// item's stages (+0.0f first, R11), then v += -lr*acc, p = (dirty ? p : +0)
+// + -lr*acc (R13) straight to HBM.  Three 20 KB stages per CTA, three CTAs
+// per SM (three producers).  Every warp walks the same item list (the
+// producer's barrier arrives are relaxed, so no header passes through shared
+// memory: a release arrive waits for the producer's copies in flight).
+constexpr int TS_SL4 = 128;          // float4 per slice (512 columns)
+constexpr int TS_CH = 8;             // occurrence rows per stage
+constexpr int TS_N = 3;              // stages per CTA (three CTAs per SM)
+constexpr int TS_CW = 4;             // consumer warps (TS_CW * 32 == TS_SL4)
+constexpr int TS_ROWS = TS_CH + 2;   // + v + p
+constexpr size_t TS_SMEM = (size_t)TS_N * TS_ROWS * TS_SL4 * 16;
+
+// calls f(e, j0, cnt, c0, dirty, col4, l, p4) for every stage of this
+// CTA's items, in order (lane l's p4: the item's first positions).  CTA b takes
+// slice b % S of the keys u = b / S + i * Q (Q = gridDim.x / S key groups):
+// 32 keys' records per load round, heads only.
+template <class F>
+__device__ __forceinline__ void ts_walk(const Call& c, int U, int S, int lane, F&& f) {
+  const int Q = (int)gridDim.x / S, q = (int)blockIdx.x / S;
+  const int col4 = ((int)blockIdx.x % S) * TS_SL4;
+  for (int u0 = q; u0 < U; u0 += 32 * Q) {
+    const int u = u0 + lane * Q;
+    int4 rec = make_int4(-1, 0, 0, 0), p4 = make_int4(0, 0, 0, 0);
+    if (u < U) { rec = __ldcg(&c.urec[u]); p4 = __ldcg(&c.upos[u]); }
+    // rmode non-heads / capacity failures / past the end carry no work
+    for (unsigned live = __ballot_sync(0xffffffffu, rec.x >= 0); live; live &= live - 1) {
+      const int l = __ffs(live) - 1;
+      const int e = __shfl_sync(0xffffffffu, rec.x, l);
+      const int j0 = __shfl_sync(0xffffffffu, rec.y, l), z = __shfl_sync(0xffffffffu, rec.z, l);
+      const int cnt = z & 0x7FFFFFFF;
+      for (int c0 = 0; c0 < cnt; c0 += TS_CH) f(e, j0, cnt, c0, z < 0, col4, l, p4);
     }
   }
+}
+
+__device__ __forceinline__ void mbar_arrive_rlx(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_rlx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__((TS_CW + 1) * 32) k_seg_tma(Dev s, Call c, const float* __restrict__ G, float lr) {
+  extern __shared__ __align__(1024) float4 ring[];   // [TS_N][TS_ROWS][TS_SL4]
+  __shared__ __align__(8) uint64_t full[TS_N], empty[TS_N];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < TS_N; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], TS_CW); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  const Ctl* ctl = s.ctl;
+  const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);
+  const int D4 = s.D >> 2, S = D4 / TS_SL4;
+  uint32_t k = 0;   // stages of this CTA
+  if (warp == TS_CW) {   // producer
+    const uint32_t SLB = TS_SL4 * 16;
+    ts_walk(c, U, S, lane, [&](int e, int j0, int cnt, int c0, bool dirty, int col4, int l, int4 p4) {
+      const int m = min(TS_CH, cnt - c0);
+      const bool last = c0 + m == cnt;
+      int pos = 0;
+      if (cnt > 4) {
+        pos = lane < m ? __ldg(&c.perm[j0 + c0 + lane]) : 0;
+      } else {
+        const int px = __shfl_sync(0xffffffffu, p4.x, l), py = __shfl_sync(0xffffffffu, p4.y, l);
+        const int pz = __shfl_sync(0xffffffffu, p4.z, l), pw = __shfl_sync(0xffffffffu, p4.w, l);
+        pos = lane == 0 ? px : lane == 1 ? py : lane == 2 ? pz : pw;
+      }
+      const uint32_t sl = k % TS_N, r = k / TS_N;
+      float4* stg = ring + (size_t)sl * TS_ROWS * TS_SL4;
+      if (lane == 0) {
+        if (r > 0) mbar_wait(&empty[sl], (r - 1) & 1);
+        const uint32_t bytes = (uint32_t)m * SLB + (last ? SLB * (dirty ? 2 : 1) : 0);
+        mbar_expect_tx_rlx(&full[sl], bytes);
+        mbar_arrive_rlx(&full[sl]);
+      }
+      for (int q = 0; q < m; ++q) {
+        const int pq = __shfl_sync(0xffffffffu, pos, q);
+        if (lane == 0) bulk_g2s(stg + q * TS_SL4, G + (int64_t)pq * s.D + col4 * 4, SLB, &full[sl]);
+      }
+      if (lane == 0 && last) {
+        bulk_g2s(stg + TS_CH * TS_SL4, s.v + (int64_t)e * s.D + col4 * 4, SLB, &full[sl]);
+        if (dirty) bulk_g2s(stg + (TS_CH + 1) * TS_SL4, s.p + (int64_t)e * s.D + col4 * 4, SLB, &full[sl]);
+      }
+      ++k;
+    });
+  } else {   // consumers: thread t owns float4 column t of the slice
+    const int t = threadIdx.x;
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float nlr = -lr;
+    float4 acc = zero;
+    ts_walk(c, U, S, lane, [&](int e, int j0, int cnt, int c0, bool dirty, int col4, int l, int4 p4) {
+      const int m = min(TS_CH, cnt - c0);
+      const bool last = c0 + m == cnt;
+      const uint32_t sl = k % TS_N, r = k / TS_N;
+      const float4* stg = ring + (size_t)sl * TS_ROWS * TS_SL4 + t;
+      mbar_wait(&full[sl], r & 1);
+      for (int q = 0; q < m; ++q) acc = f4add_(acc, stg[q * TS_SL4]);   // ascending position
+      float4 nv, np;
+      if (last) {
+        const float4 vv = stg[TS_CH * TS_SL4];
+        const float4 pp = dirty ? stg[(TS_CH + 1) * TS_SL4] : zero;
+        const float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
+                                      __fmul_rn(nlr, acc.w));
+        nv = f4add_(vv, dl);
+        np = f4add_(pp, dl);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_rlx(&empty[sl]);   // the stage's values are in registers (used above)
+      if (last) {
+        reinterpret_cast<float4*>(s.v + (int64_t)e * s.D)[col4 + t] = nv;
+        reinterpret_cast<float4*>(s.p + (int64_t)e * s.D)[col4 + t] = np;
+        acc = zero;
+      }
+      ++k;
+    });
+  }
+}
+
+// The wide lookup's row moves staged by the copy engine (after k_lookup_wide
+// with G = 0): item = (key, 512-column slice).  A loader warp brings the
+// slice's source -- v[e] for a hit, W[key] for a refetch or miss, and p[e]
+// when the Evict push W += p applies -- into a stage; a storer
+// warp adds W + p in shared memory for a push, then issues the bulk stores:
+// v[e] (Fetch), W[key] (the push) and the Get scatter to every
+// occurrence.  The storer frees a stage MV_LAG stages later, once the
+// bulk stores have read it (cp.async.bulk.wait_group.read).
+constexpr int MV_N = 12;       // stages per CTA (4 KB each)
+constexpr int MV_LAG = 4;      // stages whose bulk stores may still read shared memory
+constexpr int MV_CTAS = 4;     // CTAs per SM
+constexpr size_t MV_SMEM = (size_t)MV_N * 2 * TS_SL4 * 16;
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_lag() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(MV_LAG) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// ts_walk over the lookup's records: f(fl, e, key, j0, cnt, col4, l, p4) per head with an entry
+template <class F>
+__device__ __forceinline__ void mv_walk(const Call& c, int U, int S, int lane, F&& f) {
+  const int Q = (int)gridDim.x / S, q = (int)blockIdx.x / S;
+  const int col4 = ((int)blockIdx.x % S) * TS_SL4;
+  for (int u0 = q; u0 < U; u0 += 32 * Q) {
+    const int u = u0 + lane * Q;
+    int fl = 0;
+    int4 rec = make_int4(-1, 0, 0, 0), p4 = make_int4(0, 0, 0, 0);
+    int64_t key = 0;
+    if (u < U) {
+      fl = __ldcg(&c.ucnt[u]);
+      if (fl & 4) { rec = __ldcg(&c.urec[u]); p4 = __ldcg(&c.upos[u]); key = __ldcg(&c.uniq[u]); }
+    }
+    for (unsigned live = __ballot_sync(0xffffffffu, fl & 4); live; live &= live - 1) {
+      const int l = __ffs(live) - 1;
+      f(__shfl_sync(0xffffffffu, fl, l), __shfl_sync(0xffffffffu, rec.x, l), __shfl_sync(0xffffffffu, key, l),
+        __shfl_sync(0xffffffffu, rec.y, l), __shfl_sync(0xffffffffu, rec.z, l) & 0x7FFFFFFF, col4, l, p4);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(64) k_mv_tma(Dev s, Call c, float* __restrict__ out) {
+  extern __shared__ __align__(1024) float4 ring[];   // [MV_N][2][TS_SL4]: source slice, p slice
+  __shared__ __align__(8) uint64_t full[MV_N], empty[MV_N];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < MV_N; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  const int U = s.ctl->abort ? 0 : c.n;   // rmode
+  const int S = (s.D >> 2) / TS_SL4;
+  const uint32_t SLB = TS_SL4 * 16;
+  uint32_t k = 0;
+  if (warp == 0) {   // loader
+    mv_walk(c, U, S, lane, [&](int fl, int e, int64_t key, int j0, int cnt, int col4, int l, int4 p4) {
+      const uint32_t sl = k % MV_N, r = k / MV_N;
+      float4* stg = ring + (size_t)sl * 2 * TS_SL4;
+      if (lane == 0) {
+        if (r > 0) mbar_wait(&empty[sl], (r - 1) & 1);
+        mbar_expect_tx_rlx(&full[sl], SLB * ((fl & 2) ? 2 : 1));
+        mbar_arrive_rlx(&full[sl]);
+        const float* src = (fl & 1) ? s.W + key * s.D : s.v + (int64_t)e * s.D;
+        bulk_g2s(stg, src + col4 * 4, SLB, &full[sl]);
+        if (fl & 2) bulk_g2s(stg + TS_SL4, s.p + (int64_t)e * s.D + col4 * 4, SLB, &full[sl]);
+      }
+      ++k;
+    });
+  } else {           // storer
+    mv_walk(c, U, S, lane, [&](int fl, int e, int64_t key, int j0, int cnt, int col4, int l, int4 p4) {
+      const uint32_t sl = k % MV_N, r = k / MV_N;
+      float4* stg = ring + (size_t)sl * 2 * TS_SL4;
+      mbar_wait(&full[sl], r & 1);
+      if (fl & 2) {   // W + p, then visible to the bulk stores
+        for (int i = lane; i < TS_SL4; i += 32) stg[i] = f4add_(stg[i], stg[TS_SL4 + i]);
+        fence_proxy_async();
+        __syncwarp();
+      }
+      if (lane == 0) {
+        if (fl & 1) bulk_s2g(s.v + (int64_t)e * s.D + col4 * 4, stg, SLB);
+        if (fl & 2) bulk_s2g(s.W + key * s.D + col4 * 4, stg, SLB);
+      }
+      if (cnt <= 4) {
+        const int pq[4] = {__shfl_sync(0xffffffffu, p4.x, l), __shfl_sync(0xffffffffu, p4.y, l),
+                           __shfl_sync(0xffffffffu, p4.z, l), __shfl_sync(0xffffffffu, p4.w, l)};
+        if (lane == 0)
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float4 dl = make_float4(__fmul_rn(nlr, acc[j].x), __fmul_rn(nlr, acc[j].y), __fmul_rn(nlr, acc[j].z),
-                                  __fmul_rn(nlr, acc[j].w));
-    vr[base + 32 * j] = f4add_(vv[j], dl);
-    pr[base + 32 * j] = f4add_(pp[j], dl);
+          for (int q = 0; q < 4; ++q)
+            if (q < cnt) bulk_s2g(out + (int64_t)pq[q] * s.D + col4 * 4, stg, SLB);
+      } else {
+        for (int kb = 0; kb < cnt; kb += 32) {
+          const int src = kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0;
+          const int m = min(32, cnt - kb);
+          for (int q = 0; q < m; ++q) {
+            const int64_t pos = __shfl_sync(0xffffffffu, src, q);
+            if (lane == 0) bulk_s2g(out + pos * s.D + col4 * 4, stg, SLB);
+          }
+        }
+      }
+      if (lane == 0) {
+        bulk_commit();
+        bulk_wait_read_lag();   // the stores of stages <= k - MV_LAG have read their stage
+        if (k >= MV_LAG) mbar_arrive_rlx(&empty[(k - MV_LAG) % MV_N]);
+      }
+      __syncwarp();
+      ++k;
+    });
+    if (lane == 0) bulk_wait_all();
   }
 }
 
@@ -1253,7 +1580,7 @@ __global__ void __launch_bounds__(256) k_evict_pending(Dev s, EvBuf b, P2P pm, i
 // continue in this kernel after grid syncs.
 __global__ void __launch_bounds__(UPD_THREADS)
 k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, int stage_rows, P2P pm, int push,
-               int xb) {
+               int xb, int clock_only) {
   pdl_wait();
   const P2P* pp = push ? &pm : nullptr;
   extern __shared__ float4 dyn[];
@@ -1274,7 +1601,8 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   const int U = abort ? 0 : (c.rmode ? c.n : ctl->U);   // rmode: sorted positions, heads carry the work
   const uint32_t seq = ctl->lk_seq;   // set by the lookup; the plan flag carries it
   const int D4 = s.D >> 2;
-  const int S = (D4 >= 256 && D4 % 128 == 0) ? D4 / 128 : 1;   // wide rows: 512-column slices on separate warps
+  // wide rows (clock_only): k_seg_tma reduced the rows; this kernel steps the
+  // clocks (after every slice read the dirty flag: the kernel boundary) and plans
   const bool xblock = blockIdx.x >= 1 && blockIdx.x <= xb;
   __shared__ Plan pl;
   if (blockIdx.x == 0 || xblock) {
@@ -1323,7 +1651,7 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
     if (s_xlast && threadIdx.x == 0) {   // every victim key is listed
       ctl->ext_blocks = 0;
       const int nsel = __ldcg(&ctl->nsel);
-      const bool defer = s_emode == 1 && !s_rebuild && S == 1;
+      const bool defer = s_emode == 1 && !s_rebuild;
       ctl->nvict = s_emode == 1 ? nsel : 0;
       ctl->ev_nsel = nsel;
       ctl->ev_pending = (defer && nsel > 0) ? 1 : 0;
@@ -1337,10 +1665,14 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   const float4* G4 = reinterpret_cast<const float4*>(G);
   const int rw = gw - (1 + xb) * UPD_WARPS, nrw = nw - (1 + xb) * UPD_WARPS;
   if (rw >= 0) {
-    if (S == 1)
+    if (clock_only) {   // Cache.Clock, one lane per key
+      for (int u = rw * 32 + lane; u < U; u += nrw * 32) {
+        const int4 rec = __ldcg(&c.urec[u]);
+        if (rec.x >= 0) s.cc[rec.x] = (uint32_t)rec.w + 1;
+      }
+    } else {
       for (int u = rw; u < U; u += nrw) segreduce_key(s, c, G4, lr, u, lane, mystg, &bars[wid], phase, stage_rows);
-    else
-      for (int it = rw; it < U * S; it += nrw) segreduce_slice(s, c, G4, lr, it / S, it % S, lane);
+    }
   }
   TL_MAX(18);
   if (!xblock) read_plan();   // after this block's segment reduce (block 0: its own plan)
@@ -1349,15 +1681,8 @@ k_update_fused(Dev s, Call c, const float* __restrict__ G, float lr, EvBuf b, in
   const bool rebuild = s_rebuild;
   // LFU bitmap plan (or nothing to evict), no hash rebuild, narrow rows: done
   // -- the victims wait for the next call's first kernel (uniform decision)
-  if (emode != 2 && !rebuild && S == 1) return;
+  if (emode != 2 && !rebuild) return;
   grid.sync();
-  if (S > 1) {                                  // Cache.Clock once per key, after every slice
-    for (int u = gw * 32 + lane; u < U; u += nw * 32) {
-      const int32_t e = c.urec[u].x;
-      if (e >= 0) s.cc[e] += 1;
-    }
-    grid.sync();
-  }
   TL_MAX(19);
   // ---- in-kernel eviction: LFU bitmap victims (listed by blocks 1..xb)
   if (emode == 1) {
@@ -1679,8 +2004,25 @@ static void launch_pdl(void (*k)(KArgs...), int blocks, int threads, size_t smem
 
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st) {
   const int D4 = (int)s.D / 4;
-  if (D4 >= 256 && D4 % 128 == 0) {            // wide rows: G warps per key (a power of two)
-    int G = 1;
+  if (D4 >= 256 && D4 % 128 == 0) {            // wide rows
+    if (c.rmode) {   // decisions (warp per key), then the row moves (warp per key slice)
+      const int blocks = std::max(1, (c.n + LK_WARPS - 1) / LK_WARPS);
+      launch_pdl(k_lookup_wide, blocks, LK_WARPS * 32, 0, st, pdl_mode() >= 1, false, s, c, out, 0);
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      static const bool reg = getenv("HET_MV_REG") != nullptr;   // A/B: the register form
+      if (reg) {
+        launch_pdl(k_lookup_wide_mv, sms * 8, 256, 0, st, pdl_mode() >= 1, false, s, c, out);
+      } else {
+        static bool attr = false;
+        if (!attr) { cudaFuncSetAttribute(k_mv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MV_SMEM); attr = true; }
+        const int S = D4 / TS_SL4;
+        launch_pdl(k_mv_tma, std::max(1, sms * MV_CTAS / S) * S, 64, MV_SMEM, st, pdl_mode() >= 1, false, s, c, out);
+      }
+      return 2;
+    }
+    int G = 1;   // G warps per key (a power of two), decisions and moves in one kernel
     while (G * 2 <= std::min(LK_WARPS, D4 / 128)) G *= 2;
     const int blocks = std::max(1, (c.n + LK_WARPS / G - 1) / (LK_WARPS / G));
     launch_pdl(k_lookup_wide, blocks, LK_WARPS * 32, 0, st, pdl_mode() >= 1, false, s, c, out, G);
@@ -1741,13 +2083,32 @@ int launch_update_fused(const Dev& s, const Call& c, const float* grads, float l
   int push = 0;
   if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
   int xb = std::max(1, std::min(8, coop_blocks / 16));   // extraction blocks (after block 0's plan)
+  const int D4 = (int)s.D / 4;
+  int clock_only = (D4 >= 256 && D4 % 128 == 0) ? 1 : 0;   // wide rows: k_seg_wide reduces the rows first
+  int launches = 1;
+  if (clock_only) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cf->dev);
+    static const bool reg = getenv("HET_SEG_REG") != nullptr;   // A/B: the register form
+    if (reg) {
+      launch_pdl(k_seg_wide, sms * 4, 256, 0, st, pdl_mode() >= 1, false, sd, cd, grads, lr);
+    } else {
+      static bool attr = false;
+      if (!attr) { cudaFuncSetAttribute(k_seg_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TS_SMEM); attr = true; }
+      const int S = D4 / TS_SL4;   // grid: a multiple of the slices per row
+      launch_pdl(k_seg_tma, std::max(1, sms * 3 / S) * S, (TS_CW + 1) * 32, TS_SMEM, st, pdl_mode() >= 1, false, sd,
+                 cd, grads, lr);
+    }
+    launches += 1;
+  }
   void* args[] = {(void*)&sd, (void*)&cd, (void*)&grads, (void*)&lr, (void*)&b, (void*)&sr, (void*)&pm, (void*)&push,
-                  (void*)&xb};
+                  (void*)&xb, (void*)&clock_only};
   if (pdl_mode() >= 2)
-    launch_pdl(k_update_fused, coop_blocks, UPD_THREADS, smem, st, true, true, sd, cd, grads, lr, b, sr, pm, push, xb);
+    launch_pdl(k_update_fused, coop_blocks, UPD_THREADS, smem, st, true, true, sd, cd, grads, lr, b, sr, pm, push, xb,
+               clock_only);
   else
     cudaLaunchCooperativeKernel((void*)k_update_fused, dim3(coop_blocks), dim3(UPD_THREADS), args, smem, st);
-  return 1;
+  return launches;
 }
 
 }  // namespace het

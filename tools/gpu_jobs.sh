@@ -4,6 +4,7 @@
 #   bash tools/gpu_jobs.sh timeline [--reddit]   graph-replay timeline (HET_TIMELINE build, restored after)
 #   bash tools/gpu_jobs.sh timeline_mgpu   N=2 per-rank timeline, with and without the dense all-reduce
 #   bash tools/gpu_jobs.sh multi N         multi-process parity (p2p) + DCN bench lines up to N + Reddit at N
+#   bash tools/gpu_jobs.sh wide            wide-row parity (N=1 + loopback) and the scale-shaped bench line
 #   bash tools/gpu_jobs.sh bounds          parity + loopback with the bounds-checked build (HET_DIAG=HET_BOUNDS)
 #   bash tools/gpu_jobs.sh diag MACRO      timeline of a diagnostic build variant next to the normal one
 #   bash tools/gpu_jobs.sh ncu_launches    ncu launch list of 10 WDL steps (after a plain run)
@@ -45,6 +46,19 @@ multi)
   done
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29725 bench.py --gpus $N --steps 100 --warmup 5 --workload reddit > gpurun_out/bench_reddit_n$N.json 2> gpurun_out/bench_reddit_n$N.err
   summary gpurun_out/bench_reddit_n$N.json ;;
+wide)
+  python -m pytest tests/test_gpu_parity.py tests/test_gpu_loopback.py -x -q -k "scale or wide or heavy or toy_full or graph" 2>&1 | tail -3
+  timeout 600 python bench.py --steps 50 --warmup 5 --workload scale --no-sweep --no-cpu-baseline > gpurun_out/wide_bench.json 2> gpurun_out/wide_bench.err
+  summary gpurun_out/wide_bench.json
+  [ -n "${2:-}" ] && { HET_SEG_REG=1 timeout 600 python bench.py --steps 50 --warmup 5 --workload scale --no-sweep --no-cpu-baseline > gpurun_out/wide_bench_reg.json 2> gpurun_out/wide_bench_reg.err; summary gpurun_out/wide_bench_reg.json; }
+  python tools/prof_step.py --scale --steps 10 > gpurun_out/wide_plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/wide_launches.csv python tools/prof_step.py --scale --steps 10 > gpurun_out/wide_ncu.log 2>&1
+  echo ncu rc $?
+  python tools/launches.py gpurun_out/wide_launches.csv 10 ;;
+wide_full)
+  python tools/prof_step.py --scale --steps 3 > gpurun_out/plain.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"k_seg_tma|k_mv_tma" -c 2 -o gpurun_out/prof_wide python tools/prof_step.py --scale --steps 3 > gpurun_out/ncu.log 2>&1
+  tail -2 gpurun_out/ncu.log ;;
 bounds)
   python -m pytest tests/test_gpu_parity.py tests/test_gpu_loopback.py -x -q 2>&1 | tail -3 > gpurun_out/bd_normal.log
   HET_DIAG=HET_BOUNDS python -c "from paper_2112_07221_b200 import build; build.build(force=True)" >> gpurun_out/build.log 2>&1

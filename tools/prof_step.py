@@ -24,11 +24,12 @@ def main():
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--fill", type=int, default=6500)
     ap.add_argument("--policy", default="LFU")
+    ap.add_argument("--scale", action="store_true", help="BASELINE configs[4] per GPU: 3M rows, D = 4096")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    B, D = args.batch, 128
+    B, D = args.batch, (4096 if args.scale else 128)
     n = B * 26
-    cards = gen.cards_for("criteo")
+    cards = gen.scaled_cards(3_000_000) if args.scale else gen.cards_for("criteo")
     R = sum(cards)
     pol = het.HET_LFU if args.policy == "LFU" else het.HET_LRU
     c = het.HetCache(R, D, 0.1, 100, pol, max_keys_per_call=n)

@@ -18,10 +18,13 @@ from paper_2112_07221_b200 import het  # noqa: E402
 from workload import gen  # noqa: E402
 
 TLW = 8192
-B, D = 128, 128
 reddit = "--reddit" in sys.argv   # BASELINE configs[2]: 14,208 distinct node ids per step, s = 10
+scale = "--scale" in sys.argv     # BASELINE configs[4] per GPU: 3M rows, D = 4096
+B, D = 128, (4096 if scale else 128)
 n = 14208 if reddit else B * 26
 graph_mode = "--graph" in sys.argv
+if scale:
+    os.environ.setdefault("TL_ROWS", "3000000")
 cards = gen.scaled_cards(int(os.environ["TL_ROWS"])) if os.environ.get("TL_ROWS") else gen.cards_for("criteo")
 dev = torch.device("cuda", 0)
 R = gen.REDDIT_ROWS if reddit else sum(cards)
