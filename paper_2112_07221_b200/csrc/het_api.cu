@@ -117,14 +117,23 @@ static cudaError_t dalloc(het_cache* h, T** p, size_t count) {
   return e;
 }
 
+// Pointer kind, remembered for the last few pointers (a training loop passes
+// the same buffers every step; under UVA a device range stays device memory
+// and a host range host memory, so a reused address keeps its kind).
 static bool is_device_ptr(const void* p) {
   if (!p) return false;
+  struct Kind { const void* p; bool dev; };
+  thread_local Kind seen[8] = {};
+  thread_local int next = 0;
+  for (const Kind& k : seen)
+    if (k.p == p) return k.dev;
   cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  bool dev = false;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) cudaGetLastError();
+  else dev = a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  seen[next] = Kind{p, dev};
+  next = (next + 1) & 7;
+  return dev;
 }
 
 static cudaEvent_t ev_get(het_cache* h) {

@@ -1149,249 +1149,241 @@ __global__ void __launch_bounds__(256, 4) k_seg_wide(Dev s, Call c, const float*
   }
 }
 
-// The same items staged by the copy engine (BASELINE configs[4]; measured:
-// k_seg_wide keeps ~12 GB/s per SM in flight and a 128-occurrence key is 32
-// dependent load rounds on one warp).  Item = (key, 512-column slice); its
-// occurrence rows are cut into stages of <= TS_CH rows; a producer warp per
-// CTA issues one 2 KB bulk copy per row slice (cp.async.bulk, complete_tx on
-// the stage's full barrier) plus v and p (if dirty) with the item's last
-// stage; four consumer warps, a float4 column per thread, add the staged rows
-// in ascending position into a register accumulator carried across the
-// item's stages (+0.0f first, R11), then v += -lr*acc, p = (dirty ? p : +0)
-// + -lr*acc (R13) straight to HBM.  Three 20 KB stages per CTA, three CTAs
-// per SM (three producers).  Every warp walks the same item list (the
-// producer's barrier arrives are relaxed, so no header passes through shared
-// memory: a release arrive waits for the producer's copies in flight).
-constexpr int TS_SL4 = 128;          // float4 per slice (512 columns)
-constexpr int TS_CH = 8;             // occurrence rows per stage
-constexpr int TS_N = 3;              // stages per CTA (three CTAs per SM)
-constexpr int TS_CW = 4;             // consumer warps (TS_CW * 32 == TS_SL4)
-constexpr int TS_ROWS = TS_CH + 2;   // + v + p
-constexpr size_t TS_SMEM = (size_t)TS_N * TS_ROWS * TS_SL4 * 16;
+// The same work with every thread its own copy pipeline (BASELINE configs[4]).
+// Measured on B200 (tools/tma_probe.cu, random row chunks of an 8 GB table):
+// one warp issuing cp.async.bulk copies completes ~2.7 M copies/s whatever
+// the ring depth (1 KB copies: 2.8 GB/s per warp), so a key with 128
+// occurrences is ~48 us of copy issue on one warp, and bulk copies need
+// many issuing warps; plain loads reach the same plateau (~4 TB/s for 2 KB
+// chunks) but a warp holds only what its registers hold.  Here a CTA of 128
+// threads owns a 512-column slice of its items, thread t the float4 column
+// t: each thread issues 16-byte cp.async copies (LDGSTS: no register cost,
+// no depth cap) of its column of every occurrence row, v and p into its own
+// ring of row slots in shared memory, several stages ahead, one commit group
+// per stage, and consumes the oldest stage after cp.async.wait_group -- its
+// own copies, so no barrier.  A stage is <= AS_CH occurrence rows of one
+// item (+ v, p with its last); the sum runs in ascending position with the
+// accumulator carried across the item's stages (+0.0f first, R11), then
+// v += -lr*acc, p = (dirty ? p : +0) + -lr*acc (R13).  Items (key, slice) are
+// dealt as (key group, slice) = (b / S, b % S) over the CTAs.
+constexpr int AS_T = 128;     // threads per CTA = float4 columns per slice (512 columns)
+constexpr int AS_CH = 16;     // occurrence rows per stage
+constexpr int AS_QMAX = 7;    // stages in flight per thread (cp.async.wait_group immediates 0..6)
 
-// calls f(e, j0, cnt, c0, dirty, col4, l, p4) for every stage of this
-// CTA's items, in order (lane l's p4: the item's first positions).  CTA b takes
-// slice b % S of the keys u = b / S + i * Q (Q = gridDim.x / S key groups):
-// 32 keys' records per load round, heads only.
-template <class F>
-__device__ __forceinline__ void ts_walk(const Call& c, int U, int S, int lane, F&& f) {
-  const int Q = (int)gridDim.x / S, q = (int)blockIdx.x / S;
-  const int col4 = ((int)blockIdx.x % S) * TS_SL4;
-  for (int u0 = q; u0 < U; u0 += 32 * Q) {
-    const int u = u0 + lane * Q;
-    int4 rec = make_int4(-1, 0, 0, 0), p4 = make_int4(0, 0, 0, 0);
-    if (u < U) { rec = __ldcg(&c.urec[u]); p4 = __ldcg(&c.upos[u]); }
-    // rmode non-heads / capacity failures / past the end carry no work
-    for (unsigned live = __ballot_sync(0xffffffffu, rec.x >= 0); live; live &= live - 1) {
-      const int l = __ffs(live) - 1;
-      const int e = __shfl_sync(0xffffffffu, rec.x, l);
-      const int j0 = __shfl_sync(0xffffffffu, rec.y, l), z = __shfl_sync(0xffffffffu, rec.z, l);
-      const int cnt = z & 0x7FFFFFFF;
-      for (int c0 = 0; c0 < cnt; c0 += TS_CH) f(e, j0, cnt, c0, z < 0, col4, l, p4);
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait(int n) {   // at most n of this thread's groups still pending
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
+  }
+}
+
+// The stage sequence of this CTA (identical in every thread; lane-dependent
+// only in the lane's own record of the current batch of 32 keys).
+// MV: the lookup's row moves (k_mv_as): heads with an entry, one stage per item.
+template <bool MV>
+struct AsWalk {
+  int U, Q, u0;
+  int4 rec, p4;
+  int64_t key;
+  int fl;
+  unsigned live;
+  bool valid, dirty;
+  int l, e, j0, cnt, c0, m, flag;
+  int64_t ikey;
+
+  __device__ __forceinline__ void load(const Call& c, int lane) {
+    for (;;) {
+      if (u0 >= U) { valid = false; return; }
+      const int u = u0 + lane * Q;
+      rec = make_int4(-1, 0, 0, 0);
+      p4 = make_int4(0, 0, 0, 0);
+      key = 0;
+      fl = 0;
+      if (u < U) {
+        if (MV) {
+          fl = __ldcg(&c.ucnt[u]);
+          if (fl & 4) { rec = __ldcg(&c.urec[u]); p4 = __ldcg(&c.upos[u]); key = __ldcg(&c.uniq[u]); }
+        } else {
+          rec = __ldcg(&c.urec[u]);
+          p4 = __ldcg(&c.upos[u]);
+        }
+      }
+      // rmode non-heads / capacity failures / past the end carry no work
+      live = __ballot_sync(0xffffffffu, MV ? (fl & 4) != 0 : rec.x >= 0);
+      if (live) { valid = true; return; }
+      u0 += 32 * Q;
     }
   }
-}
-
-__device__ __forceinline__ void mbar_arrive_rlx(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_rlx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__global__ void __launch_bounds__((TS_CW + 1) * 32) k_seg_tma(Dev s, Call c, const float* __restrict__ G, float lr) {
-  extern __shared__ __align__(1024) float4 ring[];   // [TS_N][TS_ROWS][TS_SL4]
-  __shared__ __align__(8) uint64_t full[TS_N], empty[TS_N];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < TS_N; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], TS_CW); }
-    fence_mbar_init();
+  __device__ __forceinline__ void item() {
+    l = __ffs(live) - 1;
+    live &= live - 1;
+    e = __shfl_sync(0xffffffffu, rec.x, l);
+    j0 = __shfl_sync(0xffffffffu, rec.y, l);
+    const int z = __shfl_sync(0xffffffffu, rec.z, l);
+    cnt = z & 0x7FFFFFFF;
+    dirty = z < 0;
+    c0 = 0;
+    m = MV ? cnt : min(AS_CH, cnt);
+    if (MV) { flag = __shfl_sync(0xffffffffu, fl, l); ikey = __shfl_sync(0xffffffffu, key, l); }
+    valid = true;
   }
-  __syncthreads();
+  __device__ __forceinline__ void init(const Call& c, int U_, int Q_, int q, int lane) {
+    U = U_; Q = Q_; u0 = q;
+    load(c, lane);
+    if (valid) item();
+  }
+  __device__ __forceinline__ void next(const Call& c, int lane) {
+    if (!MV && c0 + m < cnt) { c0 += m; m = min(AS_CH, cnt - c0); return; }
+    if (!live) {
+      u0 += 32 * Q;
+      load(c, lane);
+      if (!valid) return;
+    }
+    item();
+  }
+  __device__ __forceinline__ bool last() const { return MV || c0 + m == cnt; }
+  __device__ __forceinline__ int rows() const {
+    return MV ? 1 + ((flag & 2) ? 1 : 0) : m + (c0 + m == cnt ? 1 + (dirty ? 1 : 0) : 0);
+  }
+  // this lane's occurrence position of the stage's row `lane` (rows < 32)
+  __device__ __forceinline__ int pos_lane(const Call& c, int lane, int kb) const {
+    if (cnt <= 4) {
+      const int px = __shfl_sync(0xffffffffu, p4.x, l), py = __shfl_sync(0xffffffffu, p4.y, l);
+      const int pz = __shfl_sync(0xffffffffu, p4.z, l), pw = __shfl_sync(0xffffffffu, p4.w, l);
+      return lane == 0 ? px : lane == 1 ? py : lane == 2 ? pz : pw;
+    }
+    return c0 + kb + lane < cnt ? __ldg(&c.perm[j0 + c0 + kb + lane]) : 0;
+  }
+};
+
+template <int RING>
+__device__ __forceinline__ int ring_at(int x) { return x >= RING ? x - RING : x; }
+
+template <int RING>
+__global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __restrict__ G, float lr) {
+  extern __shared__ __align__(16) float4 ring[];   // [RING][AS_T]: row slot r of thread t at r * AS_T + t
   pdl_wait();
   const Ctl* ctl = s.ctl;
   const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);
-  const int D4 = s.D >> 2, S = D4 / TS_SL4;
-  uint32_t k = 0;   // stages of this CTA
-  if (warp == TS_CW) {   // producer
-    const uint32_t SLB = TS_SL4 * 16;
-    ts_walk(c, U, S, lane, [&](int e, int j0, int cnt, int c0, bool dirty, int col4, int l, int4 p4) {
-      const int m = min(TS_CH, cnt - c0);
-      const bool last = c0 + m == cnt;
-      int pos = 0;
-      if (cnt > 4) {
-        pos = lane < m ? __ldg(&c.perm[j0 + c0 + lane]) : 0;
-      } else {
-        const int px = __shfl_sync(0xffffffffu, p4.x, l), py = __shfl_sync(0xffffffffu, p4.y, l);
-        const int pz = __shfl_sync(0xffffffffu, p4.z, l), pw = __shfl_sync(0xffffffffu, p4.w, l);
-        pos = lane == 0 ? px : lane == 1 ? py : lane == 2 ? pz : pw;
+  const int D4 = s.D >> 2, S = D4 / AS_T;
+  const int Q = (int)gridDim.x / S;
+  if ((int)blockIdx.x >= Q * S) return;
+  const int t = threadIdx.x, lane = t & 31;
+  const int col4 = ((int)blockIdx.x % S) * AS_T + t;
+  const float4* G4 = reinterpret_cast<const float4*>(G);
+  const float4* v4 = reinterpret_cast<const float4*>(s.v);
+  const float4* p4g = reinterpret_cast<const float4*>(s.p);
+  AsWalk<false> iw, cw;   // issue and consume positions in the same stage sequence
+  iw.init(c, U, Q, (int)blockIdx.x / S, lane);
+  cw.init(c, U, Q, (int)blockIdx.x / S, lane);
+  int inflight = 0, used = 0, head = 0, tail = 0;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float nlr = -lr;
+  float4 acc = zero;
+  while (cw.valid) {
+    while (iw.valid && inflight < AS_QMAX) {
+      const int rows = iw.rows();
+      if (used + rows > RING) break;
+      const int pos = iw.pos_lane(c, lane, 0);
+      for (int q = 0; q < iw.m; ++q) {
+        const int64_t pq = __shfl_sync(0xffffffffu, pos, q);
+        cp_async16(&ring[ring_at<RING>(head + q) * AS_T + t], G4 + pq * D4 + col4);
       }
-      const uint32_t sl = k % TS_N, r = k / TS_N;
-      float4* stg = ring + (size_t)sl * TS_ROWS * TS_SL4;
-      if (lane == 0) {
-        if (r > 0) mbar_wait(&empty[sl], (r - 1) & 1);
-        const uint32_t bytes = (uint32_t)m * SLB + (last ? SLB * (dirty ? 2 : 1) : 0);
-        mbar_expect_tx_rlx(&full[sl], bytes);
-        mbar_arrive_rlx(&full[sl]);
+      if (iw.last()) {
+        cp_async16(&ring[ring_at<RING>(head + iw.m) * AS_T + t], v4 + (int64_t)iw.e * D4 + col4);
+        if (iw.dirty) cp_async16(&ring[ring_at<RING>(head + iw.m + 1) * AS_T + t], p4g + (int64_t)iw.e * D4 + col4);
       }
-      for (int q = 0; q < m; ++q) {
-        const int pq = __shfl_sync(0xffffffffu, pos, q);
-        if (lane == 0) bulk_g2s(stg + q * TS_SL4, G + (int64_t)pq * s.D + col4 * 4, SLB, &full[sl]);
-      }
-      if (lane == 0 && last) {
-        bulk_g2s(stg + TS_CH * TS_SL4, s.v + (int64_t)e * s.D + col4 * 4, SLB, &full[sl]);
-        if (dirty) bulk_g2s(stg + (TS_CH + 1) * TS_SL4, s.p + (int64_t)e * s.D + col4 * 4, SLB, &full[sl]);
-      }
-      ++k;
-    });
-  } else {   // consumers: thread t owns float4 column t of the slice
-    const int t = threadIdx.x;
-    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float nlr = -lr;
-    float4 acc = zero;
-    ts_walk(c, U, S, lane, [&](int e, int j0, int cnt, int c0, bool dirty, int col4, int l, int4 p4) {
-      const int m = min(TS_CH, cnt - c0);
-      const bool last = c0 + m == cnt;
-      const uint32_t sl = k % TS_N, r = k / TS_N;
-      const float4* stg = ring + (size_t)sl * TS_ROWS * TS_SL4 + t;
-      mbar_wait(&full[sl], r & 1);
-      for (int q = 0; q < m; ++q) acc = f4add_(acc, stg[q * TS_SL4]);   // ascending position
-      float4 nv, np;
-      if (last) {
-        const float4 vv = stg[TS_CH * TS_SL4];
-        const float4 pp = dirty ? stg[(TS_CH + 1) * TS_SL4] : zero;
-        const float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
-                                      __fmul_rn(nlr, acc.w));
-        nv = f4add_(vv, dl);
-        np = f4add_(pp, dl);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_rlx(&empty[sl]);   // the stage's values are in registers (used above)
-      if (last) {
-        reinterpret_cast<float4*>(s.v + (int64_t)e * s.D)[col4 + t] = nv;
-        reinterpret_cast<float4*>(s.p + (int64_t)e * s.D)[col4 + t] = np;
-        acc = zero;
-      }
-      ++k;
-    });
-  }
-}
-
-// The wide lookup's row moves staged by the copy engine (after k_lookup_wide
-// with G = 0): item = (key, 512-column slice).  A loader warp brings the
-// slice's source -- v[e] for a hit, W[key] for a refetch or miss, and p[e]
-// when the Evict push W += p applies -- into a stage; a storer
-// warp adds W + p in shared memory for a push, then issues the bulk stores:
-// v[e] (Fetch), W[key] (the push) and the Get scatter to every
-// occurrence.  The storer frees a stage MV_LAG stages later, once the
-// bulk stores have read it (cp.async.bulk.wait_group.read).
-constexpr int MV_N = 12;       // stages per CTA (4 KB each)
-constexpr int MV_LAG = 4;      // stages whose bulk stores may still read shared memory
-constexpr int MV_CTAS = 4;     // CTAs per SM
-constexpr size_t MV_SMEM = (size_t)MV_N * 2 * TS_SL4 * 16;
-
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read_lag() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(MV_LAG) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-// ts_walk over the lookup's records: f(fl, e, key, j0, cnt, col4, l, p4) per head with an entry
-template <class F>
-__device__ __forceinline__ void mv_walk(const Call& c, int U, int S, int lane, F&& f) {
-  const int Q = (int)gridDim.x / S, q = (int)blockIdx.x / S;
-  const int col4 = ((int)blockIdx.x % S) * TS_SL4;
-  for (int u0 = q; u0 < U; u0 += 32 * Q) {
-    const int u = u0 + lane * Q;
-    int fl = 0;
-    int4 rec = make_int4(-1, 0, 0, 0), p4 = make_int4(0, 0, 0, 0);
-    int64_t key = 0;
-    if (u < U) {
-      fl = __ldcg(&c.ucnt[u]);
-      if (fl & 4) { rec = __ldcg(&c.urec[u]); p4 = __ldcg(&c.upos[u]); key = __ldcg(&c.uniq[u]); }
+      cp_async_commit();
+      ++inflight;
+      used += rows;
+      head = ring_at<RING>(head + rows);
+      iw.next(c, lane);
     }
-    for (unsigned live = __ballot_sync(0xffffffffu, fl & 4); live; live &= live - 1) {
-      const int l = __ffs(live) - 1;
-      f(__shfl_sync(0xffffffffu, fl, l), __shfl_sync(0xffffffffu, rec.x, l), __shfl_sync(0xffffffffu, key, l),
-        __shfl_sync(0xffffffffu, rec.y, l), __shfl_sync(0xffffffffu, rec.z, l) & 0x7FFFFFFF, col4, l, p4);
+    cp_async_wait(inflight - 1);   // the oldest stage has landed
+    for (int q = 0; q < cw.m; ++q) acc = f4add_(acc, ring[ring_at<RING>(tail + q) * AS_T + t]);   // ascending position
+    if (cw.last()) {
+      const float4 vv = ring[ring_at<RING>(tail + cw.m) * AS_T + t];
+      const float4 pp = cw.dirty ? ring[ring_at<RING>(tail + cw.m + 1) * AS_T + t] : zero;
+      const float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
+                                    __fmul_rn(nlr, acc.w));
+      reinterpret_cast<float4*>(s.v)[(int64_t)cw.e * D4 + col4] = f4add_(vv, dl);
+      reinterpret_cast<float4*>(s.p)[(int64_t)cw.e * D4 + col4] = f4add_(pp, dl);
+      acc = zero;
     }
+    const int rows = cw.rows();
+    --inflight;
+    used -= rows;
+    tail = ring_at<RING>(tail + rows);
+    cw.next(c, lane);
   }
 }
 
-__global__ void __launch_bounds__(64) k_mv_tma(Dev s, Call c, float* __restrict__ out) {
-  extern __shared__ __align__(1024) float4 ring[];   // [MV_N][2][TS_SL4]: source slice, p slice
-  __shared__ __align__(8) uint64_t full[MV_N], empty[MV_N];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < MV_N; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    fence_mbar_init();
-  }
-  __syncthreads();
+// The wide lookup's row moves (after k_lookup_wide with G = 0), the same
+// per-thread pipelines: the item's source slice -- v[e] for a hit, W[key]
+// for a refetch or miss, and p[e] when the Evict push W += p applies
+// -- staged by cp.async, then W + p for a push, the stores
+// v[e] = w (Fetch), W[key] = w (the push) and the Get scatter of w to
+// every occurrence.
+template <int RING>
+__global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict__ out) {
+  extern __shared__ __align__(16) float4 ring[];
   pdl_wait();
   const int U = s.ctl->abort ? 0 : c.n;   // rmode
-  const int S = (s.D >> 2) / TS_SL4;
-  const uint32_t SLB = TS_SL4 * 16;
-  uint32_t k = 0;
-  if (warp == 0) {   // loader
-    mv_walk(c, U, S, lane, [&](int fl, int e, int64_t key, int j0, int cnt, int col4, int l, int4 p4) {
-      const uint32_t sl = k % MV_N, r = k / MV_N;
-      float4* stg = ring + (size_t)sl * 2 * TS_SL4;
-      if (lane == 0) {
-        if (r > 0) mbar_wait(&empty[sl], (r - 1) & 1);
-        mbar_expect_tx_rlx(&full[sl], SLB * ((fl & 2) ? 2 : 1));
-        mbar_arrive_rlx(&full[sl]);
-        const float* src = (fl & 1) ? s.W + key * s.D : s.v + (int64_t)e * s.D;
-        bulk_g2s(stg, src + col4 * 4, SLB, &full[sl]);
-        if (fl & 2) bulk_g2s(stg + TS_SL4, s.p + (int64_t)e * s.D + col4 * 4, SLB, &full[sl]);
-      }
-      ++k;
-    });
-  } else {           // storer
-    mv_walk(c, U, S, lane, [&](int fl, int e, int64_t key, int j0, int cnt, int col4, int l, int4 p4) {
-      const uint32_t sl = k % MV_N, r = k / MV_N;
-      float4* stg = ring + (size_t)sl * 2 * TS_SL4;
-      mbar_wait(&full[sl], r & 1);
-      if (fl & 2) {   // W + p, then visible to the bulk stores
-        for (int i = lane; i < TS_SL4; i += 32) stg[i] = f4add_(stg[i], stg[TS_SL4 + i]);
-        fence_proxy_async();
-        __syncwarp();
-      }
-      if (lane == 0) {
-        if (fl & 1) bulk_s2g(s.v + (int64_t)e * s.D + col4 * 4, stg, SLB);
-        if (fl & 2) bulk_s2g(s.W + key * s.D + col4 * 4, stg, SLB);
-      }
-      if (cnt <= 4) {
-        const int pq[4] = {__shfl_sync(0xffffffffu, p4.x, l), __shfl_sync(0xffffffffu, p4.y, l),
-                           __shfl_sync(0xffffffffu, p4.z, l), __shfl_sync(0xffffffffu, p4.w, l)};
-        if (lane == 0)
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (q < cnt) bulk_s2g(out + (int64_t)pq[q] * s.D + col4 * 4, stg, SLB);
-      } else {
-        for (int kb = 0; kb < cnt; kb += 32) {
-          const int src = kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0;
-          const int m = min(32, cnt - kb);
-          for (int q = 0; q < m; ++q) {
-            const int64_t pos = __shfl_sync(0xffffffffu, src, q);
-            if (lane == 0) bulk_s2g(out + pos * s.D + col4 * 4, stg, SLB);
-          }
-        }
-      }
-      if (lane == 0) {
-        bulk_commit();
-        bulk_wait_read_lag();   // the stores of stages <= k - MV_LAG have read their stage
-        if (k >= MV_LAG) mbar_arrive_rlx(&empty[(k - MV_LAG) % MV_N]);
-      }
-      __syncwarp();
-      ++k;
-    });
-    if (lane == 0) bulk_wait_all();
+  const int D4 = s.D >> 2, S = D4 / AS_T;
+  const int Q = (int)gridDim.x / S;
+  if ((int)blockIdx.x >= Q * S) return;
+  const int t = threadIdx.x, lane = t & 31;
+  const int col4 = ((int)blockIdx.x % S) * AS_T + t;
+  float4* W4 = reinterpret_cast<float4*>(s.W);
+  float4* v4 = reinterpret_cast<float4*>(s.v);
+  const float4* p4g = reinterpret_cast<const float4*>(s.p);
+  float4* o4 = reinterpret_cast<float4*>(out);
+  AsWalk<true> iw, cw;
+  iw.init(c, U, Q, (int)blockIdx.x / S, lane);
+  cw.init(c, U, Q, (int)blockIdx.x / S, lane);
+  int inflight = 0, used = 0, head = 0, tail = 0;
+  while (cw.valid) {
+    while (iw.valid && inflight < AS_QMAX) {
+      const int rows = iw.rows();
+      if (used + rows > RING) break;
+      const float4* src = (iw.flag & 1) ? W4 + iw.ikey * D4 : v4 + (int64_t)iw.e * D4;
+      cp_async16(&ring[head * AS_T + t], src + col4);
+      if (iw.flag & 2) cp_async16(&ring[ring_at<RING>(head + 1) * AS_T + t], p4g + (int64_t)iw.e * D4 + col4);
+      cp_async_commit();
+      ++inflight;
+      used += rows;
+      head = ring_at<RING>(head + rows);
+      iw.next(c, lane);
+    }
+    cp_async_wait(inflight - 1);
+    float4 w = ring[tail * AS_T + t];
+    if (cw.flag & 2) w = f4add_(w, ring[ring_at<RING>(tail + 1) * AS_T + t]);
+    if (cw.flag & 1) v4[(int64_t)cw.e * D4 + col4] = w;
+    if (cw.flag & 2) W4[cw.ikey * D4 + col4] = w;
+    for (int kb = 0; kb < cw.cnt; kb += 32) {
+      const int pos = cw.pos_lane(c, lane, kb);
+      const int mm = min(32, cw.cnt - kb);
+      for (int q = 0; q < mm; ++q) __stcs(o4 + (int64_t)__shfl_sync(0xffffffffu, pos, q) * D4 + col4, w);
+    }
+    const int rows = cw.rows();
+    --inflight;
+    used -= rows;
+    tail = ring_at<RING>(tail + rows);
+    cw.next(c, lane);
   }
 }
+
+constexpr int AS_SEG_RING = 32, AS_SEG_CTAS = 3;   // 64 KB per CTA
+constexpr int AS_MV_RING = 16, AS_MV_CTAS = 6;     // 32 KB per CTA
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
@@ -2016,9 +2008,11 @@ int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st
         launch_pdl(k_lookup_wide_mv, sms * 8, 256, 0, st, pdl_mode() >= 1, false, s, c, out);
       } else {
         static bool attr = false;
-        if (!attr) { cudaFuncSetAttribute(k_mv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MV_SMEM); attr = true; }
-        const int S = D4 / TS_SL4;
-        launch_pdl(k_mv_tma, std::max(1, sms * MV_CTAS / S) * S, 64, MV_SMEM, st, pdl_mode() >= 1, false, s, c, out);
+        const size_t smem = (size_t)AS_MV_RING * AS_T * 16;
+        if (!attr) { cudaFuncSetAttribute(k_mv_as<AS_MV_RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+        const int S = D4 / AS_T;
+        launch_pdl(k_mv_as<AS_MV_RING>, std::max(1, sms * AS_MV_CTAS / S) * S, AS_T, smem, st, pdl_mode() >= 1, false, s,
+                   c, out);
       }
       return 2;
     }
@@ -2094,10 +2088,11 @@ int launch_update_fused(const Dev& s, const Call& c, const float* grads, float l
       launch_pdl(k_seg_wide, sms * 4, 256, 0, st, pdl_mode() >= 1, false, sd, cd, grads, lr);
     } else {
       static bool attr = false;
-      if (!attr) { cudaFuncSetAttribute(k_seg_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TS_SMEM); attr = true; }
-      const int S = D4 / TS_SL4;   // grid: a multiple of the slices per row
-      launch_pdl(k_seg_tma, std::max(1, sms * 3 / S) * S, (TS_CW + 1) * 32, TS_SMEM, st, pdl_mode() >= 1, false, sd,
-                 cd, grads, lr);
+      const size_t smem = (size_t)AS_SEG_RING * AS_T * 16;
+      if (!attr) { cudaFuncSetAttribute(k_seg_as<AS_SEG_RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+      const int S = D4 / AS_T;
+      launch_pdl(k_seg_as<AS_SEG_RING>, std::max(1, sms * AS_SEG_CTAS / S) * S, AS_T, smem, st, pdl_mode() >= 1, false,
+                 sd, cd, grads, lr);
     }
     launches += 1;
   }

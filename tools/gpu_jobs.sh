@@ -57,7 +57,7 @@ wide)
   python tools/launches.py gpurun_out/wide_launches.csv 10 ;;
 wide_full)
   python tools/prof_step.py --scale --steps 3 > gpurun_out/plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"k_seg_tma|k_mv_tma" -c 2 -o gpurun_out/prof_wide python tools/prof_step.py --scale --steps 3 > gpurun_out/ncu.log 2>&1
+  ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"k_seg_as|k_mv_as" -c 2 -o gpurun_out/prof_wide python tools/prof_step.py --scale --steps 3 > gpurun_out/ncu.log 2>&1
   tail -2 gpurun_out/ncu.log ;;
 bounds)
   python -m pytest tests/test_gpu_parity.py tests/test_gpu_loopback.py -x -q 2>&1 | tail -3 > gpurun_out/bd_normal.log
