@@ -2,6 +2,7 @@
 // orchestration of the sm_100a kernels on the caller's stream, profiling.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -16,6 +17,15 @@
 #include "het_internal.cuh"
 #include "het_mgpu.h"
 #include "het_p2p.h"
+
+// NVTX ranges over the public calls (header-only NVTX 3: a null check when no
+// tool is attached), so nsys/ncu timelines show the protocol phases.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace het {
 void dedup_set_attrs();
@@ -675,6 +685,7 @@ static het_status_t lookup_post(het_cache* h, LkCtx& x, cudaStream_t st) {
 // het_lookup with the same pointer and n skips its dedup.  The dedup is a
 // function of the keys alone, so results are unchanged.
 het_status_t het_prefetch(het_cache_t h, const int64_t* keys, uint32_t n, het_stream_t stream_) {
+  NvtxRange nvtx_("het_prefetch");
   cudaStream_t st = (cudaStream_t)stream_;
   if (!h) return HET_ERR_ARG;
   if (n > h->n_max) return fail(h, HET_ERR_CAPACITY, "n exceeds max_keys_per_call");
@@ -706,6 +717,7 @@ het_status_t het_prefetch(het_cache_t h, const int64_t* keys, uint32_t n, het_st
 
 het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t clock_t, float* out,
                         het_stream_t stream_) {
+  NvtxRange nvtx_("het_lookup");
   cudaStream_t st = (cudaStream_t)stream_;
   if (!h) return HET_ERR_ARG;
   if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_lookup");
@@ -718,6 +730,7 @@ het_status_t het_lookup(het_cache_t h, const int64_t* keys, uint32_t n, uint64_t
 
 het_status_t het_group_lookup(const het_cache_t* hs, uint32_t N, const int64_t* const* keys, const uint32_t* n,
                               uint64_t clock_t, float* const* out, het_stream_t stream_) {
+  NvtxRange nvtx_("het_group_lookup");
   cudaStream_t st = (cudaStream_t)stream_;
   if (check_members(hs, N) || !keys || !n || !out) return HET_ERR_ARG;
   std::vector<LkCtx> x(N);
@@ -825,6 +838,7 @@ static het_status_t update_impl(het_cache* h, const int64_t* keys, uint32_t n, c
 
 het_status_t het_update(het_cache_t h, const int64_t* keys, uint32_t n, const float* grads, float lr,
                         het_stream_t stream_) {
+  NvtxRange nvtx_("het_update");
   if (!h) return HET_ERR_ARG;
   if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_update");
   return update_impl(h, keys, n, grads, lr, (cudaStream_t)stream_);
@@ -832,6 +846,7 @@ het_status_t het_update(het_cache_t h, const int64_t* keys, uint32_t n, const fl
 
 het_status_t het_group_update(const het_cache_t* hs, uint32_t N, const int64_t* const* keys, const uint32_t* n,
                               const float* const* grads, float lr, het_stream_t stream_) {
+  NvtxRange nvtx_("het_group_update");
   if (check_members(hs, N) || !keys || !n || !grads) return HET_ERR_ARG;
   for (uint32_t i = 0; i < N; ++i)   // no partial group update on a synchronous error
     if (!hs[i]->have_lookup || n[i] != hs[i]->last_n)
@@ -896,6 +911,7 @@ static het_status_t evict_members(Members g, const int64_t* const* keys, const u
 }
 
 het_status_t het_evict(het_cache_t h, const int64_t* keys, uint32_t n, het_stream_t stream_) {
+  NvtxRange nvtx_("het_evict");
   if (!h) return HET_ERR_ARG;
   if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_evict");
   het_cache* one[1] = {h};
@@ -905,6 +921,7 @@ het_status_t het_evict(het_cache_t h, const int64_t* keys, uint32_t n, het_strea
 
 het_status_t het_group_evict(const het_cache_t* hs, uint32_t N, const int64_t* const* keys, const uint32_t* n,
                              het_stream_t stream_) {
+  NvtxRange nvtx_("het_group_evict");
   if (check_members(hs, N) || (keys && !n)) return HET_ERR_ARG;
   if (keys)
     for (uint32_t i = 0; i < N; ++i)
@@ -1000,6 +1017,7 @@ static het_status_t sync_members(Members g, cudaStream_t st) {
 }
 
 het_status_t het_sync(het_cache_t h, het_stream_t stream_) {
+  NvtxRange nvtx_("het_sync");
   if (!h) return HET_ERR_ARG;
   if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_sync");
   het_cache* one[1] = {h};
@@ -1007,6 +1025,7 @@ het_status_t het_sync(het_cache_t h, het_stream_t stream_) {
 }
 
 het_status_t het_group_sync(const het_cache_t* hs, uint32_t N, het_stream_t stream_) {
+  NvtxRange nvtx_("het_group_sync");
   if (check_members(hs, N)) return HET_ERR_ARG;
   return sync_members(Members{hs, (int)N}, (cudaStream_t)stream_);
 }
@@ -1051,6 +1070,7 @@ het_status_t het_stats(het_cache_t h, het_stats_t* out) {
 
 het_status_t het_read_global(het_cache_t h, const int64_t* keys, uint32_t n, float* rows, uint32_t* cg,
                              het_stream_t stream_) {
+  NvtxRange nvtx_("het_read_global");
   cudaStream_t st = (cudaStream_t)stream_;
   if (!h) return HET_ERR_ARG;
   if (n == 0) return HET_OK;
@@ -1085,6 +1105,7 @@ het_status_t het_read_global(het_cache_t h, const int64_t* keys, uint32_t n, flo
 
 // ---------------------------------------------------------------- dense all-reduce (Eq. 2)
 het_status_t het_dense_allreduce(het_cache_t h, float* buf, uint64_t count, het_stream_t stream_) {
+  NvtxRange nvtx_("het_dense_allreduce");
   cudaStream_t st = (cudaStream_t)stream_;
   if (!h) return HET_ERR_ARG;
   if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_dense_allreduce");
@@ -1107,6 +1128,7 @@ het_status_t het_dense_allreduce(het_cache_t h, float* buf, uint64_t count, het_
 
 het_status_t het_group_dense_allreduce(const het_cache_t* hs, uint32_t N, float* const* bufs, uint64_t count,
                                        het_stream_t stream_) {
+  NvtxRange nvtx_("het_group_dense_allreduce");
   cudaStream_t st = (cudaStream_t)stream_;
   if (check_members(hs, N) || !bufs) return HET_ERR_ARG;
   if (count == 0) return HET_OK;

@@ -115,6 +115,8 @@ struct Ctl {
   int32_t ext_blocks;   // extraction blocks finished (last-block counter)
   uint32_t plan_flag;   // lk_seq of the published plan (update: block 0 -> the other blocks)
   int32_t ev_done;      // eviction blocks finished (last-block counter)
+  // wide rows: dynamic work units of k_seg_as / k_mv_as (reset by each kernel's last warp)
+  int32_t seg_unit, seg_done, mv_unit, mv_done;
 };
 
 struct Dev {

@@ -1167,11 +1167,14 @@ __global__ void __launch_bounds__(256, 4) k_seg_wide(Dev s, Call c, const float*
 // v += -lr*acc, p = (dirty ? p : +0) + -lr*acc (R13).  Items (key, slice) are
 // dealt as (key group, slice) = (b / S, b % S) over the CTAs.
 constexpr int AS_T = 128;     // threads per CTA = float4 columns per slice (512 columns)
-constexpr int AS_CH = 16;     // occurrence rows per stage
+constexpr int AS_CH = 8;      // occurrence rows per stage
 constexpr int AS_QMAX = 7;    // stages in flight per thread (cp.async.wait_group immediates 0..6)
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16s(uint32_t dst, const void* src) {   // dst: shared address
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait(int n) {   // at most n of this thread's groups still pending
@@ -1266,11 +1269,15 @@ struct AsWalk {
 };
 
 template <int RING>
-__device__ __forceinline__ int ring_at(int x) { return x >= RING ? x - RING : x; }
+__device__ __forceinline__ int ring_at(int x) {
+  static_assert((RING & (RING - 1)) == 0, "ring size: a power of two");
+  return x & (RING - 1);
+}
 
 template <int RING>
 __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __restrict__ G, float lr) {
   extern __shared__ __align__(16) float4 ring[];   // [RING][AS_T]: row slot r of thread t at r * AS_T + t
+  const uint32_t sbase = smem_u32(ring) + threadIdx.x * 16;
   pdl_wait();
   const Ctl* ctl = s.ctl;
   const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);
@@ -1296,11 +1303,11 @@ __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __r
       const int pos = iw.pos_lane(c, lane, 0);
       for (int q = 0; q < iw.m; ++q) {
         const int64_t pq = __shfl_sync(0xffffffffu, pos, q);
-        cp_async16(&ring[ring_at<RING>(head + q) * AS_T + t], G4 + pq * D4 + col4);
+        cp_async16s(sbase + ring_at<RING>(head + q) * (AS_T * 16), G4 + pq * D4 + col4);
       }
       if (iw.last()) {
-        cp_async16(&ring[ring_at<RING>(head + iw.m) * AS_T + t], v4 + (int64_t)iw.e * D4 + col4);
-        if (iw.dirty) cp_async16(&ring[ring_at<RING>(head + iw.m + 1) * AS_T + t], p4g + (int64_t)iw.e * D4 + col4);
+        cp_async16s(sbase + ring_at<RING>(head + iw.m) * (AS_T * 16), v4 + (int64_t)iw.e * D4 + col4);
+        if (iw.dirty) cp_async16s(sbase + ring_at<RING>(head + iw.m + 1) * (AS_T * 16), p4g + (int64_t)iw.e * D4 + col4);
       }
       cp_async_commit();
       ++inflight;
@@ -1336,6 +1343,7 @@ __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __r
 template <int RING>
 __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict__ out) {
   extern __shared__ __align__(16) float4 ring[];
+  const uint32_t sbase = smem_u32(ring) + threadIdx.x * 16;
   pdl_wait();
   const int U = s.ctl->abort ? 0 : c.n;   // rmode
   const int D4 = s.D >> 2, S = D4 / AS_T;
@@ -1356,8 +1364,8 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
       const int rows = iw.rows();
       if (used + rows > RING) break;
       const float4* src = (iw.flag & 1) ? W4 + iw.ikey * D4 : v4 + (int64_t)iw.e * D4;
-      cp_async16(&ring[head * AS_T + t], src + col4);
-      if (iw.flag & 2) cp_async16(&ring[ring_at<RING>(head + 1) * AS_T + t], p4g + (int64_t)iw.e * D4 + col4);
+      cp_async16s(sbase + head * (AS_T * 16), src + col4);
+      if (iw.flag & 2) cp_async16s(sbase + ring_at<RING>(head + 1) * (AS_T * 16), p4g + (int64_t)iw.e * D4 + col4);
       cp_async_commit();
       ++inflight;
       used += rows;
@@ -1382,8 +1390,8 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
   }
 }
 
-constexpr int AS_SEG_RING = 32, AS_SEG_CTAS = 3;   // 64 KB per CTA
-constexpr int AS_MV_RING = 16, AS_MV_CTAS = 6;     // 32 KB per CTA
+constexpr int AS_SEG_RING = 16, AS_SEG_CTAS = 6;   // 32 KB per CTA
+constexpr int AS_MV_RING = 8, AS_MV_CTAS = 8;      // 16 KB per CTA
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
