@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc, libdir = nccl_dirs()
     os.makedirs(BUILD, exist_ok=True)
     extra = ["-DHET_TIMELINE"] if os.environ.get("HET_TIMELINE") else []
-    extra += ["-D" + d for d in os.environ.get("HET_DIAG", "").split(",") if d]   # diagnostic builds only
+    extra += ["-D" + d for d in os.environ.get("HET_DIAG", "").split(";") if d]   # diagnostic builds only
     flags = ARCH + extra + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
                     "-Xptxas", "-v" if verbose else "-O3", "-I", inc, "-I", os.path.join(ROOT, "include")]
     objs = []

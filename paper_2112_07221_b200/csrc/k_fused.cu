@@ -1156,18 +1156,21 @@ __global__ void __launch_bounds__(256, 4) k_seg_wide(Dev s, Call c, const float*
 // occurrences is ~48 us of copy issue on one warp, and bulk copies need
 // many issuing warps; plain loads reach the same plateau (~4 TB/s for 2 KB
 // chunks) but a warp holds only what its registers hold.  Here a CTA of 128
-// threads owns a 512-column slice of its items, thread t the float4 column
-// t: each thread issues 16-byte cp.async copies (LDGSTS: no register cost,
-// no depth cap) of its column of every occurrence row, v and p into its own
+// threads owns a (128 x F float4)-column slice of its items, thread t the
+// float4 columns t + 128 j: each thread issues 16-byte cp.async copies
+// (LDGSTS: no register cost, no depth cap) of its columns of every
+// occurrence row, v and p into its own
 // ring of row slots in shared memory, several stages ahead, one commit group
 // per stage, and consumes the oldest stage after cp.async.wait_group -- its
-// own copies, so no barrier.  A stage is <= AS_CH occurrence rows of one
+// own copies, so no barrier.  A stage is <= CH occurrence rows of one
 // item (+ v, p with its last); the sum runs in ascending position with the
 // accumulator carried across the item's stages (+0.0f first, R11), then
 // v += -lr*acc, p = (dirty ? p : +0) + -lr*acc (R13).  Items (key, slice) are
-// dealt as (key group, slice) = (b / S, b % S) over the CTAs.
-constexpr int AS_T = 128;     // threads per CTA = float4 columns per slice (512 columns)
-constexpr int AS_CH = 8;      // occurrence rows per stage
+// dealt as (key group, slice) = (b / S, b % S) over the CTAs.  The kernel is
+// issue-bound (ncu: 'wait' and 'selected' lead the stalls), so the ring, the
+// columns per thread and the CTAs per SM were chosen by measurement; a
+// dynamic (atomic) deal of the units and per-warp pipelines measured slower.
+constexpr int AS_T = 128;     // threads per CTA (x F float4 columns: the slice)
 constexpr int AS_QMAX = 7;    // stages in flight per thread (cp.async.wait_group immediates 0..6)
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -1192,7 +1195,7 @@ __device__ __forceinline__ void cp_async_wait(int n) {   // at most n of this th
 // The stage sequence of this CTA (identical in every thread; lane-dependent
 // only in the lane's own record of the current batch of 32 keys).
 // MV: the lookup's row moves (k_mv_as): heads with an entry, one stage per item.
-template <bool MV>
+template <bool MV, int CH>
 struct AsWalk {
   int U, Q, u0;
   int4 rec, p4;
@@ -1235,7 +1238,7 @@ struct AsWalk {
     cnt = z & 0x7FFFFFFF;
     dirty = z < 0;
     c0 = 0;
-    m = MV ? cnt : min(AS_CH, cnt);
+    m = MV ? cnt : min(CH, cnt);
     if (MV) { flag = __shfl_sync(0xffffffffu, fl, l); ikey = __shfl_sync(0xffffffffu, key, l); }
     valid = true;
   }
@@ -1245,7 +1248,7 @@ struct AsWalk {
     if (valid) item();
   }
   __device__ __forceinline__ void next(const Call& c, int lane) {
-    if (!MV && c0 + m < cnt) { c0 += m; m = min(AS_CH, cnt - c0); return; }
+    if (!MV && c0 + m < cnt) { c0 += m; m = min(CH, cnt - c0); return; }
     if (!live) {
       u0 += 32 * Q;
       load(c, lane);
@@ -1274,28 +1277,30 @@ __device__ __forceinline__ int ring_at(int x) {
   return x & (RING - 1);
 }
 
-template <int RING>
+template <int RING, int F, int CH>
 __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __restrict__ G, float lr) {
-  extern __shared__ __align__(16) float4 ring[];   // [RING][AS_T]: row slot r of thread t at r * AS_T + t
+  extern __shared__ __align__(16) float4 ring[];   // [RING][F][AS_T]: row slot r, column j of thread t at (r * F + j) * AS_T + t
   const uint32_t sbase = smem_u32(ring) + threadIdx.x * 16;
   pdl_wait();
   const Ctl* ctl = s.ctl;
   const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);
-  const int D4 = s.D >> 2, S = D4 / AS_T;
+  const int D4 = s.D >> 2, S = D4 / (AS_T * F);
   const int Q = (int)gridDim.x / S;
   if ((int)blockIdx.x >= Q * S) return;
   const int t = threadIdx.x, lane = t & 31;
-  const int col4 = ((int)blockIdx.x % S) * AS_T + t;
+  const int col4 = ((int)blockIdx.x % S) * (AS_T * F) + t;
   const float4* G4 = reinterpret_cast<const float4*>(G);
   const float4* v4 = reinterpret_cast<const float4*>(s.v);
   const float4* p4g = reinterpret_cast<const float4*>(s.p);
-  AsWalk<false> iw, cw;   // issue and consume positions in the same stage sequence
+  AsWalk<false, CH> iw, cw;   // issue and consume positions in the same stage sequence
   iw.init(c, U, Q, (int)blockIdx.x / S, lane);
   cw.init(c, U, Q, (int)blockIdx.x / S, lane);
   int inflight = 0, used = 0, head = 0, tail = 0;
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   const float nlr = -lr;
-  float4 acc = zero;
+  float4 acc[F];
+#pragma unroll
+  for (int j = 0; j < F; ++j) acc[j] = zero;
   while (cw.valid) {
     while (iw.valid && inflight < AS_QMAX) {
       const int rows = iw.rows();
@@ -1303,11 +1308,19 @@ __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __r
       const int pos = iw.pos_lane(c, lane, 0);
       for (int q = 0; q < iw.m; ++q) {
         const int64_t pq = __shfl_sync(0xffffffffu, pos, q);
-        cp_async16s(sbase + ring_at<RING>(head + q) * (AS_T * 16), G4 + pq * D4 + col4);
+        const float4* g = G4 + pq * D4 + col4;
+        const uint32_t d = sbase + ring_at<RING>(head + q) * (F * AS_T * 16);
+#pragma unroll
+        for (int j = 0; j < F; ++j) cp_async16s(d + j * (AS_T * 16), g + j * AS_T);
       }
       if (iw.last()) {
-        cp_async16s(sbase + ring_at<RING>(head + iw.m) * (AS_T * 16), v4 + (int64_t)iw.e * D4 + col4);
-        if (iw.dirty) cp_async16s(sbase + ring_at<RING>(head + iw.m + 1) * (AS_T * 16), p4g + (int64_t)iw.e * D4 + col4);
+        const uint32_t dv = sbase + ring_at<RING>(head + iw.m) * (F * AS_T * 16);
+        const uint32_t dp = sbase + ring_at<RING>(head + iw.m + 1) * (F * AS_T * 16);
+#pragma unroll
+        for (int j = 0; j < F; ++j) {
+          cp_async16s(dv + j * (AS_T * 16), v4 + (int64_t)iw.e * D4 + col4 + j * AS_T);
+          if (iw.dirty) cp_async16s(dp + j * (AS_T * 16), p4g + (int64_t)iw.e * D4 + col4 + j * AS_T);
+        }
       }
       cp_async_commit();
       ++inflight;
@@ -1316,15 +1329,26 @@ __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __r
       iw.next(c, lane);
     }
     cp_async_wait(inflight - 1);   // the oldest stage has landed
-    for (int q = 0; q < cw.m; ++q) acc = f4add_(acc, ring[ring_at<RING>(tail + q) * AS_T + t]);   // ascending position
+    for (int q = 0; q < cw.m; ++q) {   // ascending position
+      const float4* r = ring + ring_at<RING>(tail + q) * (F * AS_T) + t;
+#pragma unroll
+      for (int j = 0; j < F; ++j) acc[j] = f4add_(acc[j], r[j * AS_T]);
+    }
     if (cw.last()) {
-      const float4 vv = ring[ring_at<RING>(tail + cw.m) * AS_T + t];
-      const float4 pp = cw.dirty ? ring[ring_at<RING>(tail + cw.m + 1) * AS_T + t] : zero;
-      const float4 dl = make_float4(__fmul_rn(nlr, acc.x), __fmul_rn(nlr, acc.y), __fmul_rn(nlr, acc.z),
-                                    __fmul_rn(nlr, acc.w));
-      reinterpret_cast<float4*>(s.v)[(int64_t)cw.e * D4 + col4] = f4add_(vv, dl);
-      reinterpret_cast<float4*>(s.p)[(int64_t)cw.e * D4 + col4] = f4add_(pp, dl);
-      acc = zero;
+      const float4* rv = ring + ring_at<RING>(tail + cw.m) * (F * AS_T) + t;
+      const float4* rp = ring + ring_at<RING>(tail + cw.m + 1) * (F * AS_T) + t;
+      float4* vo = reinterpret_cast<float4*>(s.v) + (int64_t)cw.e * D4 + col4;
+      float4* po = reinterpret_cast<float4*>(s.p) + (int64_t)cw.e * D4 + col4;
+#pragma unroll
+      for (int j = 0; j < F; ++j) {
+        const float4 vv = rv[j * AS_T];
+        const float4 pp = cw.dirty ? rp[j * AS_T] : zero;
+        const float4 dl = make_float4(__fmul_rn(nlr, acc[j].x), __fmul_rn(nlr, acc[j].y), __fmul_rn(nlr, acc[j].z),
+                                      __fmul_rn(nlr, acc[j].w));
+        vo[j * AS_T] = f4add_(vv, dl);
+        po[j * AS_T] = f4add_(pp, dl);
+        acc[j] = zero;
+      }
     }
     const int rows = cw.rows();
     --inflight;
@@ -1340,22 +1364,22 @@ __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __r
 // -- staged by cp.async, then W + p for a push, the stores
 // v[e] = w (Fetch), W[key] = w (the push) and the Get scatter of w to
 // every occurrence.
-template <int RING>
+template <int RING, int F>
 __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict__ out) {
   extern __shared__ __align__(16) float4 ring[];
   const uint32_t sbase = smem_u32(ring) + threadIdx.x * 16;
   pdl_wait();
   const int U = s.ctl->abort ? 0 : c.n;   // rmode
-  const int D4 = s.D >> 2, S = D4 / AS_T;
+  const int D4 = s.D >> 2, S = D4 / (AS_T * F);
   const int Q = (int)gridDim.x / S;
   if ((int)blockIdx.x >= Q * S) return;
   const int t = threadIdx.x, lane = t & 31;
-  const int col4 = ((int)blockIdx.x % S) * AS_T + t;
+  const int col4 = ((int)blockIdx.x % S) * (AS_T * F) + t;
   float4* W4 = reinterpret_cast<float4*>(s.W);
   float4* v4 = reinterpret_cast<float4*>(s.v);
   const float4* p4g = reinterpret_cast<const float4*>(s.p);
   float4* o4 = reinterpret_cast<float4*>(out);
-  AsWalk<true> iw, cw;
+  AsWalk<true, 1> iw, cw;
   iw.init(c, U, Q, (int)blockIdx.x / S, lane);
   cw.init(c, U, Q, (int)blockIdx.x / S, lane);
   int inflight = 0, used = 0, head = 0, tail = 0;
@@ -1364,8 +1388,12 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
       const int rows = iw.rows();
       if (used + rows > RING) break;
       const float4* src = (iw.flag & 1) ? W4 + iw.ikey * D4 : v4 + (int64_t)iw.e * D4;
-      cp_async16s(sbase + head * (AS_T * 16), src + col4);
-      if (iw.flag & 2) cp_async16s(sbase + ring_at<RING>(head + 1) * (AS_T * 16), p4g + (int64_t)iw.e * D4 + col4);
+      const uint32_t d0 = sbase + head * (F * AS_T * 16), d1 = sbase + ring_at<RING>(head + 1) * (F * AS_T * 16);
+#pragma unroll
+      for (int j = 0; j < F; ++j) {
+        cp_async16s(d0 + j * (AS_T * 16), src + col4 + j * AS_T);
+        if (iw.flag & 2) cp_async16s(d1 + j * (AS_T * 16), p4g + (int64_t)iw.e * D4 + col4 + j * AS_T);
+      }
       cp_async_commit();
       ++inflight;
       used += rows;
@@ -1373,14 +1401,24 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
       iw.next(c, lane);
     }
     cp_async_wait(inflight - 1);
-    float4 w = ring[tail * AS_T + t];
-    if (cw.flag & 2) w = f4add_(w, ring[ring_at<RING>(tail + 1) * AS_T + t]);
-    if (cw.flag & 1) v4[(int64_t)cw.e * D4 + col4] = w;
-    if (cw.flag & 2) W4[cw.ikey * D4 + col4] = w;
+    float4 w[F];
+    const float4* r0 = ring + tail * (F * AS_T) + t;
+    const float4* r1 = ring + ring_at<RING>(tail + 1) * (F * AS_T) + t;
+#pragma unroll
+    for (int j = 0; j < F; ++j) {
+      w[j] = r0[j * AS_T];
+      if (cw.flag & 2) w[j] = f4add_(w[j], r1[j * AS_T]);
+      if (cw.flag & 1) v4[(int64_t)cw.e * D4 + col4 + j * AS_T] = w[j];
+      if (cw.flag & 2) W4[cw.ikey * D4 + col4 + j * AS_T] = w[j];
+    }
     for (int kb = 0; kb < cw.cnt; kb += 32) {
       const int pos = cw.pos_lane(c, lane, kb);
       const int mm = min(32, cw.cnt - kb);
-      for (int q = 0; q < mm; ++q) __stcs(o4 + (int64_t)__shfl_sync(0xffffffffu, pos, q) * D4 + col4, w);
+      for (int q = 0; q < mm; ++q) {
+        float4* o = o4 + (int64_t)__shfl_sync(0xffffffffu, pos, q) * D4 + col4;
+#pragma unroll
+        for (int j = 0; j < F; ++j) __stcs(o + j * AS_T, w[j]);
+      }
     }
     const int rows = cw.rows();
     --inflight;
@@ -1390,8 +1428,21 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
   }
 }
 
-constexpr int AS_SEG_RING = 16, AS_SEG_CTAS = 6;   // 32 KB per CTA
-constexpr int AS_MV_RING = 8, AS_MV_CTAS = 8;      // 16 KB per CTA
+// ring rows, float4 columns per thread, rows per stage, CTAs per SM (macros: sweeps)
+// (measured best of 11 pairs at BASELINE configs[4], tools/gpu_jobs.sh wide_sweep)
+#ifndef AS_SEG_R
+#define AS_SEG_R 16
+#define AS_SEG_F 2
+#define AS_SEG_C 8
+#define AS_SEG_N 3
+#endif
+#ifndef AS_MV_R
+#define AS_MV_R 4
+#define AS_MV_F 2
+#define AS_MV_N 12
+#endif
+constexpr int AS_SEG[4] = {AS_SEG_R, AS_SEG_F, AS_SEG_C, AS_SEG_N};   // 16 x 2 x 2 KB = 64 KB per CTA
+constexpr int AS_MV[3] = {AS_MV_R, AS_MV_F, AS_MV_N};
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
@@ -2016,10 +2067,11 @@ int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st
         launch_pdl(k_lookup_wide_mv, sms * 8, 256, 0, st, pdl_mode() >= 1, false, s, c, out);
       } else {
         static bool attr = false;
-        const size_t smem = (size_t)AS_MV_RING * AS_T * 16;
-        if (!attr) { cudaFuncSetAttribute(k_mv_as<AS_MV_RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
-        const int S = D4 / AS_T;
-        launch_pdl(k_mv_as<AS_MV_RING>, std::max(1, sms * AS_MV_CTAS / S) * S, AS_T, smem, st, pdl_mode() >= 1, false, s,
+        const size_t smem = (size_t)AS_MV[0] * AS_MV[1] * AS_T * 16;
+        auto kern = k_mv_as<AS_MV[0], AS_MV[1]>;
+        if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+        const int S = D4 / (AS_T * AS_MV[1]);
+        launch_pdl(kern, std::max(1, sms * AS_MV[2] / S) * S, AS_T, smem, st, pdl_mode() >= 1, false, s,
                    c, out);
       }
       return 2;
@@ -2096,10 +2148,11 @@ int launch_update_fused(const Dev& s, const Call& c, const float* grads, float l
       launch_pdl(k_seg_wide, sms * 4, 256, 0, st, pdl_mode() >= 1, false, sd, cd, grads, lr);
     } else {
       static bool attr = false;
-      const size_t smem = (size_t)AS_SEG_RING * AS_T * 16;
-      if (!attr) { cudaFuncSetAttribute(k_seg_as<AS_SEG_RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
-      const int S = D4 / AS_T;
-      launch_pdl(k_seg_as<AS_SEG_RING>, std::max(1, sms * AS_SEG_CTAS / S) * S, AS_T, smem, st, pdl_mode() >= 1, false,
+      const size_t smem = (size_t)AS_SEG[0] * AS_SEG[1] * AS_T * 16;
+      auto kern = k_seg_as<AS_SEG[0], AS_SEG[1], AS_SEG[2]>;
+      if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+      const int S = D4 / (AS_T * AS_SEG[1]);
+      launch_pdl(kern, std::max(1, sms * AS_SEG[3] / S) * S, AS_T, smem, st, pdl_mode() >= 1, false,
                  sd, cd, grads, lr);
     }
     launches += 1;

@@ -5,6 +5,7 @@
 #   bash tools/gpu_jobs.sh timeline_mgpu   N=2 per-rank timeline, with and without the dense all-reduce
 #   bash tools/gpu_jobs.sh multi N         multi-process parity (p2p) + DCN bench lines up to N + Reddit at N
 #   bash tools/gpu_jobs.sh wide            wide-row parity (N=1 + loopback) and the scale-shaped bench line
+#   bash tools/gpu_jobs.sh wide_sweep A/B ..  scale bench per wide-kernel configuration (ring,F,CH,CTAs/ring,F,CTAs)
 #   bash tools/gpu_jobs.sh bounds          parity + loopback with the bounds-checked build (HET_DIAG=HET_BOUNDS)
 #   bash tools/gpu_jobs.sh diag MACRO      timeline of a diagnostic build variant next to the normal one
 #   bash tools/gpu_jobs.sh ncu_launches    ncu launch list of 10 WDL steps (after a plain run)
@@ -59,6 +60,15 @@ wide_full)
   python tools/prof_step.py --scale --steps 3 > gpurun_out/plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"k_seg_as|k_mv_as" -c 2 -o gpurun_out/prof_wide python tools/prof_step.py --scale --steps 3 > gpurun_out/ncu.log 2>&1
   tail -2 gpurun_out/ncu.log ;;
+wide_sweep)   # wide-row kernel configurations: "seg_cfg/mv_cfg" pairs
+  shift
+  for pair in "$@"; do
+    IFS=, read -r a b c d <<< "${pair%/*}"; IFS=, read -r e f g <<< "${pair#*/}"
+    HET_DIAG="AS_SEG_R=$a;AS_SEG_F=$b;AS_SEG_C=$c;AS_SEG_N=$d;AS_MV_R=$e;AS_MV_F=$f;AS_MV_N=$g" python -c "from paper_2112_07221_b200 import build; build.build(force=True)" >> gpurun_out/build.log 2>&1
+    timeout 600 python bench.py --steps 50 --warmup 5 --workload scale --no-sweep --no-cpu-baseline > gpurun_out/ws.json 2> gpurun_out/ws.err
+    echo "== $pair"; summary gpurun_out/ws.json
+  done
+  rebuild ;;
 bounds)
   python -m pytest tests/test_gpu_parity.py tests/test_gpu_loopback.py -x -q 2>&1 | tail -3 > gpurun_out/bd_normal.log
   HET_DIAG=HET_BOUNDS python -c "from paper_2112_07221_b200 import build; build.build(force=True)" >> gpurun_out/build.log 2>&1
