@@ -180,7 +180,7 @@ def barrier(world, device):
 
 
 # ----------------------------------------------------------------------------- algorithmic bytes
-def algorithmic_bytes(kernel, s, D, n_steps, resident):
+def algorithmic_bytes(kernel, s, D, n_steps, resident, phases=()):
     """Algorithmic bytes per launch of one kernel:
     the bytes the method must move, from the per-step counters s (totals over
     n_steps): n occurrences, U unique, m misses, v expired, e evictions."""
@@ -213,7 +213,16 @@ def algorithmic_bytes(kernel, s, D, n_steps, resident):
         # exchange_fused: the local HBM side of the round (records over NVLink not counted)
         return sum(algorithmic_bytes(k, s, D, n_steps, resident) for k in ("probe", "sync_fetch", "gather"))
     if kernel == "update_fused":
+        if "seg_wide" in phases:      # wide rows: k_seg_as reduced the rows; this kernel steps clocks + evicts
+            return algorithmic_bytes("evict", s, D, n_steps, resident)
         return sum(algorithmic_bytes(k, s, D, n_steps, resident) for k in ("segreduce_apply", "evict"))
+    # wide rows (D >= 1024): the lookup's decisions, its row moves, the ordered segment reduce
+    if kernel == "lookup_dec":
+        return algorithmic_bytes("probe", s, D, n_steps, resident)
+    if kernel == "lookup_mv":
+        return sum(algorithmic_bytes(k, s, D, n_steps, resident) for k in ("sync_fetch", "gather"))
+    if kernel == "seg_wide":
+        return algorithmic_bytes("segreduce_apply", s, D, n_steps, resident)
     return None
 
 
@@ -368,7 +377,7 @@ def run_gpu(args):
     hbm, peak_kind = peaks()
     kern = {}
     for name, (tot_ms, cnt) in prof.items():
-        ab = algorithmic_bytes(name, pd, D, K, resident)
+        ab = algorithmic_bytes(name, pd, D, K, resident, phases=set(prof))
         avg = tot_ms / max(cnt, 1)
         kern[name] = dict(ms_per_launch=avg, launches=cnt, share=None,
                           achieved_gbs=(ab / (avg * 1e-3) / 1e9) if ab else None)

@@ -612,8 +612,7 @@ static het_status_t lookup_body(het_cache* h, LkCtx& x, cudaStream_t st) {
   Call& c = h->call;
   if (h->fused) {
     if (d.world == 1) {
-      Prof p(h, "lookup_fused", st);
-      h->launches += launch_lookup_fused(d, c, x.dout, st);
+      h->launches += launch_lookup_fused(d, c, x.dout, st, h);   // records its phases when profiling
     } else {
       Prof p(h, "exchange_fused", st);
       h->launches += p2p_round_fused(p2p_of(h), d, c, x.dout, st);
@@ -815,8 +814,7 @@ static het_status_t update_impl(het_cache* h, const int64_t* keys, uint32_t n, c
     grads = h->stage_rows;
   }
   if (h->fused) {
-    Prof p(h, "update_fused", st);
-    h->launches += launch_update_fused(d, h->call, grads, lr, h->evbuf_host, st, p2p_view(h));
+    h->launches += launch_update_fused(d, h->call, grads, lr, h->evbuf_host, st, p2p_view(h), h);
     h->overflow_bound = 0;
     h->ev_pending = true;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;

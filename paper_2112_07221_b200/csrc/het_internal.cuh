@@ -532,11 +532,12 @@ int launch_begin_evict(const Dev& s, const Call& c, int n, uint64_t t, cudaStrea
 int launch_dd_bucket(const Dev& s, const Call& c, int n, int pbits, uint64_t t, int lookup, cudaStream_t st,
                      void* evbuf, const void* p2pview, bool evict);
 constexpr int RMODE_MAX = 16384;   // rmode dedups serve n <= this
-int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st);
+// prof: the handle when phase profiling is on (het_profile_enable), else nullptr
+int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st, void* prof = nullptr);
 // SMs left free by the cooperative kernels for NCCL's blocks at N > 1
 // (= NCCL's maxCTAs and the peer-memory dense all-reduce grid; env HET_NCCL_CTAS, default 16)
 int coop_sm_reserve();
 int launch_update_fused(const Dev& s, const Call& c, const float* grads, float lr, void* evbuf, cudaStream_t st,
-                        const void* p2pview = nullptr);
+                        const void* p2pview = nullptr, void* prof = nullptr);
 
 }  // namespace het

@@ -28,6 +28,7 @@
 
 #include "evict_dev.cuh"
 #include "p2p_dev.cuh"
+#include "het_mgpu.h"   // prof_begin / prof_end
 
 namespace het {
 
@@ -75,7 +76,6 @@ constexpr int DDF_THREADS = 512;
 constexpr int DDF_WARPS = DDF_THREADS / 32;
 constexpr int DDF_ITEMS = 16;   // FUSED_MAX / DDF_THREADS (elements per lane in the finish)
 constexpr int LK_WARPS = 8;
-constexpr int SW_F4 = 64;   // wide rows: float4 per slice (256 columns), two per lane
 constexpr int UPD_THREADS = 256;
 constexpr int UPD_WARPS = UPD_THREADS / 32;
 
@@ -867,56 +867,6 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
   }
 }
 
-// The row moves of the wide lookup (after k_lookup_wide with G = 0): warp per
-// (key, 256-column slice) item -- the Evict push W += p of a dirty expired
-// entry, the Fetch v = W of a refetch or miss, and the
-// Get scatter of the slice to every occurrence -- at full occupancy.
-// Per column the same operations in the same order as the one-kernel form.
-__global__ void __launch_bounds__(256) k_lookup_wide_mv(Dev s, Call c, float* __restrict__ out) {
-  pdl_wait();
-  const Ctl* ctl = s.ctl;
-  const int U = ctl->abort ? 0 : c.n;   // rmode
-  const int D4 = s.D >> 2, S = D4 / SW_F4;
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  float4* o4 = reinterpret_cast<float4*>(out);
-  for (int it = gw; it < U * S; it += nw) {
-    const int u = it / S;
-    const int fl = __ldcg(&c.ucnt[u]);
-    if (!(fl & 4)) continue;   // not a head / no entry
-    const int4 rec = __ldcg(&c.urec[u]);
-    const int32_t e = rec.x;
-    const int j0 = rec.y, cnt = rec.z & 0x7FFFFFFF;
-    const int base = (it % S) * SW_F4 + lane;
-    float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
-    float4 val[2];
-    if (fl & 1) {
-      const int64_t key = __ldcg(&c.uniq[u]);
-      float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
-      const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        float4 w = Wr[base + 32 * j];
-        if (fl & 2) { w = f4add_(w, pr[base + 32 * j]); Wr[base + 32 * j] = w; }
-        vr[base + 32 * j] = w;
-        val[j] = w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) val[j] = vr[base + 32 * j];
-    }
-    for (int kb = 0; kb < cnt; kb += 32) {
-      const int src = kb + lane < cnt ? c.perm[j0 + kb + lane] : 0;
-      const int m = min(32, cnt - kb);
-      for (int k = 0; k < m; ++k) {
-        const int64_t pos = __shfl_sync(0xffffffffu, src, k);
-#pragma unroll
-        for (int j = 0; j < 2; ++j) __stcs(o4 + pos * D4 + base + 32 * j, val[j]);
-      }
-    }
-  }
-}
-
 // ------------------------------------------------------------------ K_upd
 // Evict push of one resident entry at N = 1 (warp-cooperative) + delete + free
 // push != nullptr (N > 1): the Evict push goes to the owner's inbox, carried
@@ -1068,88 +1018,9 @@ __device__ __forceinline__ void segreduce_key(const Dev& s, const Call& c, const
 }
 
 // Wide rows (D >= 1024, BASELINE configs[4]: 16 KB rows): the ordered
-// segment reduce + SGD + pending of every (key, 256-column slice) item, warp
-// per item, in its own kernel so that it runs at 4 blocks per SM (the
-// cooperative update holds 2): per column the order is unchanged (+0.0f, then
-// ascending batch position, R11).  Each lane keeps two columns; with <= 4
-// occurrences their positions come with the lookup's record and every
-// occurrence slice, v and p are in flight at once, and the next item's record
-// loads while this one is reduced.  The clock step follows in k_update_fused.
-__global__ void __launch_bounds__(256, 4) k_seg_wide(Dev s, Call c, const float* __restrict__ G, float lr) {
-  pdl_wait();
-  const Ctl* ctl = s.ctl;
-  const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);
-  const int D4 = s.D >> 2, S = D4 / SW_F4;
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  const float4* G4 = reinterpret_cast<const float4*>(G);
-  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float nlr = -lr;
-  const int items = U * S;
-  int4 rec = make_int4(-1, 0, 0, 0), p4 = make_int4(0, 0, 0, 0);
-  if (gw < items) { rec = __ldcg(&c.urec[gw / S]); p4 = __ldcg(&c.upos[gw / S]); }
-  for (int it = gw; it < items; it += nw) {
-    const int nx = it + nw;
-    int4 rn = make_int4(-1, 0, 0, 0), pn = make_int4(0, 0, 0, 0);
-    if (nx < items) { rn = __ldcg(&c.urec[nx / S]); pn = __ldcg(&c.upos[nx / S]); }
-    const int32_t e = rec.x;
-    if (e >= 0) {   // rmode: non-heads carry no work
-      const int j0 = rec.y, cnt = rec.z & 0x7FFFFFFF;
-      const bool dirty = rec.z < 0;
-      const int base = (it % S) * SW_F4 + lane;
-      float4* vr = reinterpret_cast<float4*>(s.v + (int64_t)e * s.D);
-      float4* pr = reinterpret_cast<float4*>(s.p + (int64_t)e * s.D);
-      float4 acc[2] = {zero, zero};
-      if (cnt <= 4) {
-        const int pq[4] = {p4.x, p4.y, p4.z, p4.w};
-        float4 g[4][2];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) g[q][j] = q < cnt ? __ldcs(G4 + (int64_t)pq[q] * D4 + base + 32 * j) : zero;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q < cnt) {
-#pragma unroll
-            for (int j = 0; j < 2; ++j) acc[j] = f4add_(acc[j], g[q][j]);
-          }
-      } else {
-        for (int kb = 0; kb < cnt; kb += 32) {
-          const int src = kb + lane < cnt ? __ldg(&c.perm[j0 + kb + lane]) : 0;
-          const int m = min(32, cnt - kb);
-          for (int k = 0; k < m; k += 4) {
-            float4 g[4][2];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int pq = __shfl_sync(0xffffffffu, src, min(k + q, m - 1));
-#pragma unroll
-              for (int j = 0; j < 2; ++j) g[q][j] = k + q < m ? __ldcs(G4 + (int64_t)pq * D4 + base + 32 * j) : zero;
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (k + q < m) {
-#pragma unroll
-                for (int j = 0; j < 2; ++j) acc[j] = f4add_(acc[j], g[q][j]);
-              }
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const float4 vv = vr[base + 32 * j];
-        const float4 pp = dirty ? pr[base + 32 * j] : zero;
-        const float4 dl = make_float4(__fmul_rn(nlr, acc[j].x), __fmul_rn(nlr, acc[j].y), __fmul_rn(nlr, acc[j].z),
-                                      __fmul_rn(nlr, acc[j].w));
-        vr[base + 32 * j] = f4add_(vv, dl);
-        pr[base + 32 * j] = f4add_(pp, dl);
-      }
-    }
-    rec = rn;
-    p4 = pn;
-  }
-}
-
-// The same work with every thread its own copy pipeline (BASELINE configs[4]).
+// segment reduce + SGD + pending of every (key, slice) item in its own kernel
+// (k_seg_as) ahead of the cooperative update, which then steps the clocks.
+// Every thread is its own copy pipeline.
 // Measured on B200 (tools/tma_probe.cu, random row chunks of an 8 GB table):
 // one warp issuing cp.async.bulk copies completes ~2.7 M copies/s whatever
 // the ring depth (1 KB copies: 2.8 GB/s per warp), so a key with 128
@@ -2053,38 +1924,40 @@ static void launch_pdl(void (*k)(KArgs...), int blocks, int threads, size_t smem
   cudaLaunchKernelEx(&cfg, k, args...);
 }
 
-int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st) {
+int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st, void* prof) {
   const int D4 = (int)s.D / 4;
   if (D4 >= 256 && D4 % 128 == 0) {            // wide rows
-    if (c.rmode) {   // decisions (warp per key), then the row moves (warp per key slice)
+    if (c.rmode) {   // decisions (warp per key), then the row moves (per-thread copy pipelines)
       const int blocks = std::max(1, (c.n + LK_WARPS - 1) / LK_WARPS);
+      void* pr = prof_begin(prof, "lookup_dec", st);
       launch_pdl(k_lookup_wide, blocks, LK_WARPS * 32, 0, st, pdl_mode() >= 1, false, s, c, out, 0);
+      prof_end(prof, pr, st);
       int dev = 0, sms = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      static const bool reg = getenv("HET_MV_REG") != nullptr;   // A/B: the register form
-      if (reg) {
-        launch_pdl(k_lookup_wide_mv, sms * 8, 256, 0, st, pdl_mode() >= 1, false, s, c, out);
-      } else {
-        static bool attr = false;
-        const size_t smem = (size_t)AS_MV[0] * AS_MV[1] * AS_T * 16;
-        auto kern = k_mv_as<AS_MV[0], AS_MV[1]>;
-        if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
-        const int S = D4 / (AS_T * AS_MV[1]);
-        launch_pdl(kern, std::max(1, sms * AS_MV[2] / S) * S, AS_T, smem, st, pdl_mode() >= 1, false, s,
-                   c, out);
-      }
+      static bool attr = false;
+      const size_t smem = (size_t)AS_MV[0] * AS_MV[1] * AS_T * 16;
+      auto kern = k_mv_as<AS_MV[0], AS_MV[1]>;
+      if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+      const int S = D4 / (AS_T * AS_MV[1]);
+      pr = prof_begin(prof, "lookup_mv", st);
+      launch_pdl(kern, std::max(1, sms * AS_MV[2] / S) * S, AS_T, smem, st, pdl_mode() >= 1, false, s, c, out);
+      prof_end(prof, pr, st);
       return 2;
     }
     int G = 1;   // G warps per key (a power of two), decisions and moves in one kernel
     while (G * 2 <= std::min(LK_WARPS, D4 / 128)) G *= 2;
     const int blocks = std::max(1, (c.n + LK_WARPS / G - 1) / (LK_WARPS / G));
+    void* pr = prof_begin(prof, "lookup_fused", st);
     launch_pdl(k_lookup_wide, blocks, LK_WARPS * 32, 0, st, pdl_mode() >= 1, false, s, c, out, G);
+    prof_end(prof, pr, st);
     return 1;
   }
   int blocks = std::max(1, (c.n + LK_WARPS - 1) / LK_WARPS);
   const int agg = c.n > FUSED_MAX_DD_RANK;   // many misses: block-aggregated free-stack pops
+  void* pr = prof_begin(prof, "lookup_fused", st);
   launch_pdl(k_lookup_fused, blocks, LK_WARPS * 32, 0, st, pdl_mode() >= 1, false, s, c, out, agg);
+  prof_end(prof, pr, st);
   return 1;
 }
 
@@ -2102,7 +1975,7 @@ int coop_sm_reserve() {
 struct UpdCfg { int dev; bool multi; uint32_t D; int blocks; size_t smem; int stage_rows; };
 
 int launch_update_fused(const Dev& s, const Call& c, const float* grads, float lr, void* evbuf, cudaStream_t st,
-                        const void* p2pview) {
+                        const void* p2pview, void* prof) {
   static std::vector<UpdCfg> cfgs;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -2138,32 +2011,30 @@ int launch_update_fused(const Dev& s, const Call& c, const float* grads, float l
   if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
   int xb = std::max(1, std::min(8, coop_blocks / 16));   // extraction blocks (after block 0's plan)
   const int D4 = (int)s.D / 4;
-  int clock_only = (D4 >= 256 && D4 % 128 == 0) ? 1 : 0;   // wide rows: k_seg_wide reduces the rows first
+  int clock_only = (D4 >= 256 && D4 % 128 == 0) ? 1 : 0;   // wide rows: k_seg_as reduces the rows first
   int launches = 1;
   if (clock_only) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cf->dev);
-    static const bool reg = getenv("HET_SEG_REG") != nullptr;   // A/B: the register form
-    if (reg) {
-      launch_pdl(k_seg_wide, sms * 4, 256, 0, st, pdl_mode() >= 1, false, sd, cd, grads, lr);
-    } else {
-      static bool attr = false;
-      const size_t smem = (size_t)AS_SEG[0] * AS_SEG[1] * AS_T * 16;
-      auto kern = k_seg_as<AS_SEG[0], AS_SEG[1], AS_SEG[2]>;
-      if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
-      const int S = D4 / (AS_T * AS_SEG[1]);
-      launch_pdl(kern, std::max(1, sms * AS_SEG[3] / S) * S, AS_T, smem, st, pdl_mode() >= 1, false,
-                 sd, cd, grads, lr);
-    }
+    static bool attr = false;
+    const size_t ssm = (size_t)AS_SEG[0] * AS_SEG[1] * AS_T * 16;
+    auto kern = k_seg_as<AS_SEG[0], AS_SEG[1], AS_SEG[2]>;
+    if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm); attr = true; }
+    const int S = D4 / (AS_T * AS_SEG[1]);
+    void* pr = prof_begin(prof, "seg_wide", st);
+    launch_pdl(kern, std::max(1, sms * AS_SEG[3] / S) * S, AS_T, ssm, st, pdl_mode() >= 1, false, sd, cd, grads, lr);
+    prof_end(prof, pr, st);
     launches += 1;
   }
   void* args[] = {(void*)&sd, (void*)&cd, (void*)&grads, (void*)&lr, (void*)&b, (void*)&sr, (void*)&pm, (void*)&push,
                   (void*)&xb, (void*)&clock_only};
+  void* pr = prof_begin(prof, "update_fused", st);
   if (pdl_mode() >= 2)
     launch_pdl(k_update_fused, coop_blocks, UPD_THREADS, smem, st, true, true, sd, cd, grads, lr, b, sr, pm, push, xb,
                clock_only);
   else
     cudaLaunchCooperativeKernel((void*)k_update_fused, dim3(coop_blocks), dim3(UPD_THREADS), args, smem, st);
+  prof_end(prof, pr, st);
   return launches;
 }
 

@@ -51,7 +51,6 @@ wide)
   python -m pytest tests/test_gpu_parity.py tests/test_gpu_loopback.py -x -q -k "scale or wide or heavy or toy_full or graph" 2>&1 | tail -3
   timeout 600 python bench.py --steps 50 --warmup 5 --workload scale --no-sweep --no-cpu-baseline > gpurun_out/wide_bench.json 2> gpurun_out/wide_bench.err
   summary gpurun_out/wide_bench.json
-  [ -n "${2:-}" ] && { HET_SEG_REG=1 timeout 600 python bench.py --steps 50 --warmup 5 --workload scale --no-sweep --no-cpu-baseline > gpurun_out/wide_bench_reg.json 2> gpurun_out/wide_bench_reg.err; summary gpurun_out/wide_bench_reg.json; }
   python tools/prof_step.py --scale --steps 10 > gpurun_out/wide_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/wide_launches.csv python tools/prof_step.py --scale --steps 10 > gpurun_out/wide_ncu.log 2>&1
   echo ncu rc $?
