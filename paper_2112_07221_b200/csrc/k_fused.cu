@@ -1076,6 +1076,7 @@ struct AsWalk {
   bool valid, dirty;
   int l, e, j0, cnt, c0, m, flag;
   int64_t ikey;
+  int hd, ihd;   // MV: bit 0 the key's head, bits 1..: the output row (lane's / item's)
 
   __device__ __forceinline__ void load(const Call& c, int lane) {
     for (;;) {
@@ -1085,10 +1086,20 @@ struct AsWalk {
       p4 = make_int4(0, 0, 0, 0);
       key = 0;
       fl = 0;
+      hd = 0;
       if (u < U) {
-        if (MV) {
-          fl = __ldcg(&c.ucnt[u]);
-          if (fl & 4) { rec = __ldcg(&c.urec[u]); p4 = __ldcg(&c.upos[u]); key = __ldcg(&c.uniq[u]); }
+        if (MV) {   // sorted position u: its output row perm[u] and its key's head inverse[perm[u]]
+          const int p = __ldcg(&c.perm[u]);
+          const int h = __ldcg(&c.inverse[p]);
+          fl = __ldcg(&c.ucnt[h]);
+          if ((fl & 4) && (!(fl & 2) || h == u)) {   // a push moves all its rows from the head
+            rec = __ldcg(&c.urec[h]);
+            key = __ldcg(&c.uniq[h]);
+            if (fl & 2) p4 = __ldcg(&c.upos[h]);
+            hd = (h == u ? 1 : 0) | (p << 1);
+          } else {
+            fl = 0;
+          }
         } else {
           rec = __ldcg(&c.urec[u]);
           p4 = __ldcg(&c.upos[u]);
@@ -1110,7 +1121,11 @@ struct AsWalk {
     dirty = z < 0;
     c0 = 0;
     m = MV ? cnt : min(CH, cnt);
-    if (MV) { flag = __shfl_sync(0xffffffffu, fl, l); ikey = __shfl_sync(0xffffffffu, key, l); }
+    if (MV) {
+      flag = __shfl_sync(0xffffffffu, fl, l);
+      ikey = __shfl_sync(0xffffffffu, key, l);
+      ihd = __shfl_sync(0xffffffffu, hd, l);
+    }
     valid = true;
   }
   __device__ __forceinline__ void init(const Call& c, int U_, int Q_, int q, int lane) {
@@ -1153,6 +1168,7 @@ __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __r
   extern __shared__ __align__(16) float4 ring[];   // [RING][F][AS_T]: row slot r, column j of thread t at (r * F + j) * AS_T + t
   const uint32_t sbase = smem_u32(ring) + threadIdx.x * 16;
   pdl_wait();
+  TL_X(5);
   const Ctl* ctl = s.ctl;
   const int U = ctl->abort ? 0 : (c.rmode ? c.n : ctl->U);
   const int D4 = s.D >> 2, S = D4 / (AS_T * F);
@@ -1227,14 +1243,19 @@ __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __r
     tail = ring_at<RING>(tail + rows);
     cw.next(c, lane);
   }
+  TL_X(6);
 }
 
 // The wide lookup's row moves (after k_lookup_wide with G = 0), the same
-// per-thread pipelines: the item's source slice -- v[e] for a hit, W[key]
-// for a refetch or miss, and p[e] when the Evict push W += p applies
-// -- staged by cp.async, then W + p for a push, the stores
-// v[e] = w (Fetch), W[key] = w (the push) and the Get scatter of w to
-// every occurrence.
+// per-thread pipelines over (sorted position, slice) items, so a key with
+// 128 occurrences is spread over as many CTAs as any other positions (dealt
+// per key, its scatter was the kernel's tail: ncu timeline, p90 26 us, max
+// 52 us).  A position stages its key's source slice -- v[e] for a hit,
+// W[key] for a refetch or miss -- and writes its own output row (Get,
+// P:474); the key's head position also writes v[e] = W[key] (Fetch).
+// No other position writes what another reads: W is read-only here except
+// under the Evict push W += p, whose key is moved whole by its
+// head (p[e] staged too, W[key] = v[e] = W + p, then every occurrence).
 template <int RING, int F>
 __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict__ out) {
   extern __shared__ __align__(16) float4 ring[];
@@ -1275,21 +1296,28 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
     float4 w[F];
     const float4* r0 = ring + tail * (F * AS_T) + t;
     const float4* r1 = ring + ring_at<RING>(tail + 1) * (F * AS_T) + t;
+    const bool head = cw.ihd & 1;
 #pragma unroll
     for (int j = 0; j < F; ++j) {
       w[j] = r0[j * AS_T];
       if (cw.flag & 2) w[j] = f4add_(w[j], r1[j * AS_T]);
-      if (cw.flag & 1) v4[(int64_t)cw.e * D4 + col4 + j * AS_T] = w[j];
+      if (head && (cw.flag & 1)) v4[(int64_t)cw.e * D4 + col4 + j * AS_T] = w[j];
       if (cw.flag & 2) W4[cw.ikey * D4 + col4 + j * AS_T] = w[j];
     }
-    for (int kb = 0; kb < cw.cnt; kb += 32) {
-      const int pos = cw.pos_lane(c, lane, kb);
-      const int mm = min(32, cw.cnt - kb);
-      for (int q = 0; q < mm; ++q) {
-        float4* o = o4 + (int64_t)__shfl_sync(0xffffffffu, pos, q) * D4 + col4;
+    if (cw.flag & 2) {   // push (the head's item): every occurrence
+      for (int kb = 0; kb < cw.cnt; kb += 32) {
+        const int pos = cw.pos_lane(c, lane, kb);
+        const int mm = min(32, cw.cnt - kb);
+        for (int q = 0; q < mm; ++q) {
+          float4* o = o4 + (int64_t)__shfl_sync(0xffffffffu, pos, q) * D4 + col4;
 #pragma unroll
-        for (int j = 0; j < F; ++j) __stcs(o + j * AS_T, w[j]);
+          for (int j = 0; j < F; ++j) __stcs(o + j * AS_T, w[j]);
+        }
       }
+    } else {             // this position's row
+      float4* o = o4 + (int64_t)(cw.ihd >> 1) * D4 + col4;
+#pragma unroll
+      for (int j = 0; j < F; ++j) __stcs(o + j * AS_T, w[j]);
     }
     const int rows = cw.rows();
     --inflight;
@@ -1297,6 +1325,7 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
     tail = ring_at<RING>(tail + rows);
     cw.next(c, lane);
   }
+  TL_X(7);
 }
 
 // ring rows, float4 columns per thread, rows per stage, CTAs per SM (macros: sweeps)

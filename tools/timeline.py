@@ -52,7 +52,7 @@ names = {0: "dd.start", 2: "dd.work",
          13: "lk.find", 14: "lk.install", 15: "lk.vread", 10: "lk.work", 16: "up.start", 18: "up.seg",
          11: "up.xwait", 20: "up.xdone", 19: "up.sync", 21: "up.end", 24: "plan.l2", 25: "plan.l1",
          26: "plan.kstar", 28: "lk.mpop", 29: "lk.mfstack", 30: "lk.minsert",
-         32: "bk.scanned", 33: "bk.scattered", 34: "bk.ranked", 35: "bk.stored", 36: "bk.keys",
+         37: "seg.start", 38: "seg.end", 39: "mv.end", 32: "bk.scanned", 33: "bk.scattered", 34: "bk.ranked", 35: "bk.stored", 36: "bk.keys",
          9: "x.bc", 4: "x.issued", 17: "x.words", 6: "x.written", 31: "x.atomic", 1: "dd.keys", 3: "dd.prefetch", 5: "dd.count"}
 kbuf, gbuf = keys[0].clone(), g.clone()
 graph = None
@@ -80,6 +80,10 @@ for j in range(20):
         x = v[m][v[m] > 0]
         if x.size:
             x = (x - t0) / 1000.0
-            parts.append(f"{names[m]} p50 {np.median(x):.1f} max {x.max():.1f}")
+            if m >= 37:   # per-warp end times of the wide-row kernels: the spread
+                parts.append(f"{names[m]} p10 {np.percentile(x, 10):.1f} p50 {np.median(x):.1f} "
+                             f"p90 {np.percentile(x, 90):.1f} max {x.max():.1f}")
+            else:
+                parts.append(f"{names[m]} p50 {np.median(x):.1f} max {x.max():.1f}")
     print(" | ".join(parts))
     print("plan", het.het_debug_eviction_plan(c.h))
