@@ -80,7 +80,7 @@ for j in range(20):
         x = v[m][v[m] > 0]
         if x.size:
             x = (x - t0) / 1000.0
-            if m >= 37:   # per-warp end times of the wide-row kernels: the spread
+            if m >= 37 or m == 18:   # per-warp end times: the spread
                 parts.append(f"{names[m]} p10 {np.percentile(x, 10):.1f} p50 {np.median(x):.1f} "
                              f"p90 {np.percentile(x, 90):.1f} max {x.max():.1f}")
             else:
