@@ -338,4 +338,51 @@ __device__ __forceinline__ void generic_select(const Dev& s, const EvBuf& b, uin
   }
 }
 
+// "When the frequency of an embedding is high enough, it will be
+// assigned a direct access index, bypassing the cost of frequency
+// maintenance."  The lookup kernels list the entries whose count reached
+// pin_thr (pin_candidate); here they are pinned -- eprim = EP_PIN, out of the
+// LFU count bitmaps, so never a victim -- in ascending key order while fewer
+// than pin_max = floor(C/2) entries are pinned (reading R27).  One CTA (any
+// block size), after every touch of the lookup.
+__device__ __forceinline__ void pin_apply_block(const Dev& s) {
+  __shared__ int dpop[LFU_CB_MAX];
+  __shared__ uint32_t h[NBIN];
+  __shared__ uint32_t s_K;
+  Ctl* ctl = s.ctl;
+  const int nc = __ldcg(&ctl->npin_cand);   // other blocks' appends (L2)
+  if (nc == 0) return;
+  dpop_init(dpop);
+  const int64_t budget = s.pin_max - __ldcg(&ctl->npinned);
+  uint32_t K = 0xFFFFFFFFu;          // pin the candidates with key <= K
+  if (budget > 0 && budget < nc) {          // the budget smallest keys (candidate keys are distinct)
+    int64_t below;
+    auto get = [&](int64_t i, uint32_t* val) -> bool { *val = (uint32_t)__ldcg(&s.pin_k[i]); return true; };
+    const uint32_t T = cta_select_u32(get, nc, budget, &below, h);
+    if (threadIdx.x == 0) s_K = T;
+    __syncthreads();
+    K = s_K;
+  }
+  __shared__ int s_np;
+  if (threadIdx.x == 0) s_np = 0;
+  __syncthreads();
+  if (budget > 0) {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      const int64_t key = __ldcg(&s.pin_k[i]);
+      if ((uint64_t)key > (uint64_t)K) continue;
+      const int32_t e = __ldcg(&s.pin_e[i]);
+      const uint32_t oldc = __ldcg(&s.eprim[e]);
+      lfu_move(s, key, oldc, EP_PIN, dpop);   // EP_PIN >= lfu_cb: out of the bitmaps
+      s.eprim[e] = EP_PIN;
+      atomicAdd(&s_np, 1);
+    }
+  }
+  __syncthreads();
+  dpop_flush(s, dpop);
+  if (threadIdx.x == 0) {
+    ctl->npinned += s_np;
+    ctl->npin_cand = 0;
+  }
+}
+
 }  // namespace het

@@ -669,7 +669,8 @@ static void lookup_phase(het_cache* h, LkCtx& x, int ph, cudaStream_t st) {
 static het_status_t lookup_post(het_cache* h, LkCtx& x, cudaStream_t st) {
   Dev& d = h->d;
   const uint32_t n = (uint32_t)h->call.n;
-  if (d.pin_thr) h->launches += launch_pin_apply(d, st);   // light-LFU promotions of this lookup
+  // light-LFU promotions of this lookup (the fused N = 1 lookup kernels apply them in their last block)
+  if (d.pin_thr && !(h->fused && d.world == 1)) h->launches += launch_pin_apply(d, st);
   if (x.out_host) CUDA_TRY(h, cudaMemcpyAsync(x.out, x.dout, (size_t)n * h->D * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaGetLastError());
   h->have_lookup = true;

@@ -80,7 +80,7 @@ struct Ctl {
   int32_t vmode;        // victims list holds 0 = entry indices, 1 = keys
   int32_t pad3_;
   int32_t dd_done;      // blocks finished in the fused dedup (last-block pattern)
-  int32_t lk_done;      // blocks finished in the fused lookup
+  int32_t lk_done;      // blocks finished in the fused lookup (light-LFU: the last one applies the promotions)
   int32_t emode;        // eviction this step: 0 none, 1 LFU bitmap threshold, 2 generic
   int32_t rebuild_req;  // hash rebuild requested for the next update
   uint32_t lk_seq;      // lookup sequence number
@@ -115,8 +115,6 @@ struct Ctl {
   int32_t ext_blocks;   // extraction blocks finished (last-block counter)
   uint32_t plan_flag;   // lk_seq of the published plan (update: block 0 -> the other blocks)
   int32_t ev_done;      // eviction blocks finished (last-block counter)
-  // wide rows: dynamic work units of k_seg_as / k_mv_as (reset by each kernel's last warp)
-  int32_t seg_unit, seg_done, mv_unit, mv_done;
 };
 
 struct Dev {

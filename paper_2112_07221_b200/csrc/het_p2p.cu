@@ -549,14 +549,18 @@ __device__ __forceinline__ PBKey probe_build_a(const Dev& s, const Call& c, cons
     const int D4 = s.D >> 2;
     const float4* vr = reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D);
     float4* o4 = reinterpret_cast<float4*>(out);
-    for (int d = lane; d - lane < D4; d += 32) {
-      const float4 val = d < D4 ? vr[d] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int d0 = lane; d0 - lane < D4; d0 += 32 * RB) {   // RB columns per lane in flight (wide rows)
+      float4 val[RB];
+#pragma unroll
+      for (int b = 0; b < RB; ++b) val[b] = d0 + 32 * b < D4 ? vr[d0 + 32 * b] : make_float4(0.f, 0.f, 0.f, 0.f);
       for (int kb = 0; kb < cnt; kb += 32) {
         const int srcp = kb == 0 ? pos_lane : (kb + lane < cnt ? c.perm[j0 + kb + lane] : 0);
         const int mm = min(32, cnt - kb);
         for (int q = 0; q < mm; ++q) {
           const int pos = __shfl_sync(0xffffffffu, srcp, q);
-          if (d < D4) __stcs(o4 + (int64_t)pos * D4 + d, val);
+#pragma unroll
+          for (int b = 0; b < RB; ++b)
+            if (d0 + 32 * b < D4) __stcs(o4 + (int64_t)pos * D4 + d0 + 32 * b, val[b]);
         }
       }
     }

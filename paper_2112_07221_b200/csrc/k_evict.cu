@@ -31,51 +31,9 @@ void evbuf_init(void* evbuf, uint32_t* hist, uint32_t* khist, int32_t* victims, 
 }
 
 // ============================================================ light-LFU promotion
-// "When the frequency of an embedding is high enough, it will be
-// assigned a direct access index, bypassing the cost of frequency
-// maintenance."  The lookup kernels list the entries whose count reached
-// pin_thr (pin_candidate); here they are pinned -- eprim = EP_PIN, out of the
-// LFU count bitmaps, so never a victim -- in ascending key order while fewer
-// than pin_max = floor(C/2) entries are pinned (reading R27).  One CTA.
-__global__ void __launch_bounds__(1024) k_pin_apply(Dev s) {
-  __shared__ int dpop[LFU_CB_MAX];
-  __shared__ uint32_t h[NBIN];
-  __shared__ uint32_t s_K;
-  Ctl* ctl = s.ctl;
-  const int nc = ctl->npin_cand;
-  if (nc == 0) return;
-  dpop_init(dpop);
-  const int64_t budget = s.pin_max - ctl->npinned;
-  uint32_t K = 0xFFFFFFFFu;          // pin the candidates with key <= K
-  if (budget > 0 && budget < nc) {          // the budget smallest keys (candidate keys are distinct)
-    int64_t below;
-    auto get = [&](int64_t i, uint32_t* val) -> bool { *val = (uint32_t)s.pin_k[i]; return true; };
-    const uint32_t T = cta_select_u32(get, nc, budget, &below, h);
-    if (threadIdx.x == 0) s_K = T;
-    __syncthreads();
-    K = s_K;
-  }
-  __shared__ int s_np;
-  if (threadIdx.x == 0) s_np = 0;
-  __syncthreads();
-  if (budget > 0) {
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-      const int64_t key = s.pin_k[i];
-      if ((uint64_t)key > (uint64_t)K) continue;
-      const int32_t e = s.pin_e[i];
-      const uint32_t oldc = s.eprim[e];
-      lfu_move(s, key, oldc, EP_PIN, dpop);   // EP_PIN >= lfu_cb: out of the bitmaps
-      s.eprim[e] = EP_PIN;
-      atomicAdd(&s_np, 1);
-    }
-  }
-  __syncthreads();
-  dpop_flush(s, dpop);
-  if (threadIdx.x == 0) {
-    ctl->npinned += s_np;
-    ctl->npin_cand = 0;
-  }
-}
+// (pin_apply_block in evict_dev.cuh; the fused N = 1 lookups run it in their
+// last block, the other lookup paths launch this kernel after the lookup)
+__global__ void __launch_bounds__(1024) k_pin_apply(Dev s) { pin_apply_block(s); }
 
 int launch_pin_apply(const Dev& s, cudaStream_t st) {
   k_pin_apply<<<1, 1024, 0, st>>>(s);

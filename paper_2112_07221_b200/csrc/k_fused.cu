@@ -703,15 +703,29 @@ k_lookup_fused(Dev s, Call c, float* __restrict__ out, int agg) {
       atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
     }
   }
+  // light-LFU (R27): the last block applies this lookup's promotions
+  if (s.pin_thr) {
+    __shared__ int s_lastpin;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_lastpin = atomicAdd(&ctl->lk_done, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (s_lastpin) {
+      __threadfence();
+      pin_apply_block(s);
+      if (threadIdx.x == 0) ctl->lk_done = 0;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ K_look, wide rows
-// D >= 1024 (BASELINE configs[4], D = 4096: 16 KB rows): G = D/512 warps per
-// unique key (up to the 8 warps of the block).  The group's first warp takes
-// every decision of k_lookup_fused (Find, CheckValid, touch, sync push clock,
-// install allocation); after a block barrier the G warps move the row bytes,
-// each its own 512-column slice: the Evict push W += p, the Fetch v = W and
-// the Get scatter to every occurrence.  Same semantics, same order per column.
+// D >= 1024 (BASELINE configs[4], D = 4096: 16 KB rows).  G = 0 (the fused
+// rmode path): a warp per sorted position takes every decision of
+// k_lookup_fused (Find, CheckValid, touch, sync push clock, install
+// allocation) and leaves the row moves to k_mv_as (flags in ucnt).  G > 0
+// (unsorted-unique mode): G = D/512 warps per key, the first takes the
+// decisions, then after a block barrier each warp moves its 512-column
+// slice: the Evict push W += p, the Fetch v = W and the Get scatter.
 struct LkMeta { int64_t key; int32_t e; int32_t j0; int32_t cnt; uint32_t g; uint8_t st; uint8_t push; };
 
 __global__ void __launch_bounds__(LK_WARPS * 32)
@@ -863,6 +877,19 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
       if (nu) atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)nu);
     } else if (blockIdx.x == 0 && !ctl->abort) {
       atomicAdd(&s.cnt[C_UNIQUE], (unsigned long long)U);
+    }
+  }
+  // light-LFU (R27): the last block applies this lookup's promotions
+  if (s.pin_thr) {
+    __shared__ int s_lastpin;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_lastpin = atomicAdd(&ctl->lk_done, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (s_lastpin) {
+      __threadfence();
+      pin_apply_block(s);
+      if (threadIdx.x == 0) ctl->lk_done = 0;
     }
   }
 }

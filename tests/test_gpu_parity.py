@@ -224,13 +224,14 @@ def test_large_batch_multi_cta_dedup():
     p.finish()
 
 
-@pytest.mark.parametrize("D,B", [(128, 4096), (36, 2048)])
+@pytest.mark.parametrize("D,B", [(128, 4096), (36, 2048), (8, 32768)])
 def test_heavy_key_segment_reduce(D, B):
     """Per-phase path with Criteo-shaped batches large enough that small fields'
     keys occur thousands of times: keys with > 32 occurrences go through the
     TMA-ring heavy-key kernel (those with >= 2048 listed first), the rest through
     the half-warp kernel, concurrently.  Rows, clocks and pendings after every
-    update must match the oracle's ordered sums."""
+    update must match the oracle's ordered sums.  B = 32768 (n = 851,968) is
+    the largest batch of bench.py's hbm_sweep, at a small D."""
     R = 200000
     cards = gen.scaled_cards(R)
     n = B * 26

@@ -46,7 +46,9 @@ multi)
     summary gpurun_out/bench_dcn_n$n.json
   done
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29725 bench.py --gpus $N --steps 100 --warmup 5 --workload reddit > gpurun_out/bench_reddit_n$N.json 2> gpurun_out/bench_reddit_n$N.err
-  summary gpurun_out/bench_reddit_n$N.json ;;
+  summary gpurun_out/bench_reddit_n$N.json
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29726 bench.py --gpus $N --steps 50 --warmup 5 --workload scale > gpurun_out/bench_scale_n$N.json 2> gpurun_out/bench_scale_n$N.err
+  summary gpurun_out/bench_scale_n$N.json ;;
 wide)
   python -m pytest tests/test_gpu_parity.py tests/test_gpu_loopback.py -x -q -k "scale or wide or heavy or toy_full or graph" 2>&1 | tail -3
   timeout 600 python bench.py --steps 50 --warmup 5 --workload scale --no-sweep --no-cpu-baseline > gpurun_out/wide_bench.json 2> gpurun_out/wide_bench.err
