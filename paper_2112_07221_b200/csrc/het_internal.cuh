@@ -482,6 +482,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+// Wide rows (D >= 1024 and a multiple of 512): the fused paths move row bytes
+// in their own kernels (k_mv_as, k_seg_as) instead of a warp per key.
+__host__ __device__ __forceinline__ bool wide_rows(uint32_t D) {
+  const uint32_t D4 = D >> 2;
+  return D4 >= 256 && D4 % 128 == 0;
+}
+
 // warp-aggregated counter increment
 __device__ __forceinline__ void warp_count(unsigned long long* c, bool pred) {
   unsigned m = __ballot_sync(__activemask(), pred);
@@ -532,6 +539,9 @@ int launch_dd_bucket(const Dev& s, const Call& c, int n, int pbits, uint64_t t, 
 constexpr int RMODE_MAX = 16384;   // rmode dedups serve n <= this
 // prof: the handle when phase profiling is on (het_profile_enable), else nullptr
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st, void* prof = nullptr);
+// N > 1, wide rows, rmode: the Get scatter out[perm[r]] = v[entry of r's key] of every sorted
+// position r after the exchange round installed the rows (k_mv_as, scatter-only)
+int launch_scatter_wide(const Dev& s, const Call& c, float* out, cudaStream_t st);
 // SMs left free by the cooperative kernels for NCCL's blocks at N > 1
 // (= NCCL's maxCTAs and the peer-memory dense all-reduce grid; env HET_NCCL_CTAS, default 16)
 int coop_sm_reserve();

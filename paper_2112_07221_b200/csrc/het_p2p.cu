@@ -543,7 +543,7 @@ __device__ __forceinline__ PBKey probe_build_a(const Dev& s, const Call& c, cons
   write_urec(c, u, e, j0, cnt, ecc > ecs, ecc, pos_lane, lane);   // resident: a hit keeps it, a refetch rewrites it
   if (c.rmode && lane == 0) { c.uniq[u] = key; c.ucnt[u] = cnt; }   // for the install phase
   k.key = key; k.e = e; k.ecc = ecc; k.st = st;
-  if (st == ST_HIT || st == ST_NEEDQ) {
+  if ((st == ST_HIT || st == ST_NEEDQ) && !(c.rmode && wide_rows(s.D))) {   // wide: launch_scatter_wide
     // Cache.Get now: a hit's row, and a clock-checked hit's row (the
     // install overwrites the occurrences of the rare one condition (2) refuses)
     const int D4 = s.D >> 2;
@@ -740,7 +740,7 @@ __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, 
   bool fresh = st != ST_HIT;   // the probe already scattered hits and clock-checked hits condition (2) kept
   if (st == ST_NEEDQ) fresh = reinterpret_cast<const uint32_t*>(
                                   resprec(m, m.rank, m.uslot[u] / (int)m.CAPS, m.uslot[u] % (int)m.CAPS))[1] == 0;
-  if (ok && e >= 0 && fresh) {
+  if (ok && e >= 0 && fresh && !(c.rmode && wide_rows(s.D))) {   // wide rows: launch_scatter_wide after the round
     const float4* vr = reinterpret_cast<const float4*>(s.v + (int64_t)e * s.D);
     float4* o4 = reinterpret_cast<float4*>(out);
     for (int d0 = lane; d0 - lane < D4; d0 += 32 * RB) {
@@ -1274,7 +1274,9 @@ int p2p_lookup_phase(P2PState* p, const Dev& d, const Call& c, float* out, int p
     case RP_BUILD: k_probe_build<<<blocks, 256, 0, st>>>(d, c, v, out); return 1;
     case RP_LINK: k_p2p_link<<<148, 256, 0, st>>>(d, v); return 1;
     case RP_PROCESS: k_p2p_process<<<148 * 2, 256, 0, st>>>(d, v); return 1;
-    default: k_install_gather<<<blocks, 256, 0, st>>>(d, c, v, out); return 1;
+    default:
+      k_install_gather<<<blocks, 256, 0, st>>>(d, c, v, out);
+      return 1 + (c.rmode && wide_rows(d.D) ? launch_scatter_wide(d, c, out, st) : 0);
   }
 }
 
@@ -1297,7 +1299,8 @@ int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaSt
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    if (cudaLaunchKernelEx(&cfg, k_exchange, d, c, v, out) == cudaSuccess) return 1;
+    if (cudaLaunchKernelEx(&cfg, k_exchange, d, c, v, out) == cudaSuccess)
+      return 1 + (c.rmode && wide_rows(d.D) ? launch_scatter_wide(d, c, out, st) : 0);
     cudaGetLastError();   // fall through to the split round
   }
   int l = 0;

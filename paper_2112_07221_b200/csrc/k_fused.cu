@@ -1104,6 +1104,7 @@ struct AsWalk {
   int l, e, j0, cnt, c0, m, flag;
   int64_t ikey;
   int hd, ihd;   // MV: bit 0 the key's head, bits 1..: the output row (lane's / item's)
+  bool scat = false;   // MV: scatter only (N > 1: the rows are installed)
 
   __device__ __forceinline__ void load(const Call& c, int lane) {
     for (;;) {
@@ -1118,6 +1119,11 @@ struct AsWalk {
         if (MV) {   // sorted position u: its output row perm[u] and its key's head inverse[perm[u]]
           const int p = __ldcg(&c.perm[u]);
           const int h = __ldcg(&c.inverse[p]);
+          if (scat) {   // scatter only: every position of a key with an entry copies v[e] to its row
+            rec = __ldcg(&c.urec[h]);
+            fl = rec.x >= 0 ? 4 : 0;
+            hd = (h == u ? 1 : 0) | (p << 1);
+          } else {
           fl = __ldcg(&c.ucnt[h]);
           if ((fl & 4) && (!(fl & 2) || h == u)) {   // a push moves all its rows from the head
             rec = __ldcg(&c.urec[h]);
@@ -1126,6 +1132,7 @@ struct AsWalk {
             hd = (h == u ? 1 : 0) | (p << 1);
           } else {
             fl = 0;
+          }
           }
         } else {
           rec = __ldcg(&c.urec[u]);
@@ -1284,7 +1291,7 @@ __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __r
 // under the Evict push W += p, whose key is moved whole by its
 // head (p[e] staged too, W[key] = v[e] = W + p, then every occurrence).
 template <int RING, int F>
-__global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict__ out) {
+__global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict__ out, int scat) {
   extern __shared__ __align__(16) float4 ring[];
   const uint32_t sbase = smem_u32(ring) + threadIdx.x * 16;
   pdl_wait();
@@ -1299,6 +1306,7 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
   const float4* p4g = reinterpret_cast<const float4*>(s.p);
   float4* o4 = reinterpret_cast<float4*>(out);
   AsWalk<true, 1> iw, cw;
+  iw.scat = cw.scat = scat != 0;
   iw.init(c, U, Q, (int)blockIdx.x / S, lane);
   cw.init(c, U, Q, (int)blockIdx.x / S, lane);
   int inflight = 0, used = 0, head = 0, tail = 0;
@@ -1997,7 +2005,7 @@ int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st
       if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
       const int S = D4 / (AS_T * AS_MV[1]);
       pr = prof_begin(prof, "lookup_mv", st);
-      launch_pdl(kern, std::max(1, sms * AS_MV[2] / S) * S, AS_T, smem, st, pdl_mode() >= 1, false, s, c, out);
+      launch_pdl(kern, std::max(1, sms * AS_MV[2] / S) * S, AS_T, smem, st, pdl_mode() >= 1, false, s, c, out, 0);
       prof_end(prof, pr, st);
       return 2;
     }
@@ -2029,6 +2037,19 @@ int coop_sm_reserve() {
 // cooperative launch configuration per (device, N > 1, D): the grid leaves
 // coop_sm_reserve() SMs free at N > 1 and the staging depends on D
 struct UpdCfg { int dev; bool multi; uint32_t D; int blocks; size_t smem; int stage_rows; };
+
+int launch_scatter_wide(const Dev& s, const Call& c, float* out, cudaStream_t st) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static bool attr = false;
+  const size_t smem = (size_t)AS_MV[0] * AS_MV[1] * AS_T * 16;
+  auto kern = k_mv_as<AS_MV[0], AS_MV[1]>;
+  if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
+  const int S = (int)(s.D / 4) / (AS_T * AS_MV[1]);
+  kern<<<std::max(1, sms * AS_MV[2] / S) * S, AS_T, smem, st>>>(s, c, out, 1);
+  return 1;
+}
 
 int launch_update_fused(const Dev& s, const Call& c, const float* grads, float lr, void* evbuf, cudaStream_t st,
                         const void* p2pview, void* prof) {

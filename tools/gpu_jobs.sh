@@ -3,6 +3,7 @@
 #   bash tools/gpu_jobs.sh iter            N=1 parity + loopback, WDL bench line, graph timeline
 #   bash tools/gpu_jobs.sh timeline [--reddit]   graph-replay timeline (HET_TIMELINE build, restored after)
 #   bash tools/gpu_jobs.sh timeline_mgpu   N=2 per-rank timeline, with and without the dense all-reduce
+#   bash tools/gpu_jobs.sh timeline_mgpu_scale   N=2 per-rank timeline at BASELINE configs[4] (D = 4096)
 #   bash tools/gpu_jobs.sh multi N         multi-process parity (p2p) + DCN bench lines up to N + Reddit at N
 #   bash tools/gpu_jobs.sh wide            wide-row parity (N=1 + loopback) and the scale-shaped bench line
 #   bash tools/gpu_jobs.sh wide_sweep A/B ..  scale bench per wide-kernel configuration (ring,F,CH,CTAs/ring,F,CTAs)
@@ -38,6 +39,10 @@ timeline_mgpu)
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29633 tools/timeline_step_mgpu.py > gpurun_out/tlm.txt 2>&1
   TL_DENSE=0 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29634 tools/timeline_step_mgpu.py > gpurun_out/tlm_nodense.txt 2>&1
   rebuild; grep rank gpurun_out/tlm.txt | tail -2; echo NODENSE; grep rank gpurun_out/tlm_nodense.txt | tail -2 ;;
+timeline_mgpu_scale)
+  tl_build
+  TL_SCALE=1 TL_DENSE=0 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29635 tools/timeline_step_mgpu.py > gpurun_out/tlm_scale.txt 2>&1
+  rebuild; grep rank gpurun_out/tlm_scale.txt | tail -2 ;;
 multi)
   N=${2:-2}
   python -m pytest tests/test_gpu_multi.py -x -q -k "1]" 2>&1 | tail -3

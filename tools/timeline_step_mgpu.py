@@ -23,6 +23,9 @@ dist.broadcast_object_list(obj, src=0)
 B, D = 128, 128
 n = B * 26
 cards = gen.cards_for("criteo")
+if os.environ.get("TL_SCALE") == "1":   # BASELINE configs[4] per GPU: 3M rows, D = 4096
+    D = 4096
+    cards = gen.scaled_cards(3_000_000 * world)
 c = het.HetCache(sum(cards), D, 0.1, 100, het.HET_LFU, rank=rank, world=world, unique_id=obj[0], max_keys_per_call=n)
 lib = het.load()
 lib.het_debug_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
