@@ -106,13 +106,14 @@ def ncu_traffic(phase, world):
     phase's kernel from the committed `ncu --set full` capture of this workload
     (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), else None.
     Cold-cache, replayed launches: compare with `achieved`'s algorithmic bytes.
-    The capture is of the default workload (WDL at N = 1) only."""
-    if CFG.get("name") not in ("WDL", "DCN"):
+    Captures: the default workload (WDL at N = 1) and the scale workload (N = 1)."""
+    key = {"WDL": "n%d", "DCN": "n%d", "scale-D4096": "scale_n%d"}.get(CFG.get("name"))
+    if key is None:
         return None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
-        ent = t["n%d" % world][phase]
+        ent = t[key % world][phase]
         return float(ent["dram_bytes"])
     except Exception:
         return None

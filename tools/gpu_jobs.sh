@@ -7,6 +7,7 @@
 #   bash tools/gpu_jobs.sh multi N         multi-process parity (p2p) + DCN bench lines up to N + Reddit at N
 #   bash tools/gpu_jobs.sh wide            wide-row parity (N=1 + loopback) and the scale-shaped bench line
 #   bash tools/gpu_jobs.sh wide_sweep A/B ..  scale bench per wide-kernel configuration (ring,F,CH,CTAs/ring,F,CTAs)
+#   bash tools/gpu_jobs.sh final           round-end evidence: pytest -m gpu, smoke, bench lines, ncu launch list + full sets
 #   bash tools/gpu_jobs.sh bounds          parity + loopback with the bounds-checked build (HET_DIAG=HET_BOUNDS)
 #   bash tools/gpu_jobs.sh diag MACRO      timeline of a diagnostic build variant next to the normal one
 #   bash tools/gpu_jobs.sh ncu_launches    ncu launch list of 10 WDL steps (after a plain run)
@@ -75,6 +76,19 @@ wide_sweep)   # wide-row kernel configurations: "seg_cfg/mv_cfg" pairs
     echo "== $pair"; summary gpurun_out/ws.json
   done
   rebuild ;;
+final)   # round-end evidence on one GPU (outputs under gpurun_out/final_*)
+  python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/final_pytest_gpu.log; cat gpurun_out/final_pytest_gpu.log
+  python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/final_smoke.log 2>&1; tail -1 gpurun_out/final_smoke.log
+  timeout 900 python bench.py > gpurun_out/final_bench_n1.json 2> gpurun_out/final_bench_n1.err; summary gpurun_out/final_bench_n1.json
+  timeout 900 python bench.py --impl reference > gpurun_out/final_reference_n1.json 2> gpurun_out/final_reference_n1.err; tail -c 300 gpurun_out/final_reference_n1.json
+  timeout 900 python bench.py --workload scale --no-cpu-baseline > gpurun_out/final_bench_scale_n1.json 2> gpurun_out/final_bench_scale_n1.err; summary gpurun_out/final_bench_scale_n1.json
+  python tools/prof_step.py --steps 10 > gpurun_out/plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/final_launches.csv python tools/prof_step.py --steps 10 > gpurun_out/ncu.log 2>&1
+  python tools/launches.py gpurun_out/final_launches.csv 10 > gpurun_out/final_launches_summary.txt; cat gpurun_out/final_launches_summary.txt
+  ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"k_update_fused|k_lookup_fused|k_dd_fused" -c 3 -o gpurun_out/final_prof python tools/prof_step.py --steps 3 > gpurun_out/ncu2.log 2>&1
+  python tools/prof_step.py --scale --steps 3 > gpurun_out/plain.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"k_seg_as|k_mv_as|k_lookup_wide|k_update_fused|k_dd_fused" -c 5 -o gpurun_out/final_prof_scale python tools/prof_step.py --scale --steps 3 > gpurun_out/ncu3.log 2>&1
+  ls -la gpurun_out/final_prof*.ncu-rep ;;
 bounds)
   python -m pytest tests/test_gpu_parity.py tests/test_gpu_loopback.py -x -q 2>&1 | tail -3 > gpurun_out/bd_normal.log
   HET_DIAG=HET_BOUNDS python -c "from paper_2112_07221_b200 import build; build.build(force=True)" >> gpurun_out/build.log 2>&1
