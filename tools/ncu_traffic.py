@@ -28,7 +28,7 @@ hdr, units, data = rows[0], rows[1], rows[2:]
 ik = hdr.index("Kernel Name")
 acc = {}
 for r in data:
-    name = r[ik].split("(")[0].split("::")[-1].split("<")[0]
+    name = r[ik].split("(")[0].split("<")[0].split("::")[-1].split()[-1]
     if name not in PHASE:
         continue
     vals = {}
