@@ -2091,6 +2091,8 @@ int launch_update_fused(const Dev& s, const Call& c, const float* grads, float l
   int push = 0;
   if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
   int xb = std::max(1, std::min(8, coop_blocks / 16));   // extraction blocks (after block 0's plan)
+  static const int xb_env = getenv("HET_XB") ? atoi(getenv("HET_XB")) : 0;   // measurement override
+  if (xb_env > 0) xb = std::min(xb_env, coop_blocks - 2);
   const int D4 = (int)s.D / 4;
   int clock_only = (D4 >= 256 && D4 % 128 == 0) ? 1 : 0;   // wide rows: k_seg_as reduces the rows first
   int launches = 1;

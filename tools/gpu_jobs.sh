@@ -89,6 +89,14 @@ final)   # round-end evidence on one GPU (outputs under gpurun_out/final_*)
   python tools/prof_step.py --scale --steps 3 > gpurun_out/plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"k_seg_as|k_mv_as|k_lookup_wide|k_update_fused|k_dd_fused" -c 5 -o gpurun_out/final_prof_scale python tools/prof_step.py --scale --steps 3 > gpurun_out/ncu3.log 2>&1
   ls -la gpurun_out/final_prof*.ncu-rep ;;
+xb_sweep)   # extraction blocks of the fused update (HET_XB) at WDL and at configs[4]
+  shift
+  for x in "$@"; do
+    for w in wdl scale; do
+      HET_XB=$x timeout 600 python bench.py --steps 100 --warmup 5 --workload $w --no-sweep --no-cpu-baseline > gpurun_out/xb.json 2> gpurun_out/xb.err
+      echo "== HET_XB=$x $w"; summary gpurun_out/xb.json | head -1
+    done
+  done ;;
 bounds)
   python -m pytest tests/test_gpu_parity.py tests/test_gpu_loopback.py -x -q 2>&1 | tail -3 > gpurun_out/bd_normal.log
   HET_DIAG=HET_BOUNDS python -c "from paper_2112_07221_b200 import build; build.build(force=True)" >> gpurun_out/build.log 2>&1
