@@ -96,6 +96,14 @@ struct het_cache {
   // after the previous update's reads of the staging buffer and before this one's
   cudaStream_t copy = nullptr;
   cudaEvent_t ev_rows_free = nullptr, ev_rows_ready = nullptr;
+  // host rows out of a lookup: the update that follows with host gradients
+  // runs on `ustream`, after the lookup's kernels (ev_lk_done, recorded before
+  // the D2H of the rows) instead of after the D2H, and the caller's stream
+  // waits for it (ev_upd_done): the update's kernels overlap the copy.  Valid
+  // only for the call right after the lookup (lk_done_valid).
+  cudaStream_t ustream = nullptr;
+  cudaEvent_t ev_lk_done = nullptr, ev_upd_done = nullptr;
+  bool lk_done_valid = false;
   // profiling
   bool prof = false;
   std::vector<ProfRec> prof_pending;
@@ -332,7 +340,10 @@ static het_status_t create_impl(uint64_t rows, uint32_t D, double cache_frac, ui
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_rows_free, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_rows_ready, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&h->ev_rows_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->ustream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_lk_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_upd_done, cudaEventDisableTiming) != cudaSuccess) {
     het_cache_destroy(h);
     return HET_ERR_CUDA;
   }
@@ -516,6 +527,7 @@ static const void* p2p_view(het_cache* h) { return h->d.world > 1 ? (const void*
 // (inspection calls -- het_stats, het_check, het_debug_* -- pass count =
 // false: the launch counter reports the hot path's kernels)
 static void flush_evict(het_cache* h, cudaStream_t st, bool count = true) {
+  h->lk_done_valid = false;   // another call between the lookup and the update: the update stays on the stream
   // after a captured update, any graph replay may have listed victims: the
   // kernel tests the device flag (cheap when nothing is listed)
   if (!h->ev_pending && !h->ev_captured) return;
@@ -671,7 +683,16 @@ static het_status_t lookup_post(het_cache* h, LkCtx& x, cudaStream_t st) {
   const uint32_t n = (uint32_t)h->call.n;
   // light-LFU promotions of this lookup (the fused N = 1 lookup kernels apply them in their last block)
   if (d.pin_thr && !(h->fused && d.world == 1)) h->launches += launch_pin_apply(d, st);
-  if (x.out_host) CUDA_TRY(h, cudaMemcpyAsync(x.out, x.dout, (size_t)n * h->D * 4, cudaMemcpyDeviceToHost, st));
+  h->lk_done_valid = false;
+  if (x.out_host) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    if (cap == cudaStreamCaptureStatusNone && h->fused && d.world == 1 && !h->group) {
+      CUDA_TRY(h, cudaEventRecord(h->ev_lk_done, st));   // the lookup's kernels, before the rows' D2H
+      h->lk_done_valid = true;
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(x.out, x.dout, (size_t)n * h->D * 4, cudaMemcpyDeviceToHost, st));
+  }
   CUDA_TRY(h, cudaGetLastError());
   h->have_lookup = true;
   h->last_n = n;
@@ -690,6 +711,7 @@ het_status_t het_prefetch(het_cache_t h, const int64_t* keys, uint32_t n, het_st
   if (!h) return HET_ERR_ARG;
   if (n > h->n_max) return fail(h, HET_ERR_CAPACITY, "n exceeds max_keys_per_call");
   if (n && !keys) return fail(h, HET_ERR_ARG, "null keys");
+  h->lk_done_valid = false;
   h->pref_keys = nullptr;
   if (h->no_fused || n == 0 || (int)n > RMODE_MAX) return HET_OK;   // nothing to run ahead on this path
   const int64_t* dkeys = keys;
@@ -799,6 +821,11 @@ static het_status_t update_impl(het_cache* h, const int64_t* keys, uint32_t n, c
     h->launches += 1;
   }
   bool staged = false;
+  // beside the lookup's D2H: host gradients, the lookup's own keys, no call in
+  // between (the update then reads only the staged rows and library state)
+  const bool beside = h->lk_done_valid && n && keys == h->last_keys && h->fused && !is_device_ptr(grads);
+  h->lk_done_valid = false;
+  cudaStream_t caller = st;
   if (n && !is_device_ptr(grads)) {
     if (!h->stage_rows) CUDA_TRY(h, (dalloc(h, &h->stage_rows, (size_t)h->n_max * h->D)));
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -807,6 +834,10 @@ static het_status_t update_impl(het_cache* h, const int64_t* keys, uint32_t n, c
       CUDA_TRY(h, cudaStreamWaitEvent(h->copy, h->ev_rows_free, 0));
       CUDA_TRY(h, cudaMemcpyAsync(h->stage_rows, grads, (size_t)n * h->D * 4, cudaMemcpyHostToDevice, h->copy));
       CUDA_TRY(h, cudaEventRecord(h->ev_rows_ready, h->copy));
+      if (beside) {
+        st = h->ustream;
+        CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_lk_done, 0));
+      }
       CUDA_TRY(h, cudaStreamWaitEvent(st, h->ev_rows_ready, 0));
       staged = true;
     } else {
@@ -830,6 +861,10 @@ static het_status_t update_impl(het_cache* h, const int64_t* keys, uint32_t n, c
     if (rc) return fail(h, rc, "evict failed");
   }
   if (staged) CUDA_TRY(h, cudaEventRecord(h->ev_rows_free, st));   // the staging buffer is read by now
+  if (st != caller) {   // the caller's stream continues after this update
+    CUDA_TRY(h, cudaEventRecord(h->ev_upd_done, st));
+    CUDA_TRY(h, cudaStreamWaitEvent(caller, h->ev_upd_done, 0));
+  }
   CUDA_TRY(h, cudaGetLastError());
   h->have_lookup = false;
   return HET_OK;
@@ -859,6 +894,7 @@ het_status_t het_group_update(const het_cache_t* hs, uint32_t N, const int64_t* 
 
 // ---------------------------------------------------------------- evict
 static het_status_t evict_keys_pre(het_cache* h, const int64_t* keys, uint32_t n, cudaStream_t st) {
+  h->lk_done_valid = false;
   if (n > h->n_max) return fail(h, HET_ERR_CAPACITY, "n exceeds max_keys_per_call");
   het_status_t rc = stage_keys(h, keys, n, st);
   if (rc) return rc;
@@ -1019,6 +1055,7 @@ het_status_t het_sync(het_cache_t h, het_stream_t stream_) {
   NvtxRange nvtx_("het_sync");
   if (!h) return HET_ERR_ARG;
   if (h->group) return fail(h, HET_ERR_PROTOCOL, "loopback workers are driven by het_group_sync");
+  h->lk_done_valid = false;
   het_cache* one[1] = {h};
   return sync_members(Members{one, 1}, (cudaStream_t)stream_);
 }
@@ -1295,6 +1332,9 @@ het_status_t het_cache_destroy(het_cache_t h) {
   if (h->copy) cudaStreamDestroy(h->copy);
   if (h->ev_rows_free) cudaEventDestroy(h->ev_rows_free);
   if (h->ev_rows_ready) cudaEventDestroy(h->ev_rows_ready);
+  if (h->ustream) cudaStreamDestroy(h->ustream);
+  if (h->ev_lk_done) cudaEventDestroy(h->ev_lk_done);
+  if (h->ev_upd_done) cudaEventDestroy(h->ev_upd_done);
   for (void* q : h->allocs) cudaFree(q);
   for (ProfRec& r : h->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);

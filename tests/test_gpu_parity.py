@@ -366,6 +366,36 @@ def test_host_pointer_path():
     g.sync()
 
 
+def test_host_pointer_path_update_beside_copy():
+    """Host rows out, host gradients in, no synchronisation between the calls:
+    the update runs on the library's stream beside the lookup's D2H of the
+    rows (after the lookup's kernels) and the caller's stream waits for it.
+    Rows, statistics and the flushed table equal the oracle's."""
+    het = _het()
+    R, D = 1000, 64
+    o = Oracle(R=R, D=D, C=capacity(0.1, R), s=10)
+    g = het.HetCache(R, D, 0.1, 10, max_keys_per_call=4096)
+    for t in range(40):
+        keys = torch.from_numpy(toy_keys(t)).pin_memory()
+        grads = torch.from_numpy(gen.grads(0, t, keys.numel(), D).numpy()).pin_memory()
+        out = torch.zeros((keys.numel(), D), dtype=torch.float32).pin_memory()
+        het.het_lookup(g.h, keys, keys.numel(), t, out)
+        het.het_update(g.h, keys, keys.numel(), grads, LR)
+        torch.cuda.synchronize()
+        assert_rows(out.numpy(), o.lookup(t, [keys.numpy()])[0])
+        o.update([grads.numpy()], LR)
+    gs, os_ = g.stats(), o.stats(0)
+    for k in ["lookups", "keys", "unique", "hits", "exp1", "misses", "evictions", "dirty_pushes"]:
+        assert gs[k] == os_[k], (k, gs[k], os_[k])
+    g.sync()
+    o.flush()
+    rows = np.arange(R, dtype=np.int64)
+    gr, gcg = g.read_global(rows)
+    orows, ocg = o.read_global(rows)
+    assert np.array_equal(gcg, ocg)
+    np.testing.assert_allclose(gr, orows, rtol=1e-6, atol=1e-30)
+
+
 @pytest.mark.parametrize("policy", [LFU, LRU])
 def test_cuda_graph_replay_parity(policy):
     """A step captured into a CUDA graph (HET_CLOCK_AUTO: t = 0, 1, 2, ...)
