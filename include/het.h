@@ -20,7 +20,11 @@
  *
  * Streams: all device work is enqueued on `stream` (a cudaStream_t); calls
  * return without host synchronisation except het_sync, het_stats, the debug
- * exports and (N > 1) the count exchanges of the all-to-alls.
+ * exports and (N > 1) the count exchanges of the all-to-alls.  One exception
+ * in where, not when: het_update with host gradients right after a
+ * het_lookup with host rows out (N = 1) runs its kernels on a library stream
+ * that waits for the lookup's kernels only (so they overlap the rows' D2H),
+ * and `stream` waits for them: the call still completes on `stream`.
  *
  * Errors: argument/shape/protocol errors are returned synchronously and leave
  * the cache untouched.  Errors detected on the device (a key outside
