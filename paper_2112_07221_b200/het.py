@@ -105,8 +105,16 @@ def load():
     return lib
 
 
+_Tensor = None   # torch.Tensor once torch is imported (argument fast path)
+_raw_stream = None   # torch's current raw CUDA stream of the current device
+
+
 def _ptr(x):
     """Device or host address of a torch tensor / numpy array / int / None."""
+    if _Tensor is not None and type(x) is _Tensor:   # the common case first (the e2e leg: per call)
+        if not x.is_contiguous():
+            raise ValueError("tensor arguments must be contiguous")
+        return x.data_ptr()
     if x is None:
         return None
     if isinstance(x, int):
@@ -121,11 +129,19 @@ def _ptr(x):
 
 
 def _stream(stream):
+    global _Tensor, _raw_stream
     if stream is None:
-        import torch
-        if torch.cuda.is_available():
-            return torch.cuda.current_stream().cuda_stream
-        return None
+        if _raw_stream is None:
+            import torch
+            if not torch.cuda.is_available():
+                return None
+            _Tensor = torch.Tensor
+            get_raw, get_dev = getattr(torch._C, "_cuda_getCurrentRawStream", None), getattr(torch._C, "_cuda_getDevice", None)
+            if get_raw is not None and get_dev is not None:
+                _raw_stream = lambda: get_raw(get_dev())   # noqa: E731  (~10x cheaper than current_stream())
+            else:
+                _raw_stream = lambda: torch.cuda.current_stream().cuda_stream   # noqa: E731
+        return _raw_stream()
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
