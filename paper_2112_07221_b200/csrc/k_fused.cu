@@ -106,6 +106,7 @@ __device__ __forceinline__ int block_scan_int(int x, int* warp_sums, int* tot) {
 }
 
 // ------------------------------------------------------------------ K_dd
+template <int RBE = 4>
 __device__ __forceinline__ void evict_listed(const Dev& s, const EvBuf& b, const P2P* pp, int eb, int neb);
 
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
@@ -274,7 +275,7 @@ k_dd_fused(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, ui
            P2P pm, int push, int ndd, int compact) {
   pdl_trigger();
   if ((int)blockIdx.x >= ndd) {
-    evict_listed(s, eb, push ? &pm : nullptr, blockIdx.x - ndd, gridDim.x - ndd);
+    evict_listed<8>(s, eb, push ? &pm : nullptr, blockIdx.x - ndd, gridDim.x - ndd);
     return;
   }
   extern __shared__ __align__(16) uint64_t comp[];
@@ -901,6 +902,7 @@ k_lookup_wide(Dev s, Call c, float* __restrict__ out, int G) {
 // vi: the victim's export index; fpos: the free-stack slot its entry goes to
 // (the caller reserved [ftop, ftop + victims) once: no per-victim atomics on
 // the shared cursors; tombstones are counted per block in *s_tomb)
+template <int RBE = 4>   // float4 columns per lane in flight in the push (wide rows)
 __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_t e, int64_t key, uint64_t slot,
                                             int lane, int* dpop, unsigned* s_dirty, unsigned* s_ev,
                                             unsigned* s_tomb, int vi, int64_t fpos, const P2P* push = nullptr) {
@@ -912,12 +914,12 @@ __device__ __forceinline__ void evict_entry(const Dev& s, const EvBuf& b, int32_
   } else if (dirty) {
     float4* Wr = reinterpret_cast<float4*>(s.W + key * s.D);
     const float4* pr = reinterpret_cast<const float4*>(s.p + (int64_t)e * s.D);
-    for (int d0 = lane; d0 < D4; d0 += 32 * 4) {   // 4 columns per lane in flight (wide rows)
-      float4 w[4], x[4];
+    for (int d0 = lane; d0 < D4; d0 += 32 * RBE) {   // RBE columns per lane in flight (wide rows)
+      float4 w[RBE], x[RBE];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) if (d0 + 32 * b < D4) { w[b] = Wr[d0 + 32 * b]; x[b] = pr[d0 + 32 * b]; }
+      for (int b = 0; b < RBE; ++b) if (d0 + 32 * b < D4) { w[b] = Wr[d0 + 32 * b]; x[b] = pr[d0 + 32 * b]; }
 #pragma unroll
-      for (int b = 0; b < 4; ++b) if (d0 + 32 * b < D4) Wr[d0 + 32 * b] = f4add_(w[b], x[b]);
+      for (int b = 0; b < RBE; ++b) if (d0 + 32 * b < D4) Wr[d0 + 32 * b] = f4add_(w[b], x[b]);
     }
   }
   if (lane == 0) {
@@ -1513,6 +1515,7 @@ __device__ __forceinline__ void make_plan(const Dev& s, bool abort, Plan* pl) {
 // c_g = max; N > 1: PUSH record to the owner's inbox), delete, free into
 // fstack[ev_ftop0 + i].  Called by the first kernel of the call
 // after the update (no other kernel touches the cache in between).
+template <int RBE>
 __device__ __forceinline__ void evict_listed(const Dev& s, const EvBuf& b, const P2P* pp, int eb, int neb) {
   __shared__ int dpop[LFU_CB_MAX];
   __shared__ unsigned s_dirty, s_ev, s_tomb;
@@ -1531,7 +1534,7 @@ __device__ __forceinline__ void evict_listed(const Dev& s, const EvBuf& b, const
     const int64_t key = __ldcg(&b.vsel[i]);
     uint64_t slot = 0;
     const int32_t e = warp_find_slot(s, key, lane, &slot);
-    if (e >= 0) evict_entry(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev, &s_tomb, i, ftop0 + i, pp);
+    if (e >= 0) evict_entry<RBE>(s, b, e, key, slot, lane, dpop, &s_dirty, &s_ev, &s_tomb, i, ftop0 + i, pp);
     else if (lane == 0) raise_err(ctl, 3 /*HET_ERR_PROTOCOL: a listed victim is not resident*/);
   }
   TL_MAX(12);
@@ -1551,7 +1554,7 @@ __device__ __forceinline__ void evict_listed(const Dev& s, const EvBuf& b, const
 
 // the deferred eviction as its own kernel (before calls that do not start with k_dd_fused)
 __global__ void __launch_bounds__(256) k_evict_pending(Dev s, EvBuf b, P2P pm, int push) {
-  evict_listed(s, b, push ? &pm : nullptr, blockIdx.x, gridDim.x);
+  evict_listed<8>(s, b, push ? &pm : nullptr, blockIdx.x, gridDim.x);
 }
 
 // Update (Alg. 3): block 0 plans this step's eviction (need, mode, LFU
@@ -1844,7 +1847,7 @@ k_dd_bucket(const int64_t* __restrict__ keys, int n, int pbits, Dev s, Call c, u
 __global__ void __launch_bounds__(256) k_begin_evict(Dev s, Call c, int n, uint64_t t, EvBuf eb, P2P pm, int push) {
   pdl_trigger();
   if (blockIdx.x > 0) {
-    evict_listed(s, eb, push ? &pm : nullptr, blockIdx.x - 1, gridDim.x - 1);
+    evict_listed<8>(s, eb, push ? &pm : nullptr, blockIdx.x - 1, gridDim.x - 1);
     return;
   }
   if (threadIdx.x == 0) dd_begin(s, c, n, t, 1, *c.pref_bad, 0);
