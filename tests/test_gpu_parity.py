@@ -537,8 +537,11 @@ def test_reddit_shaped_all_unique(fused, monkeypatch):
 @pytest.mark.parametrize("D,B,T", [(4096, 32, 8), (4096, 128, 16), (1024, 128, 24)])
 def test_scale_shaped_wide_rows(D, B, T):
     """BASELINE configs[4] row shape (D=4096, 16 KB rows) on a scaled table:
-    Criteo-shaped keys over 20,000 rows.  Wide rows run with several warps per
-    key (k_lookup_wide) and 512-column slices in the update (segreduce_slice)."""
+    Criteo-shaped keys over 20,000 rows.  Wide rows run the decisions kernel
+    (k_lookup_wide), the per-(position, slice) row moves (k_mv_as) and the
+    per-thread cp.async segment reduce (k_seg_as) before the clock-only update;
+    the flushed global table (c_g of every row, the tracked rows' values)
+    equals the oracle's."""
     R = 20000
     cards = gen.scaled_cards(R)
     p = Pair(R, D, 0.1, 100, LFU, n_max=4096, track_div=16)
@@ -555,6 +558,14 @@ def test_scale_shaped_wide_rows(D, B, T):
         p.g.update(kd, torch.from_numpy(grads).cuda(), LR)
         p.o.update([grads], LR)
     p.compare_stats()
+    p.g.sync()
+    p.o.flush()
+    rows = np.arange(R, dtype=np.int64)
+    gr, gcg = p.g.read_global(rows)
+    orows, ocg = p.o.read_global(rows)
+    assert np.array_equal(gcg, ocg)
+    sel = _tracked_mask(rows, 16)
+    assert_rows(gr[sel], orows[sel])
 
 
 @pytest.mark.parametrize("B", [128, 400])   # n = 3,328 (multi-CTA rank dedup) and 10,400 (bucket dedup)
