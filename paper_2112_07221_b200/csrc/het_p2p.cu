@@ -181,29 +181,40 @@ __global__ void k_p2p_link(Dev s, P2P m) {
 
 // ---------------------------------------------------------------- owner: apply + respond
 // Warp per linked row (warp-strided): apply the row's records in source order
-// and write the responses into the requesters' inboxes.
+// and write the responses into the requesters' inboxes.  Wide rows: PG warps
+// per row (a group inside one block), each walking the row's list and taking
+// the same decisions, each moving its 1/PG of the columns; the group's first
+// writes c_g, the response headers and the byte counters.  The lists' heads
+// are reset after the phase (reset_heads), not by the walk.
 __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigned long long* sb) {
   __shared__ int32_t wbuf[32][32];   // per warp: the row's record ids, sorted
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nl = s.ctl->abort ? 0 : *m.nlead;
   const int D4 = s.D >> 2;
+  const int PG = wide_rows(s.D) ? 4 : 1;   // divides the 8 or 32 warps of a block
+  const int nw = ((gridDim.x * blockDim.x) >> 5) / PG;
+  const int gw0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int gw = gw0 / PG, sub = gw0 % PG;
+  const bool lead = sub == 0;
+  const int c0 = sub * (D4 / PG), c1 = c0 + D4 / PG;   // this warp's float4 columns
+  const int nl = s.ctl->abort ? 0 : *m.nlead;
   const Rec* base = reqrec(m, m.rank, 0);
   for (int li = gw; li < nl; li += nw) {
     const int64_t row = m.leaders[li];
     // the row's server row and c_g do not depend on the list: load them first
     uint32_t g0 = 0;
     if (lane == 0) g0 = s.cg[row];
-    const float4 wpre = lane < D4 ? reinterpret_cast<const float4*>(s.W + row * s.D)[lane]
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);   // the first 128 columns
+    const float4 wpre = c0 + lane < c1 ? reinterpret_cast<const float4*>(s.W + row * s.D)[c0 + lane]
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);   // this warp's first 32 float4
+    if (PG > 1) {   // every warp of the group has read c_g before the group's first may write it
+      g0 = __shfl_sync(0xffffffffu, g0, 0);
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + wi / PG), "r"(PG * 32) : "memory");
+    }
     // walk the row's list once (lane 0), sort by id = (source rank, pushes
     // before requests) across the lanes, hand record i to lane i
     int cnt = 0;
     if (lane == 0) {
       int32_t cur = m.head[row];
       while (cur >= 0 && cnt < 32) { wbuf[wi][cnt++] = cur; cur = m.next[cur]; }
-      m.head[row] = -1;
     }
     __syncwarp();
     cnt = __shfl_sync(0xffffffffu, cnt, 0);
@@ -244,9 +255,9 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
       for (int o = 16; o; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
       g = max(g, x);
     }
-    if (lane == 0) s.cg[row] = g;
+    if (lane == 0 && lead) s.cg[row] = g;
     // byte counters: pushes received, requests received / answered
-    if (have) {
+    if (have && lead) {
       if (push) atomicAdd(&sb[3], 16ull + 4ull * s.D);
       else {
         atomicAdd(&sb[(r.kind & 3) == K_NEEDQ ? 1 : 3], 16ull);
@@ -258,19 +269,21 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
     float* rec_l = nullptr;
     if (req) {
       rec_l = resprec(m, src, m.rank, j - m.qpush[src]);
-      reinterpret_cast<uint32_t*>(rec_l)[0] = g;
-      reinterpret_cast<uint32_t*>(rec_l)[1] = valid ? 1u : 0u;
+      if (lead) {
+        reinterpret_cast<uint32_t*>(rec_l)[0] = g;
+        reinterpret_cast<uint32_t*>(rec_l)[1] = valid ? 1u : 0u;
+      }
     }
     PTL(13);
     // row data, lane per float4, records in sorted order: pushes, then sync pushes
     const unsigned needrow = (pushm | syncm);
     const unsigned answer = __ballot_sync(0xffffffffu, req && !valid);
     float4* Wr = reinterpret_cast<float4*>(s.W + row * s.D);
-    for (int d0 = lane; d0 - lane < D4; d0 += 32 * RB) {   // RB columns per lane per pass (wide rows)
+    for (int d0 = c0 + lane; d0 - lane < c1; d0 += 32 * RB) {   // RB columns per lane per pass (wide rows)
       float4 w[RB];
 #pragma unroll
       for (int b = 0; b < RB; ++b)
-        w[b] = (d0 == lane && b == 0) ? wpre : (d0 + 32 * b < D4 ? Wr[d0 + 32 * b] : make_float4(0.f, 0.f, 0.f, 0.f));
+        w[b] = (d0 == c0 + lane && b == 0) ? wpre : (d0 + 32 * b < c1 ? Wr[d0 + 32 * b] : make_float4(0.f, 0.f, 0.f, 0.f));
       for (int pass = 0; pass < 2; ++pass) {
         unsigned mm = pass == 0 ? pushm : syncm;
         while (mm) {
@@ -281,14 +294,14 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
           const float4* rr = reinterpret_cast<const float4*>(reqrow(m, m.rank, si, ji));
           float4 x[RB];
 #pragma unroll
-          for (int b = 0; b < RB; ++b) if (d0 + 32 * b < D4) x[b] = rr[d0 + 32 * b];
+          for (int b = 0; b < RB; ++b) if (d0 + 32 * b < c1) x[b] = rr[d0 + 32 * b];
 #pragma unroll
-          for (int b = 0; b < RB; ++b) if (d0 + 32 * b < D4) w[b] = f4add_p(w[b], x[b]);
+          for (int b = 0; b < RB; ++b) if (d0 + 32 * b < c1) w[b] = f4add_p(w[b], x[b]);
         }
       }
       if (needrow) {
 #pragma unroll
-        for (int b = 0; b < RB; ++b) if (d0 + 32 * b < D4) Wr[d0 + 32 * b] = w[b];
+        for (int b = 0; b < RB; ++b) if (d0 + 32 * b < c1) Wr[d0 + 32 * b] = w[b];
       }
       unsigned am = answer;
       while (am) {
@@ -297,12 +310,18 @@ __device__ __forceinline__ void process_rows(const Dev& s, const P2P& m, unsigne
         float* rec = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(rec_l), i));
 #pragma unroll
         for (int b = 0; b < RB; ++b)
-          if (d0 + 32 * b < D4) reinterpret_cast<float4*>(rec + 4)[d0 + 32 * b] = w[b];
+          if (d0 + 32 * b < c1) reinterpret_cast<float4*>(rec + 4)[d0 + 32 * b] = w[b];
       }
     }
     PTL(14);
     __syncwarp();
   }
+}
+
+// the row lists of this round's leaders, emptied for the next round's link
+// (after every warp of the phase walked them); thread-strided over the grid
+__device__ __forceinline__ void reset_heads(const P2P& m, int nl) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += gridDim.x * blockDim.x) m.head[m.leaders[i]] = -1;
 }
 
 __global__ void k_p2p_process(Dev s, P2P m) {
@@ -320,6 +339,9 @@ __global__ void k_p2p_process(Dev s, P2P m) {
     __threadfence_system();
     st_release(&respflag(m, threadIdx.x)[m.rank].epoch, ep);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < *m.nlead; i += blockDim.x) m.head[m.leaders[i]] = -1;   // every block has walked
+  __syncthreads();
   if (threadIdx.x == 0) { *m.nlead = 0; m.done[1] = 0; }
   PTL(8);
 }
@@ -850,12 +872,14 @@ k_exchange(Dev s, Call c, P2P m, float* __restrict__ out) {
   grid.sync();
   // ---- owner: apply + respond
   PTL(6);
+  const int nlr = *m.nlead;   // this round's leaders (block 0 zeroes the counter after the next grid sync)
   process_rows(s, m, sb);
   PTL(7);
   __syncthreads();
   bytes_flush(s, sb);
   __threadfence();
   grid.sync();
+  reset_heads(m, nlr);   // every warp has walked its rows' lists
   if (blockIdx.x == 0) {
     if (threadIdx.x < m.N) {
       __threadfence_system();
