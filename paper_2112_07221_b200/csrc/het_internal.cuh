@@ -541,7 +541,10 @@ constexpr int RMODE_MAX = 16384;   // rmode dedups serve n <= this
 int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st, void* prof = nullptr);
 // N > 1, wide rows, rmode: the Get scatter out[perm[r]] = v[entry of r's key] of every sorted
 // position r after the exchange round installed the rows (k_mv_as, scatter-only)
-int launch_scatter_wide(const Dev& s, const Call& c, float* out, cudaStream_t st);
+// resp: this worker's response records (REC floats each: 16 B header + the row), indexed by uslot;
+// the rows refetched this round come from there, and their head position also writes v
+int launch_scatter_wide(const Dev& s, const Call& c, float* out, cudaStream_t st, const float* resp, int64_t rec,
+                        const int32_t* uslot);
 // SMs left free by the cooperative kernels for NCCL's blocks at N > 1
 // (= NCCL's maxCTAs and the peer-memory dense all-reduce grid; env HET_NCCL_CTAS, default 16)
 int coop_sm_reserve();

@@ -752,8 +752,9 @@ __device__ __forceinline__ void install_gather_key(const Dev& s, const Call& c, 
         }
       }
       if (ok) {
-        warp_copy_row(reinterpret_cast<float4*>(s.v + (int64_t)e * s.D), reinterpret_cast<const float4*>(rec + 4),
-                      D4, lane);
+        if (!(c.rmode && wide_rows(s.D)))   // wide rows: launch_scatter_wide copies the response row
+          warp_copy_row(reinterpret_cast<float4*>(s.v + (int64_t)e * s.D), reinterpret_cast<const float4*>(rec + 4),
+                        D4, lane);
         if (lane == 0) { s.cs[e] = g; s.cc[e] = g; }
         write_urec(c, u, e, j0, cnt, false, g, pos_lane, lane);   // fetched: clean, c_c = c_g
       }
@@ -1300,7 +1301,7 @@ int p2p_lookup_phase(P2PState* p, const Dev& d, const Call& c, float* out, int p
     case RP_PROCESS: k_p2p_process<<<148 * 2, 256, 0, st>>>(d, v); return 1;
     default:
       k_install_gather<<<blocks, 256, 0, st>>>(d, c, v, out);
-      return 1 + (c.rmode && wide_rows(d.D) ? launch_scatter_wide(d, c, out, st) : 0);
+      return 1 + (c.rmode && wide_rows(d.D) ? launch_scatter_wide(d, c, out, st, reinterpret_cast<const float*>(p->inbox + v.off_resp), v.REC, v.uslot) : 0);
   }
 }
 
@@ -1324,7 +1325,7 @@ int p2p_round_fused(P2PState* p, const Dev& d, const Call& c, float* out, cudaSt
     cfg.attrs = at;
     cfg.numAttrs = 2;
     if (cudaLaunchKernelEx(&cfg, k_exchange, d, c, v, out) == cudaSuccess)
-      return 1 + (c.rmode && wide_rows(d.D) ? launch_scatter_wide(d, c, out, st) : 0);
+      return 1 + (c.rmode && wide_rows(d.D) ? launch_scatter_wide(d, c, out, st, reinterpret_cast<const float*>(p->inbox + v.off_resp), v.REC, v.uslot) : 0);
     cudaGetLastError();   // fall through to the split round
   }
   int l = 0;

@@ -1107,6 +1107,7 @@ struct AsWalk {
   int64_t ikey;
   int hd, ihd;   // MV: bit 0 the key's head, bits 1..: the output row (lane's / item's)
   bool scat = false;   // MV: scatter only (N > 1: the rows are installed)
+  const int32_t* uslot = nullptr;   // scat: each key's response slot (owner * CAPS + slot)
 
   __device__ __forceinline__ void load(const Call& c, int lane) {
     for (;;) {
@@ -1121,9 +1122,14 @@ struct AsWalk {
         if (MV) {   // sorted position u: its output row perm[u] and its key's head inverse[perm[u]]
           const int p = __ldcg(&c.perm[u]);
           const int h = __ldcg(&c.inverse[p]);
-          if (scat) {   // scatter only: every position of a key with an entry copies v[e] to its row
+          if (scat) {   // scatter only: every position of a key with an entry copies its row to out
             rec = __ldcg(&c.urec[h]);
             fl = rec.x >= 0 ? 4 : 0;
+            const uint8_t st = __ldcg(&c.status[h]);
+            if (fl && (st == ST_MISS || st == ST_EXP1 || st == ST_EXP2)) {   // refetched this round:
+              fl |= 8;                                                        // the row is in its response
+              key = __ldcg(&uslot[h]);
+            }
             hd = (h == u ? 1 : 0) | (p << 1);
           } else {
           fl = __ldcg(&c.ucnt[h]);
@@ -1293,7 +1299,9 @@ __global__ void __launch_bounds__(AS_T) k_seg_as(Dev s, Call c, const float* __r
 // under the Evict push W += p, whose key is moved whole by its
 // head (p[e] staged too, W[key] = v[e] = W + p, then every occurrence).
 template <int RING, int F>
-__global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict__ out, int scat) {
+__global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict__ out, int scat,
+                                                const float* __restrict__ resp, int64_t rec,
+                                                const int32_t* __restrict__ uslot) {
   extern __shared__ __align__(16) float4 ring[];
   const uint32_t sbase = smem_u32(ring) + threadIdx.x * 16;
   pdl_wait();
@@ -1309,6 +1317,7 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
   float4* o4 = reinterpret_cast<float4*>(out);
   AsWalk<true, 1> iw, cw;
   iw.scat = cw.scat = scat != 0;
+  iw.uslot = cw.uslot = uslot;
   iw.init(c, U, Q, (int)blockIdx.x / S, lane);
   cw.init(c, U, Q, (int)blockIdx.x / S, lane);
   int inflight = 0, used = 0, head = 0, tail = 0;
@@ -1316,7 +1325,9 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
     while (iw.valid && inflight < AS_QMAX) {
       const int rows = iw.rows();
       if (used + rows > RING) break;
-      const float4* src = (iw.flag & 1) ? W4 + iw.ikey * D4 : v4 + (int64_t)iw.e * D4;
+      const float4* src = (iw.flag & 8)   ? reinterpret_cast<const float4*>(resp + iw.ikey * rec + 4)
+                          : (iw.flag & 1) ? W4 + iw.ikey * D4
+                                          : v4 + (int64_t)iw.e * D4;
       const uint32_t d0 = sbase + head * (F * AS_T * 16), d1 = sbase + ring_at<RING>(head + 1) * (F * AS_T * 16);
 #pragma unroll
       for (int j = 0; j < F; ++j) {
@@ -1338,7 +1349,7 @@ __global__ void __launch_bounds__(AS_T) k_mv_as(Dev s, Call c, float* __restrict
     for (int j = 0; j < F; ++j) {
       w[j] = r0[j * AS_T];
       if (cw.flag & 2) w[j] = f4add_(w[j], r1[j * AS_T]);
-      if (head && (cw.flag & 1)) v4[(int64_t)cw.e * D4 + col4 + j * AS_T] = w[j];
+      if (head && (cw.flag & 9)) v4[(int64_t)cw.e * D4 + col4 + j * AS_T] = w[j];   // Fetch: v = the row
       if (cw.flag & 2) W4[cw.ikey * D4 + col4 + j * AS_T] = w[j];
     }
     if (cw.flag & 2) {   // push (the head's item): every occurrence
@@ -2012,7 +2023,8 @@ int launch_lookup_fused(const Dev& s, const Call& c, float* out, cudaStream_t st
       if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
       const int S = D4 / (AS_T * AS_MV[1]);
       pr = prof_begin(prof, "lookup_mv", st);
-      launch_pdl(kern, std::max(1, sms * AS_MV[2] / S) * S, AS_T, smem, st, pdl_mode() >= 1, false, s, c, out, 0);
+      launch_pdl(kern, std::max(1, sms * AS_MV[2] / S) * S, AS_T, smem, st, pdl_mode() >= 1, false, s, c, out, 0,
+                 (const float*)nullptr, (int64_t)0, (const int32_t*)nullptr);
       prof_end(prof, pr, st);
       return 2;
     }
@@ -2045,7 +2057,8 @@ int coop_sm_reserve() {
 // coop_sm_reserve() SMs free at N > 1 and the staging depends on D
 struct UpdCfg { int dev; bool multi; uint32_t D; int blocks; size_t smem; int stage_rows; };
 
-int launch_scatter_wide(const Dev& s, const Call& c, float* out, cudaStream_t st) {
+int launch_scatter_wide(const Dev& s, const Call& c, float* out, cudaStream_t st, const float* resp, int64_t rec,
+                        const int32_t* uslot) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2054,7 +2067,7 @@ int launch_scatter_wide(const Dev& s, const Call& c, float* out, cudaStream_t st
   auto kern = k_mv_as<AS_MV[0], AS_MV[1]>;
   if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); attr = true; }
   const int S = (int)(s.D / 4) / (AS_T * AS_MV[1]);
-  kern<<<std::max(1, sms * AS_MV[2] / S) * S, AS_T, smem, st>>>(s, c, out, 1);
+  kern<<<std::max(1, sms * AS_MV[2] / S) * S, AS_T, smem, st>>>(s, c, out, 1, resp, rec, uslot);
   return 1;
 }
 
