@@ -1954,7 +1954,9 @@ int launch_dd_fused(const Dev& s, const Call& c, int n, int pbits, uint64_t t, i
   P2P pm{};
   int push = 0;
   if (p2pview) { pm = *reinterpret_cast<const P2P*>(p2pview); push = 1; }
-  k_dd_fused<<<ndd + (evict ? EV_BLOCKS : 0), DDF_THREADS, (size_t)std::max(n, 1) * 8, st>>>(
+  // wide rows: twice the eviction blocks (a warp per victim row of up to 16 KB)
+  const int evb = evict ? (wide_rows(s.D) ? 2 * EV_BLOCKS : EV_BLOCKS) : 0;
+  k_dd_fused<<<ndd + evb, DDF_THREADS, (size_t)std::max(n, 1) * 8, st>>>(
       c.keys, n, pbits, s, c, t, lookup, *reinterpret_cast<EvBuf*>(evbuf), pm, push, ndd, compact);
   return 1;
 }
